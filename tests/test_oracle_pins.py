@@ -1,0 +1,317 @@
+"""Pins for the oracle (CPU only): each part of oracle/cold_oracle.c is checked against
+something other than itself — the paper's closed forms, the hand-computed worked
+example (tests/golden/), hash known answers, torch fp64 library routines, brute
+force and the independent pure-Python twin oracle/mini.py.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import coldgen
+import oracle
+from oracle import mini
+from tests.fixtures import bag_schema, load_golden, small_case, worked_example
+
+
+# ---- P-1 linear_log (Eq. eq:log) --------------------------------
+
+def test_linear_log_closed_forms():
+    for x, want in load_golden("linear_log_values.json")["points"]:
+        assert oracle.linear_log(x) == pytest.approx(want, rel=1e-14, abs=1e-15)
+
+
+def test_linear_log_odd_monotone_c1():
+    xs = np.concatenate([-np.logspace(-6, 30, 400), np.linspace(-3, 3, 601), np.logspace(-6, 30, 400)])
+    xs.sort()
+    ys = np.array([oracle.linear_log(x) for x in xs])
+    assert np.all(np.diff(ys) >= 0) and np.all(np.diff(ys)[np.diff(xs) > 0] > 0)   # strictly increasing
+    for x in xs:
+        assert oracle.linear_log(-x) == -oracle.linear_log(x)                      # odd
+    assert max(abs(y) for y in ys) <= 71.0                                         # range compression
+    eps = 1e-6                                                                     # C^1 at |x| = 1
+    for c in (1.0, -1.0):
+        left = (oracle.linear_log(c) - oracle.linear_log(c - eps)) / eps
+        right = (oracle.linear_log(c + eps) - oracle.linear_log(c)) / eps
+        assert abs(left - right) <= 2 * eps
+
+
+# ---- P-2 sigma --------------------------------------------------------
+
+def test_sigmoid():
+    assert oracle.sigmoid(0.0) == 0.5
+    assert oracle.sigmoid(40.0) >= 1 - 1e-15
+    for z in np.linspace(-50, 50, 201):
+        assert oracle.sigmoid(-z) == pytest.approx(1 - oracle.sigmoid(z), abs=3e-16)
+        assert oracle.sigmoid(z) == pytest.approx(mini.sigmoid(z), rel=1e-15)
+    assert oracle.sigmoid(-800.0) == 0.0 and oracle.sigmoid(800.0) == 1.0
+
+
+# ---- P-3 cross-feature hash (AMB-9) ----------------------------------------------------
+
+def test_cross_hash_known_answers():
+    kat = load_golden("cross_hash_kat.json")
+    for k, v in kat["fmix64"]:
+        assert oracle.fmix64(k) == int(v, 16)
+    for g, x, y, card, want in kat["cross_row"]:
+        assert oracle.cross_row(g, x, y, card) == want
+        assert mini.cross_row(g, x, y, card) == want
+
+
+def test_cross_hash_properties():
+    rng = np.random.default_rng(5)
+    xs = rng.integers(0, 2**31 - 1, 100000)
+    ys = rng.integers(0, 2**31 - 1, 100000)
+    counts = np.zeros(1000, np.int64)
+    for x, y in zip(xs[:100000], ys[:100000]):
+        counts[oracle.cross_row(3, int(x), int(y), 1000)] += 1
+    assert counts.max() <= 3 * counts.mean()
+    for x, y in zip(xs[:200], ys[:200]):
+        assert oracle.cross_row(9, int(x), int(y), 1) == 0    # cardinality 1 -> row 0
+        r = oracle.cross_row(9, int(x), int(y), 12345)
+        assert 0 <= r < 12345 and r == oracle.cross_row(9, int(x), int(y), 12345)
+
+
+# ---- P-4 worked example ----------------------------------------------------------------
+
+@pytest.mark.parametrize("head", ["one", "two"])
+def test_worked_example(head):
+    schema, params, batch, exp = worked_example(head)
+    m = oracle.Model(schema, params)
+    p, z = oracle.score(m, batch)
+    if head == "one":
+        assert p[0] == pytest.approx(exp["adA_p_one_wide"], abs=1e-14)
+        assert p[1] == pytest.approx(exp["adB_p_one_wide"], abs=1e-14)
+        assert z[0] == pytest.approx(exp["adA_z_one_wide"], abs=1e-14)
+        assert z[1] == pytest.approx(exp["adB_z_one_wide"], abs=1e-14)
+        idx, _ = oracle.topk(p, 1)
+        assert idx[0] == exp["top1_one_wide"]
+        p_off, _ = oracle.score(oracle.Model(schema, params, linear_log=False), batch)
+        assert p_off[0] == pytest.approx(exp["adA_p_one_wide_ll_off"], abs=1e-14)
+        assert p_off[1] == pytest.approx(exp["adB_p_one_wide_ll_off"], abs=1e-14)
+    else:
+        assert p[0] == pytest.approx(exp["adA_p_two_wide"], abs=1e-14)
+        assert p[1] == pytest.approx(exp["adB_p_two_wide"], abs=1e-14)
+        idx, _ = oracle.topk(p, 1)
+        assert idx[0] == exp["top1_two_wide"]
+
+
+def test_worked_example_features():
+    """ê (after LL) and s for ad A: x = [s_g * ê_g]."""
+    schema, params, batch, exp = worked_example("one")
+    m = oracle.Model(schema, params)
+    x = oracle.features(m, batch)[0]
+    eh = np.asarray(exp["adA_features_ll_on"])
+    s = np.repeat(exp["adA_se_ll_on"], 2)
+    np.testing.assert_allclose(x, s * eh, rtol=1e-14, atol=1e-15)
+
+
+# ---- P-6 reduction to library routines (torch fp64) ---------------------------------
+
+def test_reduces_to_torch_embedding_bag_mlp():
+    """LL off and SE pinned to s = 1 (w = 0, b = +40): the model is
+    MLP(concat(embedding_bag_sum)). Rows for cross groups come from the pinned twin hash."""
+    torch = pytest.importorskip("torch")
+    import torch.nn.functional as F
+    sch, params, batch = small_case("tiny", R=3, n_ads=(6, 11, 2), precision="f32", se="identity")
+    m = oracle.Model(sch, params, linear_log=False)
+    p, z = oracle.score(m, batch)
+    feats = []
+    for g, grp in enumerate(sch.groups):
+        bags = []
+        for r in range(batch.R):
+            for a in range(batch.ad_offsets[r], batch.ad_offsets[r + 1]):
+                bags.append(mini.rows(sch, batch, g, r, a))
+        flat = torch.tensor([x for b in bags for x in b], dtype=torch.long)
+        offs = torch.tensor(np.cumsum([0] + [len(b) for b in bags[:-1]]), dtype=torch.long)
+        T = torch.tensor(params.table_f64(g))
+        feats.append(F.embedding_bag(flat, T, offs, mode="sum"))
+    h = torch.cat(feats, 1)
+    L = len(params.fc_w)
+    for l in range(L):
+        h = F.linear(h, torch.tensor(params.fc_w[l], dtype=torch.float64), torch.tensor(params.fc_b[l], dtype=torch.float64))
+        if l < L - 1:
+            h = F.relu(h)
+    zt = h[:, 0] if h.shape[1] == 1 else h[:, 1] - h[:, 0]
+    np.testing.assert_allclose(z, zt.numpy(), rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(p, torch.sigmoid(zt).numpy(), rtol=1e-12, atol=1e-14)
+
+
+def test_zero_fcn_scores_sigma_of_bias():
+    sch, params, batch = small_case("tiny", R=2, n_ads=(9, 4), init="zero")
+    p, _ = oracle.score(oracle.Model(sch, params), batch)
+    np.testing.assert_allclose(p, mini.sigmoid(float(params.fc_b[-1][-1])), rtol=1e-15)
+
+
+# ---- P-12 the two oracles agree --------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["tiny_f32", "tiny_f16_zipf", "paper_bf16", "bags", "bags_2req_empty"])
+def test_c_oracle_matches_python_twin(case):
+    if case == "tiny_f32":
+        sch, params, batch = small_case("tiny", R=2, n_ads=(7, 5))
+    elif case == "tiny_f16_zipf":
+        sch, params, batch = small_case("tiny", R=2, n_ads=(3, 9), precision="f16", dist="zipf")
+    elif case == "paper_bf16":
+        sch, params, batch = small_case("paper", R=1, n_ads=(4,), precision="bf16", cap=5000)
+    else:
+        sch = bag_schema()
+        params = coldgen.make_params(sch, seed=3, precision="f32")
+        batch = coldgen.make_batch(sch, 3, [4, 0, 6] if case == "bags_2req_empty" else [5, 3, 6], seed=11)
+    for sel in (None, [0, 2, 4, 5, 6] if sch.M >= 7 else None):
+        d_in = (len(sel) if sel else sch.M) * sch.k
+        if d_in != params.fc_w[0].shape[1]:
+            params = coldgen.make_params(sch, seed=3, precision=params.precision, d_in=d_in,
+                                         table_dtype=params.table_dtype)
+        p, z = oracle.score(oracle.Model(sch, params, selected=sel), batch)
+        pm, zm = mini.score(sch, params, batch, selected=sel)
+        np.testing.assert_allclose(p, pm, rtol=1e-14, atol=1e-15)
+        np.testing.assert_allclose(z, zm, rtol=1e-13, atol=1e-14)
+
+
+def test_rows_match_twin_and_definition():
+    sch = bag_schema()
+    params = coldgen.make_params(sch, seed=3, precision="f32")
+    batch = coldgen.make_batch(sch, 3, [5, 3, 6], seed=12)
+    m = oracle.Model(sch, params)
+    for r in range(batch.R):
+        for a in range(batch.ad_offsets[r], batch.ad_offsets[r + 1]):
+            for g in range(sch.M):
+                got = oracle.rows(m, batch, g, a).tolist()
+                assert got == mini.rows(sch, batch, g, r, a)
+            # cross g=4 is the x-major product of user bag x ad bag: count = |x| * |y|
+            ub = batch.ids[1][batch.offs[1][r]:batch.offs[1][r + 1]]
+            ab = batch.ids[3][batch.offs[3][a]:batch.offs[3][a + 1]]
+            assert len(oracle.rows(m, batch, 4, a)) == len(ub) * len(ab)
+            assert oracle.rows(m, batch, 6, a).tolist() == [0] * len(ub)    # card 1
+
+
+# ---- invariants ------------------------------------------------------------------------
+
+def test_permuting_ads_permutes_scores():
+    sch, params, batch = small_case("tiny", R=1, n_ads=(23,))
+    p, _ = oracle.score(oracle.Model(sch, params), batch)
+    perm = np.random.default_rng(0).permutation(23)
+    b2 = coldgen.Batch(batch.R, batch.ad_offsets, [None if v is None else (v[perm] if batch.offs[g] is None else v)
+                                                   for g, v in enumerate(batch.ids)], batch.offs, None, batch.req_ids)
+    p2, _ = oracle.score(oracle.Model(sch, params), b2)
+    np.testing.assert_array_equal(p2, p[perm])
+
+
+def test_request_independence_and_sampling():
+    """Scores of a request do not depend on the other requests in the batch,
+    and scoring a sample of ads equals scoring all of them."""
+    sch, params, batch = small_case("tiny", R=4, n_ads=(5, 8, 3, 6))
+    m = oracle.Model(sch, params)
+    p, _ = oracle.score(m, batch)
+    for r in range(batch.R):
+        sb = coldgen.sub_batch(batch, [r])
+        pr, _ = oracle.score(m, sb)
+        np.testing.assert_array_equal(pr, p[batch.ad_offsets[r]:batch.ad_offsets[r + 1]])
+    ads = np.array([21, 0, 7, 13, 13])
+    ps, _ = oracle.score(m, batch, ad_list=ads)
+    np.testing.assert_array_equal(ps, p[ads])
+
+
+def test_row_order_equals_column_order():
+    """column-based computation reorders work, not results."""
+    sch = bag_schema()
+    params = coldgen.make_params(sch, seed=4, precision="f32")
+    batch = coldgen.make_batch(sch, 3, [5, 2, 7], seed=13)
+    m = oracle.Model(sch, params)
+    np.testing.assert_array_equal(oracle.features(m, batch, order=0), oracle.features(m, batch, order=1))
+
+
+def test_user_broadcast_equals_per_pair():
+    """Hoisting the user side is exact: user-group features are identical for all ads of a
+    request, and equal those of a one-ad request of the same user."""
+    sch, params, batch = small_case("tiny", R=2, n_ads=(6, 4))
+    m = oracle.Model(sch, params)
+    x = oracle.features(m, batch)
+    k = sch.k
+    ucols = np.concatenate([np.arange(g * k, (g + 1) * k) for g in sch.side_indices(coldgen.USER)])
+    for r in range(batch.R):
+        blk = x[batch.ad_offsets[r]:batch.ad_offsets[r + 1]][:, ucols]
+        assert np.all(blk == blk[0])
+
+
+def test_se_weights_in_unit_interval():
+    sch, params, batch = small_case("tiny", R=1, n_ads=(30,))
+    m = oracle.Model(sch, params)
+    x = oracle.features(m, batch)
+    xe = oracle.features(oracle.Model(sch, coldgen.make_params(sch, seed=7, precision="f32", se="identity")), batch)
+    k = sch.k
+    for g in range(sch.M):
+        cols = slice(g * k, (g + 1) * k)
+        nz = np.abs(xe[:, cols]) > 1e-12
+        s = x[:, cols][nz] / xe[:, cols][nz]
+        assert np.all((s > 0) & (s < 1))
+
+
+def test_dense_se_block_diagonal_equals_per_group():
+    """AMB-1: Doc B's dense SE with a block-diagonal W is Doc A's per-group SE."""
+    sch, params, batch = small_case("tiny", R=2, n_ads=(4, 5))
+    M, k = sch.M, sch.k
+    Wd = np.zeros((M, M * k))
+    for g in range(M):
+        Wd[g, g * k:(g + 1) * k] = params.se_w[g]
+    p1, _ = oracle.score(oracle.Model(sch, params), batch)
+    p2, _ = oracle.score(oracle.Model(sch, params, se_dense=(Wd, params.se_b.astype(np.float64))), batch)
+    np.testing.assert_allclose(p1, p2, rtol=1e-15)
+
+
+def test_ll_order_variants_agree_when_gate_is_one():
+    sch, params, batch = small_case("tiny", R=1, n_ads=(9,), se="identity")
+    a = oracle.features(oracle.Model(sch, params), batch)
+    b = oracle.features(oracle.Model(sch, params, ll_after_se=True), batch)
+    np.testing.assert_allclose(a, b, rtol=1e-15)
+
+
+def test_pooled_f32_mode():
+    """fp32-ordered gather: single ids are exact copies; pooled sums equal a sequential
+    float32 sum over the twin's rows in bag order."""
+    sch = bag_schema()
+    params = coldgen.make_params(sch, seed=4, precision="f32")
+    batch = coldgen.make_batch(sch, 2, [5, 4], seed=14)
+    m = oracle.Model(sch, params)
+    got = oracle.pooled_f32(m, batch)
+    for r in range(batch.R):
+        for a in range(batch.ad_offsets[r], batch.ad_offsets[r + 1]):
+            for g in range(sch.M):
+                acc = np.zeros(sch.k, np.float32)
+                for row in mini.rows(sch, batch, g, r, a):
+                    acc = (acc + params.tables[g][row]).astype(np.float32)
+                np.testing.assert_array_equal(got[a, g], acc)
+
+
+def test_id_out_of_range_raises():
+    sch, params, batch = small_case("tiny", R=1, n_ads=(4,))
+    batch.ids[3][2] = sch.groups[3].card
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.score(oracle.Model(sch, params), batch)
+    assert e.value.code == oracle.ORC_ERR_ID_RANGE
+
+
+# ---- top-K ---------------------------------------------------------------------
+
+def test_topk_brute_force_ties_nan():
+    rng = np.random.default_rng(1)
+    for n in (1, 2, 7, 100, 1000):
+        keys = np.round(rng.random(n), 2)                 # many ties
+        keys[rng.random(n) < 0.05] = np.nan
+        for K in sorted({1, max(1, n // 3), n}):
+            idx, kv = oracle.topk(keys, K)
+            want = mini.topk(list(keys), K)
+            assert idx.tolist() == want
+            assert all((math.isnan(a) and math.isnan(b)) or a == b for a, b in zip(kv, keys[want]))
+    with pytest.raises(oracle.OracleError):
+        oracle.topk(np.zeros(5), 6)
+    with pytest.raises(oracle.OracleError):
+        oracle.topk(np.zeros(5), 0)
+
+
+def test_ecpm_key():
+    """eCPM = pCTR * bid (PAPER.md L155 footnote, L332) reorders the top-K."""
+    p = np.array([0.5, 0.1, 0.3])
+    bid = np.array([1.0, 10.0, 1.0])
+    assert oracle.topk(p, 1)[0][0] == 0
+    assert oracle.topk(p * bid, 1)[0][0] == 1
