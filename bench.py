@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""bench.py — candidate ads scored/sec (and p99 request latency) of the COLD scoring pass on B200.
+
+Workload (BASELINE.json configs[4], per GPU): a stream of 8192 requests x 10,000 candidate ads,
+S-paper schema (8 user + 8 ad + 8 cross groups, k=16, D_in=384), FC 384x1024x512x256x128x64x2,
+fp16 storage + fp32 accumulation, linear_log on, SE gate on every group, top-K=500 per request.
+One step = score every ad of the rank's requests (cold_score_batch) + per-request top-K
+(cold_topk) + NCCL all-gather of the top-K lists (N>1). Requests are partitioned across ranks
+(weak scaling: every rank owns its own 8192-request block of the stream). Inputs (2.6 GB of ids +
+4.8 GB of tables per GPU) are far larger than L2, so no L2 flush is needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W]            # our CUDA path
+  python bench.py --impl reference [--steps K --warmup W]    # the fp64 oracle on the host cores
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import coldgen  # noqa: E402
+
+METRIC = "candidate ads scored/sec and p99 request latency at N ads/request, 1/2/4/8 B200"
+PAPER_FLOP_LAYERS = None
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="f16", choices=["f16", "bf16", "f32"])
+    ap.add_argument("--requests", type=int, default=8192, help="requests per GPU per step")
+    ap.add_argument("--ads", type=int, default=10000, help="ads per request")
+    ap.add_argument("--topk", type=int, default=500)
+    ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--cap", type=int, default=0, help="cap cardinalities (quick runs only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-latency", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--latency-requests", type=int, default=1000)
+    ap.add_argument("--seed", type=int, default=1234)
+    return ap.parse_args()
+
+
+def schema_for(args):
+    sch = coldgen.schema_paper()
+    if args.cap:
+        sch = coldgen.scaled_schema(sch, args.cap)
+    return sch
+
+
+def fc_flops_per_ad(sch, d_ac):
+    dims = [d_ac] + list(sch.widths)
+    return [2 * dims[i] * dims[i + 1] for i in range(len(sch.widths))]
+
+
+def gather_bytes_per_ad(sch, elem):
+    """Algorithmic HBM bytes per ad of the ad+cross gather kernel: gathered rows,
+    ad ids, the request index of the ad, and the X_ac write."""
+    k = sch.k
+    rows, id_bytes = 0, 0
+    for g in sch.groups:
+        if g.side == coldgen.AD:
+            id_bytes += 4
+            rows += 1 if not g.pooled else (g.bag[0] + g.bag[1]) / 2
+        elif g.side == coldgen.CROSS:
+            u = sch.groups[g.user_ref]
+            lu = 1 if not u.pooled else (u.bag[0] + u.bag[1]) / 2
+            a = sch.groups[g.ad_ref]
+            la = 1 if not a.pooled else (a.bag[0] + a.bag[1]) / 2
+            rows += lu * la
+    n_ac = len([g for g in sch.groups if g.side != coldgen.USER])
+    return rows * k * elem + id_bytes + 4 + n_ac * k * elem, rows
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+        "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_id):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu_id), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_ctx_params(ctx, params):
+    tables = params.tables
+    tdt = params.table_dtype
+    if tdt == "f16":
+        tables = [t.view(np.uint16) for t in tables]
+    ctx.load_params(tables, params.se_w, params.se_b, params.fc_w, params.fc_b, table_dtype=tdt)
+
+
+# --------------------------------------------------------------------------------------------
+def cpu_oracle_sample(sch, params, batch, target_s=15.0, max_ads=None):
+    """Time the fp64 oracle (as it stands) on a bounded prefix of request 0's ads."""
+    import oracle
+    model = oracle.Model(sch, params)
+    cores = os.cpu_count() or 1
+    n0 = min(256, batch.n_ads)
+    t = time.perf_counter()
+    oracle.score(model, batch, ad_list=np.arange(n0), nthreads=cores)
+    t0 = time.perf_counter() - t
+    n = int(min(max_ads or batch.n_ads, max(n0, n0 * target_s / max(t0, 1e-6))))
+    t = time.perf_counter()
+    oracle.score(model, batch, ad_list=np.arange(n), nthreads=cores)
+    dt = time.perf_counter() - t
+    return {"value": n / dt, "unit": "ads/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n} ads of the workload's request stream (fp64 C oracle, OpenMP over ads, "
+                      f"{dt:.1f} s)"}
+
+
+def run_reference(args):
+    """--impl reference: the fp64 oracle on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    sch = schema_for(args)
+    params = coldgen.make_params(sch, seed=args.seed, precision=args.precision)
+    batch = coldgen.make_batch(sch, range(0, 2), args.ads, seed=args.seed + 1)
+    model = oracle.Model(sch, params)
+    cores = os.cpu_count() or 1
+    # size one step to ~3 s of oracle work
+    t = time.perf_counter()
+    oracle.score(model, batch, ad_list=np.arange(128), nthreads=cores)
+    per_ad = (time.perf_counter() - t) / 128
+    n = int(min(batch.n_ads, max(128, 3.0 / max(per_ad, 1e-9))))
+    ads = np.arange(n)
+    for _ in range(args.warmup):
+        oracle.score(model, batch, ad_list=ads, nthreads=cores)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.score(model, batch, ad_list=ads, nthreads=cores)
+    dt = time.perf_counter() - t
+    v = n * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "ads/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": config_dict(args, sch),
+        "cpu_baseline": {"value": v, "unit": "ads/s", "cores": cores, "kind": "oracle",
+                         "sample": f"each step = {n} ads of request 0 of the workload stream"},
+        "e2e": {"value": v, "unit": "ads/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, sch):
+    return {"workload": f"BASELINE configs[4] per GPU: {args.requests} requests x {args.ads} ads "
+                        f"(S-paper schema {sch.name}, M={sch.M}, k={sch.k}, FC {sch.M * sch.k}x"
+                        + "x".join(map(str, sch.widths)) + f", {args.precision} + linear_log, top-K={args.topk})",
+            "requests_per_gpu": args.requests, "ads_per_request": args.ads, "top_k": args.topk,
+            "ids": "uniform", "l2": "inputs larger than L2 (ids 2.6 GB + tables 4.8 GB per GPU); no flush",
+            "parallelism": f"request partition x{args.gpus}, replicated params"}
+
+
+# --------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+    from paper_2007_16122_b200 import Batch, Context
+    from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER, PROF_KINDS, PROF_TOPK, PROF_USER
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    sch = schema_for(args)
+    t_setup = time.perf_counter()
+    params = coldgen.make_params(sch, seed=args.seed, precision=args.precision)
+    r0 = rank * args.requests
+    batch = coldgen.make_batch(sch, range(r0, r0 + args.requests), args.ads, seed=args.seed + 1)
+    N = batch.n_ads
+    ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, device=local, max_ads=N,
+                  max_requests=args.requests, chunk_ads=args.chunk)
+    load_ctx_params(ctx, params)
+    db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs)
+    K = args.topk
+    scores = torch.empty(N, dtype=torch.float32, device=dev)
+    idx = torch.empty(args.requests * K, dtype=torch.int32, device=dev)
+    key = torch.empty(args.requests * K, dtype=torch.float32, device=dev)
+    g_idx = torch.empty(world * args.requests * K, dtype=torch.int32, device=dev) if world > 1 else None
+    g_key = torch.empty(world * args.requests * K, dtype=torch.float32, device=dev) if world > 1 else None
+    stream = torch.cuda.current_stream()
+    setup_s = time.perf_counter() - t_setup
+
+    def step(b, out_idx, out_key):
+        ctx.score_batch(b, scores)
+        ctx.topk(scores, db.ad_offsets, batch.ad_offsets, K, out_idx, out_key)
+        if world > 1:
+            dist.all_gather_into_tensor(g_idx, idx)
+            dist.all_gather_into_tensor(g_key, key)
+
+    def timed(b, out_idx, out_key, steps, sampler=None, profile=False):
+        for _ in range(args.warmup):
+            step(b, out_idx, out_key)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        if profile:
+            ctx.profile(True)
+        if sampler:
+            sampler.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step(b, out_idx, out_key)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        clocks = sampler.stop() if sampler else None
+        prof = None
+        if profile:
+            prof = ctx.profile_read()
+            ctx.profile(False)
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, clocks, prof
+
+    gpu_id = local
+    try:
+        gpu_id = "GPU-" + str(torch.cuda.get_device_properties(local).uuid)
+    except Exception:
+        pass
+    sampler = ClockSampler(gpu_id)
+    ms, clocks, prof = timed(db, idx, key, args.steps, sampler=sampler, profile=True)
+    ms_step = ms / args.steps
+    total_ads = N * world * args.steps
+    value = total_ads / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (FC2, the largest layer: 54.7% of FLOPs) ----
+    peaks, peak_src = measured_peaks()
+    prof_ms, prof_n = prof
+    info = ctx.info()
+    d_ac = info["d_ad"]
+    layer_flops = fc_flops_per_ad(sch, d_ac)
+    per_kernel = {}
+    names = {PROF_USER: "user", PROF_GATHER: "gather", PROF_TOPK: "topk"}
+    n_gemm = len(sch.widths) - 1
+    for l in range(n_gemm):
+        names[PROF_FC + l] = f"fc{l + 1}" + ("+head" if l == n_gemm - 1 else "")
+    step_kernel_ms = float(prof_ms.sum())
+    for kind, name in names.items():
+        if prof_n[kind]:
+            per_kernel[name] = {"launches": int(prof_n[kind]), "avg_us": float(prof_ms[kind] / prof_n[kind] * 1e3),
+                                "share": float(prof_ms[kind] / step_kernel_ms)}
+    for l in range(n_gemm):
+        kind = PROF_FC + l
+        if prof_n[kind]:
+            fl = N * args.steps * (layer_flops[l] + (layer_flops[l + 1] if l == n_gemm - 1 else 0))
+            per_kernel[names[kind]]["tflops"] = fl / (prof_ms[kind] / 1e3) / 1e12
+    gb_per_ad, rows_per_ad = gather_bytes_per_ad(sch, 2 if args.precision != "f32" else 4)
+    if prof_n[PROF_GATHER]:
+        per_kernel["gather"]["gbs"] = N * args.steps * gb_per_ad / (prof_ms[PROF_GATHER] / 1e3) / 1e9
+    dom = PROF_FC + 1 if n_gemm >= 2 else PROF_FC
+    peak_tf = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
+    achieved = per_kernel[names[dom]]["tflops"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("fc2_dram_bytes_per_launch")
+    roofline = {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": peak_tf,
+                "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
+                "peak_source": f"bf16_tflops_sustained {peak_src} (fp16 runs at the bf16 rate; kernel timed "
+                               f"inside a long step)",
+                "algorithmic": f"2*{layer_flops[dom - PROF_FC] // 2} FLOP/ad x ads per launch"}
+    roofline_gather = None
+    if prof_n[PROF_GATHER]:
+        hb = float(peaks["hbm_gbs"])
+        ga = per_kernel["gather"]["gbs"]
+        roofline_gather = {"bound": "hbm", "kernel": "gather", "achieved": ga, "peak": hb, "unit": "GB/s",
+                           "frac": ga / hb, "traffic": None,
+                           "algorithmic": f"{gb_per_ad:.0f} B/ad ({rows_per_ad:.0f} rows x {sch.k} x 2 B + ids "
+                                          f"+ X_ac write)"}
+    fc_total_ms = sum(prof_ms[PROF_FC + l] for l in range(n_gemm))
+    fc_flops_all = N * args.steps * sum(layer_flops)
+    fc_stack = {"tflops": fc_flops_all / (fc_total_ms / 1e3) / 1e12,
+                "frac": fc_flops_all / (fc_total_ms / 1e3) / 1e12 / peak_tf}
+    gpu_launches = int(prof_n.sum())
+
+    # ---- e2e: host (pinned) inputs through the C ABI, top-K back to host, every step ----
+    e2e = None
+    if not args.no_e2e:
+        hb = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs, pin=True)
+        h_idx = torch.empty(args.requests * K, dtype=torch.int32).pin_memory()
+        h_key = torch.empty(args.requests * K, dtype=torch.float32).pin_memory()
+
+        def e2e_step(b, oi, ok):
+            ctx.score_batch(hb, scores)
+            ctx.topk(scores, db.ad_offsets, batch.ad_offsets, K, h_idx, h_key)
+            if world > 1:
+                dist.all_gather_into_tensor(g_idx, idx)
+                dist.all_gather_into_tensor(g_key, key)
+
+        # same procedure as `timed`
+        for _ in range(args.warmup):
+            e2e_step(hb, h_idx, h_key)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step(hb, h_idx, h_key)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        ms_e = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms_e], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_e = float(t.item())
+        h2d = sum(int(x.nbytes) for x in batch.ids if x is not None) + \
+            sum(int(x.nbytes) for x in batch.offs if x is not None) + int(batch.ad_offsets.nbytes)
+        d2h = args.requests * K * 8
+        e2e = {"value": total_ads / (ms_e / 1e3), "unit": "ads/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e / args.steps}
+
+    # ---- p50 / p99 request latency at configs[1] (1 user x 4000 ads), device-timed ----
+    latency = None
+    if not args.no_latency and rank == 0:
+        nl = args.latency_requests
+        lb = coldgen.make_batch(sch, range(10**7, 10**7 + nl), 4000, seed=args.seed + 1)
+        singles = [Batch.from_numpy(s.ad_offsets, s.ids, s.offs) for s in
+                   (coldgen.sub_batch(lb, [i]) for i in range(nl))]
+        lscores = torch.empty(4000, dtype=torch.float32, device=dev)
+        lidx = torch.empty(K, dtype=torch.int32, device=dev)
+        lkey = torch.empty(K, dtype=torch.float32, device=dev)
+        ao = np.asarray([0, 4000], np.int32)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
+        for i in range(min(10, nl)):
+            ctx.score_request(singles[i], lscores)
+            ctx.topk(lscores, singles[i].ad_offsets, ao, K, lidx, lkey)
+        torch.cuda.synchronize()
+        for i in range(nl):
+            evs[i][0].record(stream)
+            ctx.score_request(singles[i], lscores)
+            ctx.topk(lscores, singles[i].ad_offsets, ao, K, lidx, lkey)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        lat = np.array([a.elapsed_time(b) for a, b in evs])
+        latency = {"n_ads": 4000, "requests": nl, "p50_ms": float(np.percentile(lat, 50)),
+                   "p99_ms": float(np.percentile(lat, 99)), "mean_ms": float(lat.mean()),
+                   "timing": "device events per request (score + top-500), requests back to back on one stream"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_oracle_sample(sch, params, batch)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "ads/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": args.precision, "data": "synthetic (seeded ids, tables, weights)",
+            "config": config_dict(args, sch),
+            "roofline": roofline, "roofline_gather": roofline_gather, "fc_stack": fc_stack,
+            "kernels": per_kernel, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "clocks": clocks, "latency": latency, "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/* include/cold.h — C ABI of the B200-native COLD pre-ranking scorer.
+ *
+ * COLD (arXiv 2007.16122, "COLD: Towards the Next Generation of Pre-Ranking System").
+ * Citations: "P:n" = PAPER.md line n, with the section or equation it falls in.
+ *
+ * One request is one user against N candidate ads (§2: the pre-ranking stage
+ * scores ~10^4 candidates and passes the top N on). For every ad the library computes
+ *   1. rows of every selected feature group: user / ad ids, and user x ad cross
+ *      features (§3.3 "computes cross-features"; construction = DESIGN.md AMB-9);
+ *   2. e_g = sum-pooled embedding of the rows ("sum-pooling");
+ *   3. ê_g = linear_log(e_g) elementwise (P:278-287 Eq. eq:log; "in the first layer");
+ *   4. s_g = sigmoid(w_g . ê_g + b_g), v_g = s_g ê_g (SE gate, P:11-14 Doc A / P:229-235
+ *      §3.2; per-group reading AMB-1);
+ *   5. x = concat of v_g over the selected groups in schema order ("D_in");
+ *   6. the FC stack D_in x 1024 x 512 x 256 x 128 x 64 x 2 (§4.1) with ReLU
+ *      (AMB-6) between layers;
+ *   7. p = sigmoid(z1 - z0) for a 2-wide head, sigmoid(z) for a 1-wide head (AMB-7);
+ * and cold_topk selects the K best ads per request by p (or eCPM = p * bid, P:155
+ * footnote / P:332), ties by ascending position, NaN last (AMB-13).
+ *
+ * User-side groups are computed once per request and broadcast over its ads; their
+ * contribution to FC1 (W1[:, user] x_u + b1) is computed once per request (exact:
+ * FC1 is linear and, with the per-group SE, v_u does not depend on the ad).
+ *
+ * Conventions for every entry point:
+ *  - Returns cold_status; never throws, never aborts. On an argument / shape error
+ *    nothing is launched and outputs are untouched. cold_last_error() gives a
+ *    thread-local detail message for the last failing call.
+ *  - Launches are asynchronous on the given stream (cudaStream_t passed as void*;
+ *    NULL = legacy default stream) unless stated otherwise. Asynchronous CUDA faults
+ *    surface as COLD_ERR_CUDA on a later call.
+ *  - A cold_ctx is externally synchronised (like a cuBLAS handle): one thread / stream
+ *    at a time.
+ *  - "device or host" pointers: the library inspects each pointer
+ *    (cudaPointerGetAttributes). A batch whose id arrays are host memory (pinned
+ *    recommended) is staged to the device by the library chunk by chunk on an internal
+ *    copy stream, overlapped with compute; all arrays of one batch must then be host.
+ */
+#ifndef COLD_H
+#define COLD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cold_ctx cold_ctx;   /* opaque: device parameters + workspace + streams */
+
+typedef enum {
+  COLD_OK = 0,
+  COLD_ERR_INVALID_ARG = 1,   /* NULL pointer, bad enum, non-monotone offsets, empty request */
+  COLD_ERR_SHAPE = 2,         /* widths chain / selection / group refs inconsistent */
+  COLD_ERR_ID_RANGE = 3,      /* an id outside [0, cardinality) (only with COLD_VALIDATE_IDS) */
+  COLD_ERR_K_RANGE = 4,       /* K < 1 or K > ads of some request */
+  COLD_ERR_NOT_LOADED = 5,    /* scoring before cold_load_params */
+  COLD_ERR_PARAMS = 6,        /* parameter arrays missing or wrong dtype */
+  COLD_ERR_OOM = 7,           /* device allocation failed */
+  COLD_ERR_CUDA = 8,          /* a CUDA runtime / driver call failed */
+  COLD_ERR_UNSUPPORTED = 9,   /* a configuration this build has no kernel for */
+  COLD_ERR_CAPACITY = 10      /* more requests / ads in one call than the ctx was created for */
+} cold_status;
+
+enum { COLD_USER = 0, COLD_AD = 1, COLD_CROSS = 2 };          /* feature-group side */
+enum { COLD_FP32 = 0, COLD_FP16 = 1, COLD_BF16 = 2 };         /* compute / storage precision */
+enum { COLD_RELU = 0 };                                        /* hidden activation (AMB-6) */
+
+/* config.flags */
+#define COLD_VALIDATE_IDS 1u   /* check every id against its cardinality (one D2H sync per call);
+                                  without it out-of-range ids are clamped to card-1 */
+
+/* A feature group ("the embedding of the i-th feature group e_i"). */
+typedef struct {
+  int32_t side;          /* COLD_USER / COLD_AD / COLD_CROSS */
+  int32_t pooled;        /* AD groups: 1 = multi-valued bag (CSR offsets), 0 = one id per ad.
+                            USER groups are always CSR (a single-valued group has bags of 1).
+                            CROSS: ignored (rows = user bag x ad bag, x-major). */
+  int64_t cardinality;   /* table rows, >= 1 */
+  int32_t user_ref;      /* CROSS: schema index of a USER group */
+  int32_t ad_ref;        /* CROSS: schema index of an AD group */
+} cold_group;
+
+typedef struct {
+  int32_t num_groups;            /* M, 1..64 */
+  const cold_group* groups;      /* [M], schema order */
+  int32_t emb_dim;               /* k, uniform over groups (16); one of 2, 4, 8, 16, 32 */
+  int32_t num_selected;          /* groups fed to the network; 0 = all */
+  const int32_t* selected;       /* [num_selected] schema indices, strictly ascending */
+  int32_t num_layers;            /* L >= 1 */
+  const int32_t* widths;         /* [L] FC output widths; input of layer 0 = D_in = k * #selected;
+                                    last width in {1, 2}. Tensor-core path (FP16/BF16): L >= 2,
+                                    hidden widths multiples of 64, last hidden width <= 256. */
+  int32_t activation;            /* COLD_RELU */
+  int32_t linear_log;            /* 1 = apply linear_log to every pooled group embedding */
+  int32_t precision;             /* COLD_FP32 (SIMT FFMA, no TF32), COLD_FP16, COLD_BF16 (tcgen05) */
+  int32_t device;                /* CUDA device ordinal */
+  int64_t max_ads_per_call;      /* capacity: ads summed over the requests of one call */
+  int32_t max_requests_per_call; /* capacity: requests in one call */
+  int32_t chunk_ads;             /* ads per pipeline chunk (0 = library default) */
+  uint32_t flags;                /* COLD_VALIDATE_IDS */
+} cold_config;
+
+/* Model parameters. All pointers are HOST memory; cold_load_params copies them
+ * synchronously, so the caller may free them on return. */
+typedef struct {
+  int32_t table_dtype;           /* dtype of `tables`: COLD_FP32 (the library rounds to the compute
+                                    precision, RNE) or equal to config.precision (stored as-is; bf16 /
+                                    fp16 as uint16 bit patterns) */
+  const void* const* tables;     /* [M] each [cardinality x k], row-major */
+  const float* se_w;             /* [M x k]  SE weight w_g (per-group reading AMB-1) */
+  const float* se_b;             /* [M]      SE bias b_g */
+  const float* const* fc_w;      /* [L] each [out_l x in_l], row-major (in_0 = D_in, schema order of
+                                    the selected groups); rounded RNE to the compute precision for the
+                                    tensor-core layers; the per-request user block of W1 stays fp32 */
+  const float* const* fc_b;      /* [L] each [out_l], kept fp32 */
+} cold_params;
+
+/* One call's requests. Column-major per group ("column based computation"). */
+typedef struct {
+  int32_t num_requests;          /* R >= 1 */
+  const int32_t* ad_offsets;     /* [R+1] ads of request r are [ad_offsets[r], ad_offsets[r+1]); device or host */
+  const int32_t* ad_offsets_host;/* [R+1] host copy (sizing and validation without a sync); required */
+  const int32_t* const* ids;     /* host array [M] of pointers: USER -> ids of the CSR bags; AD -> [N_tot]
+                                    (single) or the bag ids; CROSS -> NULL (always computed) */
+  const int32_t* const* offs;    /* host array [M] of pointers: USER -> [R+1]; AD pooled -> [N_tot+1];
+                                    otherwise NULL */
+  const int32_t* const* offs_host;/* host array [M] of host copies of `offs` (NULL entries allowed when
+                                    ids are device memory; required for pooled groups of a host batch) */
+} cold_batch;
+
+typedef struct {
+  uint64_t version;              /* parameter version, +1 per cold_load_params */
+  int32_t d_in, d_user, d_ad;    /* input widths: total, hoisted user part, ad + cross part */
+  int32_t chunk_ads;             /* ads per pipeline chunk */
+  int32_t kernels_per_chunk;     /* kernel launches per chunk */
+  int32_t kernels_per_call;      /* launches per call outside the chunk loop */
+  int32_t tensor_core;           /* 1 if the FC stack runs on tcgen05 */
+  int64_t device_bytes;          /* device memory owned by the ctx */
+} cold_info;
+
+/* Create a context on config->device: validates the schema (AMB-1..AMB-18 readings in
+ * DESIGN.md), allocates the workspace for the stated capacities. */
+cold_status cold_create(const cold_config* config, cold_ctx** out);
+void cold_destroy(cold_ctx* ctx);
+
+/* Upload parameters (synchronous). Replaces any previous version after all work already
+ * queued on the ctx's streams (no call sees a mix of versions). */
+cold_status cold_load_params(cold_ctx* ctx, const cold_params* params, uint64_t* version_out);
+
+/* Score all ads of a batch: scores[N_tot] fp32 (device or host). */
+cold_status cold_score_batch(cold_ctx* ctx, const cold_batch* batch, float* scores, void* stream);
+
+/* Same as cold_score_batch for exactly one request (R == 1), the latency path. */
+cold_status cold_score_request(cold_ctx* ctx, const cold_batch* one, float* scores, void* stream);
+
+/* Per-request top-K: for request r, the K ads with the largest key, key = scores
+ * (pCTR) or scores * bids (eCPM) when bids != NULL, ordered by (key desc, position asc),
+ * NaN last. idx_out[r*K + i] = position of the ad within request r; key_out[r*K + i] = key.
+ * scores / bids / ad_offsets / outputs: device or host. */
+cold_status cold_topk(cold_ctx* ctx, const float* scores, const int32_t* ad_offsets,
+                      const int32_t* ad_offsets_host, int32_t R, int32_t K, const float* bids,
+                      int32_t* idx_out, float* key_out, void* stream);
+
+cold_status cold_get_info(const cold_ctx* ctx, cold_info* out);
+
+/* ---- per-kernel timing (bench) -------------------------------------------------------- */
+
+/* Kernel classes reported by cold_profile_read. */
+enum { COLD_PROF_USER = 0, COLD_PROF_GATHER = 1, COLD_PROF_TOPK = 2, COLD_PROF_FC = 3 /* + layer */,
+       COLD_PROF_KINDS = 3 + 16 };
+
+/* enable = 1: reset counters and record a CUDA event pair around every kernel the library
+ * launches (on the launching stream); enable = 0: stop recording. */
+cold_status cold_profile(cold_ctx* ctx, int32_t enable);
+
+/* Synchronises the recorded events and returns, per kernel class, the summed device time
+ * (ms) and launch count since the last cold_profile(ctx, 1). Arrays of COLD_PROF_KINDS. */
+cold_status cold_profile_read(cold_ctx* ctx, double* total_ms, int64_t* launches);
+
+/* ---- parity hooks (tests) ------------------------------------------------------------ */
+
+/* Raw pooled sums e_g (before linear_log / SE), fp32, summed in bag order (cross: x-major):
+ * out[N_tot][n_sel][k], device memory. */
+cold_status cold_debug_pooled(cold_ctx* ctx, const cold_batch* batch, float* out, void* stream);
+
+/* The network input x = [v_g] as the FC stack consumes it, widened to fp32:
+ * out[N_tot][D_in], device memory (schema order of the selected groups; user groups are the
+ * per-request fp32 values, ad/cross groups the stored fp16/bf16/fp32 values). */
+cold_status cold_debug_features(cold_ctx* ctx, const cold_batch* batch, float* out, void* stream);
+
+/* Rows of group g for every ad: rows_out[N_tot][max_rows] int64, -1 padded, device memory. */
+cold_status cold_debug_rows(cold_ctx* ctx, const cold_batch* batch, int32_t group, int64_t* rows_out,
+                            int32_t max_rows, void* stream);
+
+const char* cold_status_string(cold_status s);
+const char* cold_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COLD_H */

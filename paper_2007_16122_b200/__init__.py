@@ -1,0 +1,6 @@
+"""B200-native COLD online pre-ranking scorer (arXiv 2007.16122).
+
+The product is libcold.so (C ABI in include/cold.h; CUDA kernels for sm_100a in csrc/).
+`cold` is the thin ctypes binding used by the tests and bench.py.
+"""
+from .cold import Batch, ColdError, Context, lib  # noqa: F401

@@ -1,0 +1,261 @@
+"""Thin ctypes binding over libcold.so (include/cold.h). Argument marshalling only: every
+step of the scoring pass runs in the library's CUDA kernels. There is no CPU fallback —
+if libcold.so is missing or no sm_100 device is present, the calls raise.
+
+PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libcold.so")
+
+USER, AD, CROSS = 0, 1, 2
+FP32, FP16, BF16 = 0, 1, 2
+PRECISION = {"f32": FP32, "f16": FP16, "bf16": BF16}
+VALIDATE_IDS = 1
+
+STATUS = {0: "COLD_OK", 1: "COLD_ERR_INVALID_ARG", 2: "COLD_ERR_SHAPE", 3: "COLD_ERR_ID_RANGE",
+          4: "COLD_ERR_K_RANGE", 5: "COLD_ERR_NOT_LOADED", 6: "COLD_ERR_PARAMS", 7: "COLD_ERR_OOM",
+          8: "COLD_ERR_CUDA", 9: "COLD_ERR_UNSUPPORTED", 10: "COLD_ERR_CAPACITY"}
+
+EXPORTS = ["cold_create", "cold_destroy", "cold_load_params", "cold_score_batch", "cold_score_request",
+           "cold_topk", "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
+           "cold_status_string", "cold_last_error", "cold_profile", "cold_profile_read"]
+PROF_KINDS = 3 + 16
+PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC = 0, 1, 2, 3
+
+
+class ColdError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{STATUS.get(status, status)}: {detail}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class cold_group(C.Structure):
+    _fields_ = [("side", C.c_int32), ("pooled", C.c_int32), ("cardinality", C.c_int64),
+                ("user_ref", C.c_int32), ("ad_ref", C.c_int32)]
+
+
+class cold_config(C.Structure):
+    _fields_ = [("num_groups", C.c_int32), ("groups", C.POINTER(cold_group)), ("emb_dim", C.c_int32),
+                ("num_selected", C.c_int32), ("selected", C.POINTER(C.c_int32)),
+                ("num_layers", C.c_int32), ("widths", C.POINTER(C.c_int32)),
+                ("activation", C.c_int32), ("linear_log", C.c_int32), ("precision", C.c_int32),
+                ("device", C.c_int32), ("max_ads_per_call", C.c_int64), ("max_requests_per_call", C.c_int32),
+                ("chunk_ads", C.c_int32), ("flags", C.c_uint32)]
+
+
+class cold_params(C.Structure):
+    _fields_ = [("table_dtype", C.c_int32), ("tables", C.POINTER(C.c_void_p)),
+                ("se_w", C.c_void_p), ("se_b", C.c_void_p),
+                ("fc_w", C.POINTER(C.c_void_p)), ("fc_b", C.POINTER(C.c_void_p))]
+
+
+class cold_batch(C.Structure):
+    _fields_ = [("num_requests", C.c_int32), ("ad_offsets", C.c_void_p), ("ad_offsets_host", C.c_void_p),
+                ("ids", C.POINTER(C.c_void_p)), ("offs", C.POINTER(C.c_void_p)),
+                ("offs_host", C.POINTER(C.c_void_p))]
+
+
+class cold_info(C.Structure):
+    _fields_ = [("version", C.c_uint64), ("d_in", C.c_int32), ("d_user", C.c_int32), ("d_ad", C.c_int32),
+                ("chunk_ads", C.c_int32), ("kernels_per_chunk", C.c_int32), ("kernels_per_call", C.c_int32),
+                ("tensor_core", C.c_int32), ("device_bytes", C.c_int64)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libcold.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} not built (python -m paper_2007_16122_b200.build)")
+        L = C.CDLL(LIB_PATH)
+        L.cold_create.argtypes = [C.POINTER(cold_config), C.POINTER(C.c_void_p)]
+        L.cold_destroy.argtypes = [C.c_void_p]
+        L.cold_destroy.restype = None
+        L.cold_load_params.argtypes = [C.c_void_p, C.POINTER(cold_params), C.POINTER(C.c_uint64)]
+        L.cold_score_batch.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_void_p, C.c_void_p]
+        L.cold_score_request.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_void_p, C.c_void_p]
+        L.cold_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.cold_get_info.argtypes = [C.c_void_p, C.POINTER(cold_info)]
+        L.cold_debug_pooled.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_void_p, C.c_void_p]
+        L.cold_debug_features.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_void_p, C.c_void_p]
+        L.cold_debug_rows.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_int32, C.c_void_p, C.c_int32,
+                                      C.c_void_p]
+        L.cold_profile.argtypes = [C.c_void_p, C.c_int32]
+        L.cold_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.cold_status_string.restype = C.c_char_p
+        L.cold_status_string.argtypes = [C.c_int]
+        L.cold_last_error.restype = C.c_char_p
+        for f in ["cold_create", "cold_load_params", "cold_score_batch", "cold_score_request", "cold_topk",
+                  "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
+                  "cold_profile", "cold_profile_read"]:
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise ColdError(status, lib().cold_last_error().decode())
+
+
+def _addr(x) -> int:
+    """Address of a torch tensor or numpy array (None -> 0)."""
+    if x is None:
+        return 0
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return x.ctypes.data
+
+
+def _stream_handle(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class Batch:
+    """A call's requests (include/cold.h cold_batch). Arrays are torch tensors (device or
+    pinned host) or numpy arrays (host). The object keeps them alive."""
+
+    def __init__(self, ad_offsets, ids: Sequence, offs: Sequence, ad_offsets_host: Optional[np.ndarray] = None,
+                 offs_host: Optional[Sequence] = None):
+        self.ad_offsets = ad_offsets
+        self.ids, self.offs = list(ids), list(offs)
+        if ad_offsets_host is None:
+            ad_offsets_host = ad_offsets.cpu().numpy() if hasattr(ad_offsets, "cpu") else ad_offsets
+        self.ad_offsets_host = np.ascontiguousarray(ad_offsets_host, dtype=np.int32)
+        M = len(self.ids)
+        if offs_host is None:
+            offs_host = [None if o is None else (o.cpu().numpy() if hasattr(o, "is_cuda") and o.is_cuda else
+                                                 (o.numpy() if hasattr(o, "numpy") and not isinstance(o, np.ndarray) else o))
+                         for o in self.offs]
+        self.offs_host = [None if o is None else np.ascontiguousarray(o, dtype=np.int32) for o in offs_host]
+        self._ids = (C.c_void_p * M)(*[_addr(x) for x in self.ids])
+        self._offs = (C.c_void_p * M)(*[_addr(x) for x in self.offs])
+        self._offs_host = (C.c_void_p * M)(*[_addr(x) for x in self.offs_host])
+        self.R = len(self.ad_offsets_host) - 1
+        self.n_ads = int(self.ad_offsets_host[-1])
+        self.c = cold_batch(self.R, _addr(self.ad_offsets), self.ad_offsets_host.ctypes.data,
+                            C.cast(self._ids, C.POINTER(C.c_void_p)), C.cast(self._offs, C.POINTER(C.c_void_p)),
+                            C.cast(self._offs_host, C.POINTER(C.c_void_p)))
+
+    @staticmethod
+    def from_numpy(ad_offsets, ids, offs, device="cuda", pin: bool = False):
+        """Device batch (pin=False) or pinned-host batch (pin=True) from host numpy arrays."""
+        import torch
+
+        def conv(a):
+            if a is None:
+                return None
+            t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32))
+            return t.pin_memory() if pin else t.to(device)
+        return Batch(conv(ad_offsets), [conv(x) for x in ids], [conv(x) for x in offs],
+                     ad_offsets_host=np.asarray(ad_offsets, np.int32),
+                     offs_host=[None if o is None else np.asarray(o, np.int32) for o in offs])
+
+
+class Context:
+    """A cold_ctx: schema, FC widths, precision, capacities."""
+
+    def __init__(self, groups, emb_dim: int, widths: Sequence[int], precision: str = "f16",
+                 selected: Optional[Sequence[int]] = None, linear_log: bool = True, device: int = 0,
+                 max_ads: int = 1 << 20, max_requests: int = 1024, chunk_ads: int = 0, validate_ids: bool = False):
+        L = lib()
+        M = len(groups)
+        self._groups = (cold_group * M)()
+        for i, g in enumerate(groups):
+            self._groups[i] = cold_group(int(g.side), int(bool(getattr(g, "pooled", False))), int(g.card),
+                                         int(getattr(g, "user_ref", -1)), int(getattr(g, "ad_ref", -1)))
+        self._sel = np.asarray(list(selected) if selected else [], np.int32)
+        self._widths = np.asarray(list(widths), np.int32)
+        cfg = cold_config()
+        cfg.num_groups, cfg.groups, cfg.emb_dim = M, self._groups, emb_dim
+        cfg.num_selected = len(self._sel)
+        cfg.selected = self._sel.ctypes.data_as(C.POINTER(C.c_int32)) if len(self._sel) else None
+        cfg.num_layers, cfg.widths = len(self._widths), self._widths.ctypes.data_as(C.POINTER(C.c_int32))
+        cfg.activation, cfg.linear_log = 0, int(linear_log)
+        cfg.precision, cfg.device = PRECISION[precision], device
+        cfg.max_ads_per_call, cfg.max_requests_per_call = max_ads, max_requests
+        cfg.chunk_ads, cfg.flags = chunk_ads, VALIDATE_IDS if validate_ids else 0
+        self.precision = precision
+        self.device = device
+        self.ctx = C.c_void_p()
+        _check(L.cold_create(C.byref(cfg), C.byref(self.ctx)))
+
+    def close(self):
+        if self.ctx:
+            lib().cold_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load_params(self, tables, se_w, se_b, fc_w, fc_b, table_dtype: str = "f32") -> int:
+        """Host arrays: tables[g] [card, k] (float32, or uint16/float16 bit patterns in the compute
+        precision), se_w [M, k], se_b [M], fc_w[l] [out, in], fc_b[l] [out] (float32)."""
+        keep = [np.ascontiguousarray(t) for t in tables]
+        sw = np.ascontiguousarray(se_w, np.float32)
+        sb = np.ascontiguousarray(se_b, np.float32)
+        ws = [np.ascontiguousarray(w, np.float32) for w in fc_w]
+        bs = [np.ascontiguousarray(b, np.float32) for b in fc_b]
+        tp = (C.c_void_p * len(keep))(*[t.ctypes.data for t in keep])
+        wp = (C.c_void_p * len(ws))(*[w.ctypes.data for w in ws])
+        bp = (C.c_void_p * len(bs))(*[b.ctypes.data for b in bs])
+        p = cold_params(PRECISION[table_dtype], C.cast(tp, C.POINTER(C.c_void_p)), sw.ctypes.data, sb.ctypes.data,
+                        C.cast(wp, C.POINTER(C.c_void_p)), C.cast(bp, C.POINTER(C.c_void_p)))
+        v = C.c_uint64()
+        _check(lib().cold_load_params(self.ctx, C.byref(p), C.byref(v)))
+        return v.value
+
+    def score_batch(self, batch: Batch, scores, stream=None):
+        _check(lib().cold_score_batch(self.ctx, C.byref(batch.c), _addr(scores), _stream_handle(stream)))
+
+    def score_request(self, batch: Batch, scores, stream=None):
+        _check(lib().cold_score_request(self.ctx, C.byref(batch.c), _addr(scores), _stream_handle(stream)))
+
+    def topk(self, scores, ad_offsets, ad_offsets_host, K: int, idx_out, key_out, bids=None, stream=None):
+        aoh = np.ascontiguousarray(ad_offsets_host, np.int32)
+        _check(lib().cold_topk(self.ctx, _addr(scores), _addr(ad_offsets), aoh.ctypes.data, len(aoh) - 1, K,
+                               _addr(bids), _addr(idx_out), _addr(key_out), _stream_handle(stream)))
+
+    def info(self) -> dict:
+        i = cold_info()
+        _check(lib().cold_get_info(self.ctx, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in cold_info._fields_}
+
+    def profile(self, enable: bool):
+        _check(lib().cold_profile(self.ctx, int(enable)))
+
+    def profile_read(self):
+        """{kind: (total_ms, launches)} since profile(True)."""
+        ms = np.zeros(PROF_KINDS, np.float64)
+        n = np.zeros(PROF_KINDS, np.int64)
+        _check(lib().cold_profile_read(self.ctx, ms.ctypes.data, n.ctypes.data))
+        return ms, n
+
+    def debug_pooled(self, batch: Batch, out, stream=None):
+        _check(lib().cold_debug_pooled(self.ctx, C.byref(batch.c), _addr(out), _stream_handle(stream)))
+
+    def debug_features(self, batch: Batch, out, stream=None):
+        _check(lib().cold_debug_features(self.ctx, C.byref(batch.c), _addr(out), _stream_handle(stream)))
+
+    def debug_rows(self, batch: Batch, group: int, rows_out, max_rows: int, stream=None):
+        _check(lib().cold_debug_rows(self.ctx, C.byref(batch.c), group, _addr(rows_out), max_rows,
+                                     _stream_handle(stream)))

@@ -1,0 +1,1038 @@
+// cold_api.cu — host runtime behind include/cold.h: context, parameter upload, the chunked
+// scoring pipeline, host-batch staging, top-K and the parity hooks.
+//
+// Per call:
+//   user_kernel (once per request: x_u, u1 = b1 + W1_u x_u, ad -> request map)
+//   for each chunk of `chunk_ads` ads (kept L2-sized so X_ac / H1 / H2 stay on chip):
+//     gather_kernel  (ad + cross groups, column-wise)           -> X_ac   [chunk][D_ac_pad]
+//     gemm FC1 (+u1[request], ReLU)                              -> H1     [chunk][1024]
+//     gemm FC2 .. FC(L-2) (+bias, ReLU)                          -> H2 ...
+//     gemm FC(L-1) (+bias, ReLU) with FC L + sigmoid fused       -> scores [chunk]
+// fp32 precision replaces the GEMMs by the SIMT kernel mlp_f32 (no TF32).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cold.h"
+#include "internal.h"
+
+using namespace cold;
+
+static thread_local std::string g_last_error;
+
+static cold_status fail(cold_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define CK(call)                                                                                        \
+  do {                                                                                                  \
+    cudaError_t _e = (call);                                                                            \
+    if (_e != cudaSuccess)                                                                              \
+      return fail(COLD_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));                   \
+  } while (0)
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+struct cold_ctx {
+  // ---- configuration ----
+  int M = 0, k = 0, L = 0, precision = 0, device = 0, linear_log = 1;
+  uint32_t flags = 0;
+  std::vector<cold_group> groups;
+  std::vector<int> sel, widths, sel_user, sel_ac, sel_pos;
+  int d_u = 0, d_ac = 0, d_ac_pad = 0, d_in = 0;
+  int64_t max_ads = 0;
+  int max_req = 0, chunk = 0, num_sms = 148;
+  bool tensor = false;
+  int bn[COLD_MAX_LAYERS] = {0};
+  // ---- parameters (device) ----
+  bool loaded = false;
+  uint64_t version = 0;
+  std::vector<void*> d_tables;
+  DevGroup* d_groups = nullptr;
+  float* d_se_w = nullptr;
+  float* d_se_b = nullptr;
+  float* d_w1u_t = nullptr;
+  float* d_b1 = nullptr;
+  void* d_w[COLD_MAX_LAYERS] = {nullptr};    // tensor path: compute-dtype weights of GEMM layers
+  float* d_b[COLD_MAX_LAYERS] = {nullptr};
+  float* d_wt[COLD_MAX_LAYERS] = {nullptr};  // fp32 path: transposed weights
+  float* d_head_w = nullptr;
+  float* d_head_b = nullptr;
+  CUtensorMap tmB[COLD_MAX_LAYERS];
+  // ---- workspace ----
+  float* d_u1 = nullptr;
+  float* d_xu = nullptr;
+  int32_t* d_req = nullptr;
+  void* d_X = nullptr;
+  void* d_H[COLD_MAX_LAYERS] = {nullptr};
+  CUtensorMap tmA[COLD_MAX_LAYERS];
+  int* d_err = nullptr;
+  float* d_scores_stage = nullptr;  // [2][chunk] for host outputs
+  int32_t* d_adoff = nullptr;       // [max_req+1] staged ad offsets
+  // host-batch staging
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  cudaEvent_t ev_scored[2] = {nullptr, nullptr}, ev_drained[2] = {nullptr, nullptr};
+  void* d_stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  void* d_user_stage = nullptr;
+  size_t user_stage_bytes = 0;
+  float* d_topk_in = nullptr;
+  size_t topk_in_bytes = 0;
+  void* d_topk_out = nullptr;
+  size_t topk_out_bytes = 0;
+  int64_t device_bytes = 0;
+  std::vector<void*> allocs;
+  // per-kernel event profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_events;       // pool
+  size_t prof_used = 0;
+  std::vector<int> prof_kind;                 // kind of each recorded pair
+  double prof_ms[COLD_PROF_KINDS] = {0};
+  int64_t prof_n[COLD_PROF_KINDS] = {0};
+
+  ~cold_ctx() {
+    cudaSetDevice(device);
+    cudaDeviceSynchronize();
+    for (void* p : allocs) cudaFree(p);
+    for (int i = 0; i < 2; i++) {
+      if (d_stage[i]) cudaFree(d_stage[i]);
+      if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
+      if (ev_consumed[i]) cudaEventDestroy(ev_consumed[i]);
+      if (ev_scored[i]) cudaEventDestroy(ev_scored[i]);
+      if (ev_drained[i]) cudaEventDestroy(ev_drained[i]);
+    }
+    if (d_user_stage) cudaFree(d_user_stage);
+    if (d_topk_in) cudaFree(d_topk_in);
+    if (d_topk_out) cudaFree(d_topk_out);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
+    freeParams();
+    cudaGetLastError();
+  }
+  void freeParams() {
+    for (void* p : d_tables) cudaFree(p);
+    d_tables.clear();
+    void** ps[] = {(void**)&d_groups, (void**)&d_se_w, (void**)&d_se_b, (void**)&d_w1u_t, (void**)&d_b1,
+                   (void**)&d_head_w, (void**)&d_head_b};
+    for (void** p : ps) { if (*p) cudaFree(*p); *p = nullptr; }
+    for (int l = 0; l < COLD_MAX_LAYERS; l++) {
+      if (d_w[l]) cudaFree(d_w[l]);
+      if (d_b[l]) cudaFree(d_b[l]);
+      if (d_wt[l]) cudaFree(d_wt[l]);
+      d_w[l] = nullptr; d_b[l] = nullptr; d_wt[l] = nullptr;
+    }
+  }
+  cudaError_t alloc(void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes < 16 ? 16 : bytes);
+    if (e == cudaSuccess) { allocs.push_back(*p); device_bytes += (int64_t)bytes; }
+    return e;
+  }
+  int elem() const { return precision == COLD_FP32 ? 4 : 2; }
+  // bracket one kernel launch with an event pair (only while profiling)
+  void mark_begin(cudaStream_t st) {
+    if (!prof) return;
+    while (prof_events.size() < prof_used + 2) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      prof_events.push_back(e);
+    }
+    cudaEventRecord(prof_events[prof_used], st);
+  }
+  void mark_end(int kind, cudaStream_t st) {
+    if (!prof) return;
+    cudaEventRecord(prof_events[prof_used + 1], st);
+    prof_kind.push_back(kind);
+    prof_used += 2;
+    if (prof_used >= 8192) flush_profile();
+  }
+  void flush_profile() {
+    if (prof_used == 0) return;
+    cudaEventSynchronize(prof_events[prof_used - 1]);
+    for (size_t i = 0; i < prof_kind.size(); i++) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, prof_events[2 * i], prof_events[2 * i + 1]);
+      prof_ms[prof_kind[i]] += ms;
+      prof_n[prof_kind[i]] += 1;
+    }
+    prof_kind.clear();
+    prof_used = 0;
+  }
+};
+
+// ---------------------------------------------------------------------------------------------
+extern "C" const char* cold_status_string(cold_status s) {
+  switch (s) {
+    case COLD_OK: return "ok";
+    case COLD_ERR_INVALID_ARG: return "invalid argument";
+    case COLD_ERR_SHAPE: return "shape mismatch";
+    case COLD_ERR_ID_RANGE: return "id out of range";
+    case COLD_ERR_K_RANGE: return "K out of range";
+    case COLD_ERR_NOT_LOADED: return "parameters not loaded";
+    case COLD_ERR_PARAMS: return "bad parameters";
+    case COLD_ERR_OOM: return "out of device memory";
+    case COLD_ERR_CUDA: return "CUDA error";
+    case COLD_ERR_UNSUPPORTED: return "unsupported configuration";
+    case COLD_ERR_CAPACITY: return "capacity exceeded";
+  }
+  return "unknown status";
+}
+
+extern "C" const char* cold_last_error(void) { return g_last_error.c_str(); }
+
+static bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static int pick_bn(int n) {
+  if (n % 256 == 0) return 256;
+  if (n % 128 == 0) return 128;
+  return 64;
+}
+
+static cold_status make_tmap(CUtensorMap* tm, void* ptr, int precision, uint64_t inner, uint64_t rows,
+                             uint32_t box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(tm, precision == COLD_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return COLD_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
+  if (!cfg || !out) return fail(COLD_ERR_INVALID_ARG, "null config/out");
+  *out = nullptr;
+  if (cfg->num_groups < 1 || cfg->num_groups > COLD_MAX_GROUPS || !cfg->groups)
+    return fail(COLD_ERR_INVALID_ARG, "num_groups must be in [1, 64]");
+  if (cfg->emb_dim != 2 && cfg->emb_dim != 4 && cfg->emb_dim != 8 && cfg->emb_dim != 16 && cfg->emb_dim != 32)
+    return fail(COLD_ERR_UNSUPPORTED, "emb_dim must be 2, 4, 8, 16 or 32");
+  if (cfg->num_layers < 1 || cfg->num_layers > COLD_MAX_LAYERS || !cfg->widths)
+    return fail(COLD_ERR_SHAPE, "num_layers must be in [1, 16]");
+  if (cfg->precision < COLD_FP32 || cfg->precision > COLD_BF16) return fail(COLD_ERR_INVALID_ARG, "bad precision");
+  if (cfg->activation != COLD_RELU) return fail(COLD_ERR_UNSUPPORTED, "only ReLU");
+  if (cfg->max_ads_per_call < 1 || cfg->max_requests_per_call < 1)
+    return fail(COLD_ERR_INVALID_ARG, "capacities must be >= 1");
+  for (int l = 0; l < cfg->num_layers; l++)
+    if (cfg->widths[l] < 1) return fail(COLD_ERR_SHAPE, "widths must be >= 1");
+  const int last = cfg->widths[cfg->num_layers - 1];
+  if (last != 1 && last != 2) return fail(COLD_ERR_SHAPE, "last width must be 1 or 2");
+  for (int g = 0; g < cfg->num_groups; g++) {
+    const cold_group& G = cfg->groups[g];
+    if (G.side < COLD_USER || G.side > COLD_CROSS) return fail(COLD_ERR_INVALID_ARG, "bad group side");
+    if (G.cardinality < 1 || G.cardinality > (int64_t)1 << 40) return fail(COLD_ERR_INVALID_ARG, "bad cardinality");
+    if (G.side == COLD_CROSS) {
+      if (G.user_ref < 0 || G.user_ref >= cfg->num_groups || cfg->groups[G.user_ref].side != COLD_USER ||
+          G.ad_ref < 0 || G.ad_ref >= cfg->num_groups || cfg->groups[G.ad_ref].side != COLD_AD)
+        return fail(COLD_ERR_SHAPE, "cross group must reference a USER and an AD group");
+    }
+  }
+  cold_ctx* c = new cold_ctx();
+  c->M = cfg->num_groups;
+  c->k = cfg->emb_dim;
+  c->L = cfg->num_layers;
+  c->precision = cfg->precision;
+  c->device = cfg->device;
+  c->linear_log = cfg->linear_log ? 1 : 0;
+  c->flags = cfg->flags;
+  c->groups.assign(cfg->groups, cfg->groups + cfg->num_groups);
+  c->widths.assign(cfg->widths, cfg->widths + cfg->num_layers);
+  if (cfg->num_selected > 0) {
+    if (!cfg->selected) { delete c; return fail(COLD_ERR_INVALID_ARG, "selected is NULL"); }
+    for (int j = 0; j < cfg->num_selected; j++) {
+      int g = cfg->selected[j];
+      if (g < 0 || g >= c->M || (j > 0 && g <= cfg->selected[j - 1])) {
+        delete c;
+        return fail(COLD_ERR_SHAPE, "selected must be strictly ascending schema indices");
+      }
+      c->sel.push_back(g);
+    }
+  } else {
+    for (int g = 0; g < c->M; g++) c->sel.push_back(g);
+  }
+  if (c->sel.empty()) { delete c; return fail(COLD_ERR_SHAPE, "empty selection"); }
+  c->sel_pos.assign(c->M, -1);
+  for (size_t j = 0; j < c->sel.size(); j++) {
+    int g = c->sel[j];
+    c->sel_pos[g] = (int)j;
+    if (c->groups[g].side == COLD_USER) c->sel_user.push_back(g);
+    else c->sel_ac.push_back(g);
+  }
+  c->d_u = (int)c->sel_user.size() * c->k;
+  c->d_ac = (int)c->sel_ac.size() * c->k;
+  c->d_in = c->d_u + c->d_ac;
+  c->max_ads = cfg->max_ads_per_call;
+  c->max_req = cfg->max_requests_per_call;
+
+  if (cudaSetDevice(c->device) != cudaSuccess) { delete c; return fail(COLD_ERR_CUDA, "cudaSetDevice failed"); }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, c->device) != cudaSuccess) {
+    delete c;
+    return fail(COLD_ERR_CUDA, "cudaGetDeviceProperties failed");
+  }
+  c->num_sms = prop.multiProcessorCount;
+  c->tensor = (c->precision != COLD_FP32);
+  if (c->tensor) {
+    if (prop.major != 10) { delete c; return fail(COLD_ERR_UNSUPPORTED, "tcgen05 path needs an sm_100 device"); }
+    if (c->L < 2) { delete c; return fail(COLD_ERR_UNSUPPORTED, "tensor-core path needs >= 2 layers"); }
+    for (int l = 0; l < c->L - 1; l++)
+      if (c->widths[l] % 64 != 0) { delete c; return fail(COLD_ERR_UNSUPPORTED, "hidden widths must be multiples of 64"); }
+    const int pen = c->widths[c->L - 2];
+    if (pen != 64 && pen != 128 && pen != 256) {
+      delete c;
+      return fail(COLD_ERR_UNSUPPORTED, "last hidden width must be 64, 128 or 256");
+    }
+    for (int l = 0; l < c->L - 1; l++) c->bn[l] = (l == c->L - 2) ? pen : pick_bn(c->widths[l]);
+    c->d_ac_pad = std::max(64, (c->d_ac + 63) / 64 * 64);
+  } else {
+    c->d_ac_pad = std::max(1, c->d_ac);
+  }
+  int chunk = cfg->chunk_ads > 0 ? cfg->chunk_ads : c->num_sms * 128 * 2;
+  if (c->tensor) chunk = (chunk + 127) / 128 * 128;
+  c->chunk = (int)std::min<int64_t>(chunk, std::max<int64_t>(c->max_ads, 128));
+  if (c->tensor) c->chunk = (c->chunk + 127) / 128 * 128;
+
+  // ---- workspace ----
+  const int W0 = c->widths[0];
+  cudaError_t e = cudaSuccess;
+  e = e ? e : c->alloc((void**)&c->d_u1, (size_t)c->max_req * W0 * 4);
+  e = e ? e : c->alloc((void**)&c->d_xu, (size_t)c->max_req * std::max(1, c->d_u) * 4);
+  e = e ? e : c->alloc((void**)&c->d_req, (size_t)c->max_ads * 4);
+  e = e ? e : c->alloc((void**)&c->d_X, (size_t)c->chunk * c->d_ac_pad * c->elem());
+  e = e ? e : c->alloc((void**)&c->d_err, 16);
+  e = e ? e : c->alloc((void**)&c->d_scores_stage, (size_t)2 * c->chunk * 4);
+  e = e ? e : c->alloc((void**)&c->d_adoff, (size_t)(c->max_req + 1) * 4);
+  if (c->tensor)
+    for (int l = 0; l < c->L - 2 && !e; l++) e = c->alloc(&c->d_H[l], (size_t)c->chunk * c->widths[l] * 2);
+  if (e != cudaSuccess) {
+    delete c;
+    cudaGetLastError();
+    return fail(COLD_ERR_OOM, std::string("workspace allocation failed: ") + cudaGetErrorString(e));
+  }
+  cudaMemset(c->d_X, 0, (size_t)c->chunk * c->d_ac_pad * c->elem());  // pad columns stay 0
+  if (c->tensor) {
+    for (int l = 0; l < c->L - 1; l++) {
+      void* in = (l == 0) ? c->d_X : c->d_H[l - 1];
+      int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
+      cold_status s = make_tmap(&c->tmA[l], in, c->precision, K, c->chunk, 128);
+      if (s) { delete c; return s; }
+    }
+  }
+  if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return fail(COLD_ERR_CUDA, "stream create failed");
+  }
+  for (int i = 0; i < 2; i++) {
+    cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_consumed[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_scored[i], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_drained[i], cudaEventDisableTiming);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) { delete c; return fail(COLD_ERR_CUDA, "init sync failed"); }
+  *out = c;
+  return COLD_OK;
+}
+
+extern "C" void cold_destroy(cold_ctx* c) { delete c; }
+
+// ---------------------------------------------------------------------------------------------
+// RNE fp32 -> fp16 / bf16 on the host (parameter upload only)
+static uint16_t f32_to_f16_bits(float f) {
+  uint32_t x;
+  memcpy(&x, &f, 4);
+  uint32_t sign = (x >> 16) & 0x8000u;
+  uint32_t ax = x & 0x7fffffffu;
+  if (ax > 0x7f800000u) return (uint16_t)(sign | 0x7e00u);         // NaN
+  if (ax >= 0x477ff000u) return (uint16_t)(sign | 0x7c00u);         // >= 65520 rounds to inf
+  if (ax < 0x38800000u) {                                           // subnormal half
+    const uint32_t e = ax >> 23;                                    // |x| = m * 2^(e-150)
+    const uint32_t m = (ax & 0x7fffffu) | 0x800000u;                // in units of 2^-24: m >> (126-e)
+    const uint32_t shift = 126u - e;                                // 14 .. 126
+    if (shift > 24) return (uint16_t)sign;                          // < 2^-25, or the 2^-25 tie -> 0
+    uint32_t val = m >> shift;
+    const uint32_t rem = m & ((1u << shift) - 1u);
+    const uint32_t half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (val & 1u))) val++;           // may carry into the smallest normal
+    return (uint16_t)(sign | val);
+  }
+  uint32_t val = ((ax >> 13) - (112u << 10));
+  uint32_t rem = ax & 0x1fffu;
+  if (rem > 0x1000u || (rem == 0x1000u && (val & 1))) val++;
+  return (uint16_t)(sign | val);
+}
+static uint16_t f32_to_bf16_bits(float f) {
+  uint32_t x;
+  memcpy(&x, &f, 4);
+  if ((x & 0x7fffffffu) > 0x7f800000u) return 0x7fc0u;
+  return (uint16_t)((x + 0x7fffu + ((x >> 16) & 1u)) >> 16);
+}
+
+template <typename F>
+static cold_status upload(cold_ctx* c, void** dst, size_t bytes, F fill) {
+  std::vector<uint8_t> h(bytes);
+  fill(h.data());
+  if (*dst) { cudaFree(*dst); *dst = nullptr; }
+  if (cudaMalloc(dst, bytes < 16 ? 16 : bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(COLD_ERR_OOM, "parameter allocation failed");
+  }
+  CK(cudaMemcpy(*dst, h.data(), bytes, cudaMemcpyHostToDevice));
+  return COLD_OK;
+}
+
+extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint64_t* version_out) {
+  if (!c || !p) return fail(COLD_ERR_INVALID_ARG, "null ctx/params");
+  if (!p->tables || !p->se_w || !p->se_b || !p->fc_w || !p->fc_b) return fail(COLD_ERR_PARAMS, "missing arrays");
+  if (p->table_dtype != COLD_FP32 && p->table_dtype != c->precision)
+    return fail(COLD_ERR_PARAMS, "table_dtype must be FP32 or the compute precision");
+  for (int g = 0; g < c->M; g++) if (!p->tables[g]) return fail(COLD_ERR_PARAMS, "missing table");
+  for (int l = 0; l < c->L; l++) if (!p->fc_w[l] || !p->fc_b[l]) return fail(COLD_ERR_PARAMS, "missing fc layer");
+  CK(cudaSetDevice(c->device));
+  CK(cudaDeviceSynchronize());   // no in-flight call sees a mix of versions
+  c->loaded = false;
+  c->freeParams();
+  const int k = c->k, es = c->elem();
+  // tables
+  c->d_tables.assign(c->M, nullptr);
+  for (int g = 0; g < c->M; g++) {
+    const size_t n = (size_t)c->groups[g].cardinality * k;
+    void* d = nullptr;
+    if (cudaMalloc(&d, n * es) != cudaSuccess) { cudaGetLastError(); return fail(COLD_ERR_OOM, "table allocation failed"); }
+    c->d_tables[g] = d;
+    if (p->table_dtype == c->precision) {
+      CK(cudaMemcpy(d, p->tables[g], n * es, cudaMemcpyHostToDevice));
+    } else {   // fp32 -> fp16 / bf16, RNE, in slabs
+      const float* src = (const float*)p->tables[g];
+      const size_t slab = (size_t)1 << 24;
+      std::vector<uint16_t> h(std::min(n, slab));
+      for (size_t o = 0; o < n; o += slab) {
+        size_t m = std::min(slab, n - o);
+        for (size_t i = 0; i < m; i++)
+          h[i] = c->precision == COLD_FP16 ? f32_to_f16_bits(src[o + i]) : f32_to_bf16_bits(src[o + i]);
+        CK(cudaMemcpy((uint16_t*)d + o, h.data(), m * 2, cudaMemcpyHostToDevice));
+      }
+    }
+  }
+  // group descriptors
+  std::vector<DevGroup> dg(c->M);
+  std::vector<int> slot(c->M, -1);
+  for (size_t j = 0; j < c->sel_user.size(); j++) slot[c->sel_user[j]] = (int)j;
+  for (size_t j = 0; j < c->sel_ac.size(); j++) slot[c->sel_ac[j]] = (int)j;
+  for (int g = 0; g < c->M; g++) {
+    dg[g].table = c->d_tables[g];
+    dg[g].card = c->groups[g].cardinality;
+    dg[g].side = c->groups[g].side;
+    dg[g].pooled = c->groups[g].pooled;
+    dg[g].user_ref = c->groups[g].user_ref;
+    dg[g].ad_ref = c->groups[g].ad_ref;
+    dg[g].sel_slot = slot[g];
+    dg[g].sel_pos = c->sel_pos[g];
+  }
+  cold_status s;
+  s = upload(c, (void**)&c->d_groups, sizeof(DevGroup) * c->M, [&](uint8_t* h) { memcpy(h, dg.data(), sizeof(DevGroup) * c->M); });
+  if (s) return s;
+  s = upload(c, (void**)&c->d_se_w, sizeof(float) * c->M * k, [&](uint8_t* h) { memcpy(h, p->se_w, sizeof(float) * c->M * k); });
+  if (s) return s;
+  s = upload(c, (void**)&c->d_se_b, sizeof(float) * c->M, [&](uint8_t* h) { memcpy(h, p->se_b, sizeof(float) * c->M); });
+  if (s) return s;
+  // FC1 split into the per-request user block (fp32, transposed) and the ad+cross block
+  const int W0 = c->widths[0];
+  const float* W1 = p->fc_w[0];   // [W0][d_in], columns = selected groups in schema order
+  const int d_in = c->d_in;
+  auto col_of = [&](int g, int d) { return c->sel_pos[g] * k + d; };
+  s = upload(c, (void**)&c->d_w1u_t, sizeof(float) * (size_t)std::max(1, c->d_u) * W0, [&](uint8_t* h) {
+    float* o = (float*)h;
+    for (size_t j = 0; j < c->sel_user.size(); j++)
+      for (int d = 0; d < k; d++)
+        for (int n = 0; n < W0; n++) o[((size_t)j * k + d) * W0 + n] = W1[(size_t)n * d_in + col_of(c->sel_user[j], d)];
+  });
+  if (s) return s;
+  s = upload(c, (void**)&c->d_b1, sizeof(float) * W0, [&](uint8_t* h) { memcpy(h, p->fc_b[0], sizeof(float) * W0); });
+  if (s) return s;
+  auto layer_in = [&](int l) { return l == 0 ? d_in : c->widths[l - 1]; };
+  if (c->tensor) {
+    for (int l = 0; l < c->L - 1; l++) {
+      const int out = c->widths[l];
+      const int Kp = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
+      const float* W = p->fc_w[l];
+      s = upload(c, &c->d_w[l], (size_t)out * Kp * 2, [&](uint8_t* h) {
+        uint16_t* o = (uint16_t*)h;
+        for (int n = 0; n < out; n++)
+          for (int kk = 0; kk < Kp; kk++) {
+            float v = 0.0f;
+            if (l == 0) {
+              int j = kk / k, d = kk % k;
+              if (j < (int)c->sel_ac.size()) v = W[(size_t)n * d_in + col_of(c->sel_ac[j], d)];
+            } else {
+              v = W[(size_t)n * Kp + kk];
+            }
+            o[(size_t)n * Kp + kk] = c->precision == COLD_FP16 ? f32_to_f16_bits(v) : f32_to_bf16_bits(v);
+          }
+      });
+      if (s) return s;
+      if (l > 0) {
+        s = upload(c, (void**)&c->d_b[l], sizeof(float) * out, [&](uint8_t* h) { memcpy(h, p->fc_b[l], sizeof(float) * out); });
+        if (s) return s;
+      }
+      s = make_tmap(&c->tmB[l], c->d_w[l], c->precision, Kp, out, c->bn[l]);
+      if (s) return s;
+    }
+    const int hl = c->L - 1, hin = c->widths[hl - 1], hout = c->widths[hl];
+    s = upload(c, (void**)&c->d_head_w, sizeof(float) * hout * hin, [&](uint8_t* h) { memcpy(h, p->fc_w[hl], sizeof(float) * hout * hin); });
+    if (s) return s;
+    s = upload(c, (void**)&c->d_head_b, sizeof(float) * hout, [&](uint8_t* h) { memcpy(h, p->fc_b[hl], sizeof(float) * hout); });
+    if (s) return s;
+  } else {
+    for (int l = 0; l < c->L; l++) {
+      const int out = c->widths[l];
+      const int in = (l == 0) ? c->d_ac : layer_in(l);
+      const float* W = p->fc_w[l];
+      s = upload(c, (void**)&c->d_wt[l], sizeof(float) * (size_t)std::max(1, in) * out, [&](uint8_t* h) {
+        float* o = (float*)h;
+        for (int i = 0; i < in; i++)
+          for (int n = 0; n < out; n++) {
+            float v;
+            if (l == 0) v = W[(size_t)n * d_in + col_of(c->sel_ac[i / k], i % k)];
+            else v = W[(size_t)n * in + i];
+            o[(size_t)i * out + n] = v;
+          }
+      });
+      if (s) return s;
+      if (l > 0) {
+        s = upload(c, (void**)&c->d_b[l], sizeof(float) * out, [&](uint8_t* h) { memcpy(h, p->fc_b[l], sizeof(float) * out); });
+        if (s) return s;
+      }
+    }
+  }
+  CK(cudaDeviceSynchronize());
+  c->loaded = true;
+  c->version++;
+  if (version_out) *version_out = c->version;
+  return COLD_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// batch validation and views
+
+struct CallPlan {
+  int R = 0;
+  int64_t N = 0;
+  bool host = false;
+  std::vector<int> needed;      // non-cross groups whose ids the call reads
+  BatchView bv;                 // device-mode view (host mode: per chunk)
+};
+
+static cold_status plan_batch(cold_ctx* c, const cold_batch* b, CallPlan& pl) {
+  if (!b || !b->ad_offsets || !b->ad_offsets_host || !b->ids || !b->offs)
+    return fail(COLD_ERR_INVALID_ARG, "batch arrays missing");
+  const int R = b->num_requests;
+  if (R < 1) return fail(COLD_ERR_INVALID_ARG, "num_requests must be >= 1");
+  if (R > c->max_req) return fail(COLD_ERR_CAPACITY, "more requests than max_requests_per_call");
+  const int32_t* ao = b->ad_offsets_host;
+  if (ao[0] != 0) return fail(COLD_ERR_INVALID_ARG, "ad_offsets[0] must be 0");
+  for (int r = 0; r < R; r++)
+    if (ao[r + 1] <= ao[r]) return fail(COLD_ERR_INVALID_ARG, "every request needs >= 1 ad (ad_offsets strictly increasing)");
+  pl.R = R;
+  pl.N = ao[R];
+  if (pl.N > c->max_ads) return fail(COLD_ERR_CAPACITY, "more ads than max_ads_per_call");
+  std::vector<char> need(c->M, 0);
+  for (int g : c->sel) {
+    if (c->groups[g].side == COLD_CROSS) { need[c->groups[g].user_ref] = 1; need[c->groups[g].ad_ref] = 1; }
+    else need[g] = 1;
+  }
+  pl.host = !is_device_ptr(b->ad_offsets);
+  for (int g = 0; g < c->M; g++) {
+    if (!need[g]) continue;
+    pl.needed.push_back(g);
+    const cold_group& G = c->groups[g];
+    if (!b->ids[g]) return fail(COLD_ERR_INVALID_ARG, "ids missing for a needed group");
+    const bool has_offs = (G.side == COLD_USER) || G.pooled;
+    if (has_offs && !b->offs[g]) return fail(COLD_ERR_INVALID_ARG, "offsets missing for a bag group");
+    if (is_device_ptr(b->ids[g]) == pl.host) return fail(COLD_ERR_INVALID_ARG, "a batch must be all-host or all-device");
+    if (pl.host && has_offs && (!b->offs_host || !b->offs_host[g]))
+      return fail(COLD_ERR_INVALID_ARG, "host batch needs offs_host for bag groups");
+  }
+  memset(&pl.bv, 0, sizeof(pl.bv));
+  if (!pl.host) {
+    for (int g : pl.needed) {
+      pl.bv.g[g].ids = b->ids[g];
+      pl.bv.g[g].offs = b->offs[g];
+    }
+  }
+  return COLD_OK;
+}
+
+static cold_status check_err(cold_ctx* c, cudaStream_t st) {
+  if (!(c->flags & COLD_VALIDATE_IDS)) return COLD_OK;
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, c->d_err, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (h) return fail(COLD_ERR_ID_RANGE, "an id is outside its group's cardinality");
+  return COLD_OK;
+}
+
+// stage the user CSR arrays of a host batch (small) and the ad offsets
+static cold_status stage_user(cold_ctx* c, const cold_batch* b, CallPlan& pl, cudaStream_t st) {
+  size_t bytes = (size_t)(pl.R + 1) * 4;
+  for (int g : pl.needed)
+    if (c->groups[g].side == COLD_USER) bytes += (size_t)(pl.R + 1) * 4 + (size_t)b->offs_host[g][pl.R] * 4 + 64;
+  if (bytes > c->user_stage_bytes) {
+    CK(cudaStreamSynchronize(st));
+    if (c->d_user_stage) cudaFree(c->d_user_stage);
+    c->d_user_stage = nullptr;
+    if (cudaMalloc(&c->d_user_stage, bytes * 2) != cudaSuccess) { cudaGetLastError(); return fail(COLD_ERR_OOM, "staging"); }
+    c->user_stage_bytes = bytes * 2;
+  }
+  uint8_t* p = (uint8_t*)c->d_user_stage;
+  CK(cudaMemcpyAsync(c->d_adoff, b->ad_offsets_host, (size_t)(pl.R + 1) * 4, cudaMemcpyHostToDevice, st));
+  for (int g : pl.needed) {
+    if (c->groups[g].side != COLD_USER) continue;
+    int32_t* o = (int32_t*)p;
+    p += ((size_t)(pl.R + 1) * 4 + 15) / 16 * 16;
+    int32_t* ids = (int32_t*)p;
+    const int64_t nids = b->offs_host[g][pl.R];
+    p += ((size_t)nids * 4 + 15) / 16 * 16;
+    CK(cudaMemcpyAsync(o, b->offs_host[g], (size_t)(pl.R + 1) * 4, cudaMemcpyHostToDevice, st));
+    if (nids) CK(cudaMemcpyAsync(ids, b->ids[g], (size_t)nids * 4, cudaMemcpyHostToDevice, st));
+    pl.bv.g[g].ids = ids;
+    pl.bv.g[g].offs = o;
+  }
+  return COLD_OK;
+}
+
+// bytes of ad-side inputs for ads [a0, a1) of a host batch
+static size_t chunk_stage_bytes(cold_ctx* c, const cold_batch* b, const CallPlan& pl, int64_t a0, int64_t a1) {
+  size_t bytes = 0;
+  for (int g : pl.needed) {
+    const cold_group& G = c->groups[g];
+    if (G.side != COLD_AD) continue;
+    if (!G.pooled) bytes += (size_t)(a1 - a0) * 4 + 16;
+    else bytes += (size_t)(a1 - a0 + 1) * 4 + 16 + (size_t)(b->offs_host[g][a1] - b->offs_host[g][a0]) * 4 + 16;
+  }
+  return bytes;
+}
+
+// copy ad-side inputs of [a0, a1) into stage slot `s` on the copy stream; fills bv
+static cold_status stage_chunk(cold_ctx* c, const cold_batch* b, const CallPlan& pl, int64_t a0, int64_t a1, int s,
+                               BatchView& bv) {
+  uint8_t* p = (uint8_t*)c->d_stage[s];
+  for (int g : pl.needed) {
+    const cold_group& G = c->groups[g];
+    if (G.side != COLD_AD) continue;
+    if (!G.pooled) {
+      CK(cudaMemcpyAsync(p, b->ids[g] + a0, (size_t)(a1 - a0) * 4, cudaMemcpyHostToDevice, c->copy_stream));
+      bv.g[g].ids = (const int32_t*)p;
+      bv.g[g].id_shift = a0;
+      p += ((size_t)(a1 - a0) * 4 + 15) / 16 * 16;
+    } else {
+      const int32_t* oh = b->offs_host[g];
+      CK(cudaMemcpyAsync(p, oh + a0, (size_t)(a1 - a0 + 1) * 4, cudaMemcpyHostToDevice, c->copy_stream));
+      bv.g[g].offs = (const int32_t*)p;
+      bv.g[g].offs_shift = a0;
+      bv.g[g].val_shift = oh[a0];
+      p += ((size_t)(a1 - a0 + 1) * 4 + 15) / 16 * 16;
+      const int64_t nid = oh[a1] - oh[a0];
+      if (nid) CK(cudaMemcpyAsync(p, b->ids[g] + oh[a0], (size_t)nid * 4, cudaMemcpyHostToDevice, c->copy_stream));
+      bv.g[g].ids = (const int32_t*)p;
+      p += ((size_t)nid * 4 + 15) / 16 * 16;
+    }
+  }
+  return COLD_OK;
+}
+
+enum { RUN_SCORE = 0, RUN_DEBUG = 1 };
+
+struct DebugOut {
+  float* pooled = nullptr;
+  float* feat = nullptr;
+};
+
+static UserArgs make_user_args(cold_ctx* c, const CallPlan& pl, const int32_t* d_adoff, const DebugOut& dbg) {
+  UserArgs ua;
+  memset(&ua, 0, sizeof(ua));
+  ua.groups = c->d_groups;
+  ua.bv = pl.bv;
+  ua.n_user = (int)c->sel_user.size();
+  for (int j = 0; j < ua.n_user; j++) ua.user_g[j] = c->sel_user[j];
+  ua.k = c->k;
+  ua.se_w = c->d_se_w;
+  ua.se_b = c->d_se_b;
+  ua.linear_log = c->linear_log;
+  ua.w1u_t = c->d_w1u_t;
+  ua.b1 = c->d_b1;
+  ua.H = c->widths[0];
+  ua.u1 = c->d_u1;
+  ua.xu = c->d_xu;
+  ua.ad_offsets = d_adoff;
+  ua.req_of_ad = c->d_req;
+  ua.validate = (c->flags & COLD_VALIDATE_IDS) ? 1 : 0;
+  ua.err = c->d_err;
+  ua.dbg_pooled = dbg.pooled;
+  ua.dbg_feat = dbg.feat;
+  ua.n_sel = (int)c->sel.size();
+  ua.d_in = c->d_in;
+  return ua;
+}
+
+static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0, int64_t n, const DebugOut& dbg) {
+  GatherArgs ga;
+  memset(&ga, 0, sizeof(ga));
+  ga.groups = c->d_groups;
+  ga.bv = bv;
+  ga.n_ac = (int)c->sel_ac.size();
+  for (int j = 0; j < ga.n_ac; j++) ga.ac_g[j] = c->sel_ac[j];
+  ga.k = c->k;
+  ga.se_w = c->d_se_w;
+  ga.se_b = c->d_se_b;
+  ga.linear_log = c->linear_log;
+  ga.req_of_ad = c->d_req;
+  ga.a0 = a0;
+  ga.n = n;
+  ga.X = c->d_X;
+  ga.ldx = c->d_ac_pad;
+  ga.validate = (c->flags & COLD_VALIDATE_IDS) ? 1 : 0;
+  ga.err = c->d_err;
+  ga.dbg_pooled = dbg.pooled;
+  ga.dbg_feat = dbg.feat;
+  ga.n_sel = (int)c->sel.size();
+  ga.d_in = c->d_in;
+  return ga;
+}
+
+// the network on one chunk: X (rows a0 .. a0+n) -> scores_out[0 .. n)
+static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, cudaStream_t st) {
+  if (!c->tensor) {
+    MlpF32Args m;
+    memset(&m, 0, sizeof(m));
+    m.X = (const float*)c->d_X;
+    m.ldx = c->d_ac_pad;
+    m.d_ac = c->d_ac;
+    m.u1 = c->d_u1;
+    m.ld_u1 = c->widths[0];
+    m.req_of_ad = c->d_req;
+    m.a0 = a0;
+    m.n = n;
+    m.L = c->L;
+    int mw = std::max(1, c->d_ac);
+    for (int l = 0; l < c->L; l++) {
+      m.wt[l] = c->d_wt[l];
+      m.b[l] = c->d_b[l];
+      m.width[l] = c->widths[l];
+      mw = std::max(mw, c->widths[l]);
+    }
+    m.max_w = mw;
+    m.scores = scores_out;
+    c->mark_begin(st);
+    launch_mlp_f32(m, st);
+    c->mark_end(COLD_PROF_FC, st);
+    return;
+  }
+  for (int l = 0; l < c->L - 1; l++) {
+    EpiParams ep;
+    memset(&ep, 0, sizeof(ep));
+    ep.relu = 1;
+    if (l == 0) {
+      ep.u1 = c->d_u1;
+      ep.ld_u1 = c->widths[0];
+      ep.req_of_ad = c->d_req;
+      ep.a0 = a0;
+    } else {
+      ep.bias = c->d_b[l];
+    }
+    const bool head = (l == c->L - 2);
+    if (head) {
+      ep.head_w = c->d_head_w;
+      ep.head_b = c->d_head_b;
+      ep.head_n = c->widths[c->L - 1];
+      ep.scores = scores_out;
+    } else {
+      ep.out = c->d_H[l];
+      ep.ldo = c->widths[l];
+    }
+    const int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
+    c->mark_begin(st);
+    launch_gemm(&c->tmA[l], &c->tmB[l], (int)n, c->widths[l], K, c->bn[l], c->precision == COLD_BF16 ? 1 : 0, ep,
+                c->num_sms, st);
+    c->mark_end(COLD_PROF_FC + l, st);
+  }
+}
+
+static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStream_t st, int mode, const DebugOut& dbg) {
+  if (!c) return fail(COLD_ERR_INVALID_ARG, "null ctx");
+  if (!c->loaded) return fail(COLD_ERR_NOT_LOADED, "cold_load_params has not been called");
+  CallPlan pl;
+  cold_status s = plan_batch(c, b, pl);
+  if (s) return s;
+  if (mode == RUN_SCORE && !scores) return fail(COLD_ERR_INVALID_ARG, "scores is NULL");
+  CK(cudaSetDevice(c->device));
+  cudaGetLastError();   // start clean: only report errors of this call's launches
+  if (c->flags & COLD_VALIDATE_IDS) CK(cudaMemsetAsync(c->d_err, 0, 4, st));
+  const int32_t* d_adoff = b->ad_offsets;
+  if (pl.host) {
+    s = stage_user(c, b, pl, st);
+    if (s) return s;
+    d_adoff = c->d_adoff;
+  }
+  const bool scores_dev = mode == RUN_SCORE && is_device_ptr(scores);
+  UserArgs ua = make_user_args(c, pl, d_adoff, dbg);
+  c->mark_begin(st);
+  launch_user(ua, pl.R, c->precision, st);
+  c->mark_end(COLD_PROF_USER, st);
+  CK(cudaGetLastError());
+  const int64_t chunk = c->chunk;
+  const int64_t nchunks = (pl.N + chunk - 1) / chunk;
+  if (pl.host) {
+    size_t need = 0;
+    for (int64_t ci = 0; ci < nchunks; ci++)
+      need = std::max(need, chunk_stage_bytes(c, b, pl, ci * chunk, std::min(pl.N, (ci + 1) * chunk)));
+    if (need > c->stage_bytes) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaStreamSynchronize(c->copy_stream));
+      for (int i = 0; i < 2; i++) {
+        if (c->d_stage[i]) cudaFree(c->d_stage[i]);
+        c->d_stage[i] = nullptr;
+        if (cudaMalloc(&c->d_stage[i], need) != cudaSuccess) { cudaGetLastError(); return fail(COLD_ERR_OOM, "staging"); }
+      }
+      c->stage_bytes = need;
+    }
+    // the copy stream must not run ahead of earlier work on `st` that still reads the slots
+    CK(cudaEventRecord(c->ev_consumed[0], st));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[0], 0));
+    CK(cudaEventRecord(c->ev_consumed[1], st));
+  }
+  for (int64_t ci = 0; ci < nchunks; ci++) {
+    const int64_t a0 = ci * chunk, a1 = std::min(pl.N, a0 + chunk), n = a1 - a0;
+    const int slot = (int)(ci & 1);
+    BatchView bv = pl.bv;
+    if (pl.host) {
+      if (ci >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[slot], 0));
+      s = stage_chunk(c, b, pl, a0, a1, slot, bv);
+      if (s) return s;
+      CK(cudaEventRecord(c->ev_copied[slot], c->copy_stream));
+      CK(cudaStreamWaitEvent(st, c->ev_copied[slot], 0));
+    }
+    GatherArgs ga = make_gather_args(c, bv, a0, n, dbg);
+    c->mark_begin(st);
+    launch_gather(ga, c->precision, st);
+    c->mark_end(COLD_PROF_GATHER, st);
+    if (pl.host) CK(cudaEventRecord(c->ev_consumed[slot], st));
+    if (mode == RUN_SCORE) {
+      float* out = scores_dev ? scores + a0 : c->d_scores_stage + (int64_t)slot * chunk;
+      if (!scores_dev && ci >= 2) CK(cudaStreamWaitEvent(st, c->ev_drained[slot], 0));
+      run_network(c, a0, n, out, st);
+      if (!scores_dev) {
+        CK(cudaEventRecord(c->ev_scored[slot], st));
+        CK(cudaStreamWaitEvent(c->copy_stream, c->ev_scored[slot], 0));
+        CK(cudaMemcpyAsync(scores + a0, out, (size_t)n * 4, cudaMemcpyDeviceToHost, c->copy_stream));
+        CK(cudaEventRecord(c->ev_drained[slot], c->copy_stream));
+      }
+    }
+    CK(cudaGetLastError());
+  }
+  if (pl.host || !scores_dev) {
+    // join the copy stream back into the caller's stream
+    CK(cudaEventRecord(c->ev_drained[0], c->copy_stream));
+    CK(cudaStreamWaitEvent(st, c->ev_drained[0], 0));
+  }
+  return check_err(c, st);
+}
+
+extern "C" cold_status cold_score_batch(cold_ctx* c, const cold_batch* b, float* scores, void* stream) {
+  return run(c, b, scores, (cudaStream_t)stream, RUN_SCORE, DebugOut());
+}
+
+extern "C" cold_status cold_score_request(cold_ctx* c, const cold_batch* one, float* scores, void* stream) {
+  if (!one || one->num_requests != 1) return fail(COLD_ERR_INVALID_ARG, "cold_score_request takes exactly one request");
+  return run(c, one, scores, (cudaStream_t)stream, RUN_SCORE, DebugOut());
+}
+
+extern "C" cold_status cold_debug_pooled(cold_ctx* c, const cold_batch* b, float* out, void* stream) {
+  if (!out || !is_device_ptr(out)) return fail(COLD_ERR_INVALID_ARG, "out must be device memory");
+  DebugOut d;
+  d.pooled = out;
+  return run(c, b, nullptr, (cudaStream_t)stream, RUN_DEBUG, d);
+}
+
+extern "C" cold_status cold_debug_features(cold_ctx* c, const cold_batch* b, float* out, void* stream) {
+  if (!out || !is_device_ptr(out)) return fail(COLD_ERR_INVALID_ARG, "out must be device memory");
+  DebugOut d;
+  d.feat = out;
+  return run(c, b, nullptr, (cudaStream_t)stream, RUN_DEBUG, d);
+}
+
+extern "C" cold_status cold_debug_rows(cold_ctx* c, const cold_batch* b, int32_t group, int64_t* rows_out,
+                                       int32_t max_rows, void* stream) {
+  if (!c) return fail(COLD_ERR_INVALID_ARG, "null ctx");
+  if (!c->loaded) return fail(COLD_ERR_NOT_LOADED, "cold_load_params has not been called");
+  if (group < 0 || group >= c->M || max_rows < 1 || !rows_out || !is_device_ptr(rows_out))
+    return fail(COLD_ERR_INVALID_ARG, "bad group / max_rows / rows_out");
+  CallPlan pl;
+  cold_status s = plan_batch(c, b, pl);
+  if (s) return s;
+  if (pl.host) return fail(COLD_ERR_INVALID_ARG, "cold_debug_rows takes a device batch");
+  const cold_group& G = c->groups[group];
+  // the group's own ids (and for CROSS its refs) must be present
+  std::vector<int> gs = {group};
+  if (G.side == COLD_CROSS) gs = {G.user_ref, G.ad_ref};
+  for (int g : gs) {
+    if (!b->ids[g]) return fail(COLD_ERR_INVALID_ARG, "ids missing");
+    pl.bv.g[g].ids = b->ids[g];
+    pl.bv.g[g].offs = b->offs[g];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  cudaGetLastError();
+  UserArgs ua = make_user_args(c, pl, b->ad_offsets, DebugOut());
+  launch_user(ua, pl.R, c->precision, st);
+  RowsArgs ra;
+  ra.groups = c->d_groups;
+  ra.bv = pl.bv;
+  ra.g = group;
+  ra.req_of_ad = c->d_req;
+  ra.n = pl.N;
+  ra.rows = rows_out;
+  ra.max_rows = max_rows;
+  launch_rows(ra, st);
+  CK(cudaGetLastError());
+  return COLD_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+extern "C" cold_status cold_topk(cold_ctx* c, const float* scores, const int32_t* ad_offsets,
+                                 const int32_t* ad_offsets_host, int32_t R, int32_t K, const float* bids,
+                                 int32_t* idx_out, float* key_out, void* stream) {
+  if (!c) return fail(COLD_ERR_INVALID_ARG, "null ctx");
+  if (!scores || !ad_offsets || !ad_offsets_host || !idx_out || !key_out) return fail(COLD_ERR_INVALID_ARG, "null pointer");
+  if (R < 1 || R > c->max_req) return fail(COLD_ERR_INVALID_ARG, "R out of range");
+  if (ad_offsets_host[0] != 0) return fail(COLD_ERR_INVALID_ARG, "ad_offsets[0] must be 0");
+  int32_t min_n = INT32_MAX;
+  for (int r = 0; r < R; r++) {
+    int32_t n = ad_offsets_host[r + 1] - ad_offsets_host[r];
+    if (n < 1) return fail(COLD_ERR_INVALID_ARG, "every request needs >= 1 ad");
+    min_n = std::min(min_n, n);
+  }
+  if (K < 1 || K > min_n) return fail(COLD_ERR_K_RANGE, "K must be in [1, min ads per request]");
+  if (K > 4096) return fail(COLD_ERR_UNSUPPORTED, "K > 4096");
+  const int64_t N = ad_offsets_host[R];
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  cudaGetLastError();
+  const bool s_dev = is_device_ptr(scores), o_dev = is_device_ptr(ad_offsets);
+  const bool b_dev = !bids || is_device_ptr(bids);
+  const bool out_dev = is_device_ptr(idx_out) && is_device_ptr(key_out);
+  size_t in_need = (s_dev ? 0 : (size_t)N * 4) + (b_dev ? 0 : (size_t)N * 4) + (o_dev ? 0 : (size_t)(R + 1) * 4) + 64;
+  size_t out_need = out_dev ? 16 : (size_t)R * K * 8 + 64;
+  if (in_need > c->topk_in_bytes) {
+    CK(cudaStreamSynchronize(st));
+    if (c->d_topk_in) cudaFree(c->d_topk_in);
+    c->d_topk_in = nullptr;
+    if (cudaMalloc((void**)&c->d_topk_in, in_need) != cudaSuccess) { cudaGetLastError(); return fail(COLD_ERR_OOM, "topk staging"); }
+    c->topk_in_bytes = in_need;
+  }
+  if (out_need > c->topk_out_bytes) {
+    CK(cudaStreamSynchronize(st));
+    if (c->d_topk_out) cudaFree(c->d_topk_out);
+    c->d_topk_out = nullptr;
+    if (cudaMalloc(&c->d_topk_out, out_need) != cudaSuccess) { cudaGetLastError(); return fail(COLD_ERR_OOM, "topk staging"); }
+    c->topk_out_bytes = out_need;
+  }
+  uint8_t* p = (uint8_t*)c->d_topk_in;
+  TopkArgs ta;
+  ta.scores = scores;
+  ta.bids = bids;
+  ta.ad_offsets = ad_offsets;
+  if (!s_dev) {
+    CK(cudaMemcpyAsync(p, scores, (size_t)N * 4, cudaMemcpyHostToDevice, st));
+    ta.scores = (const float*)p;
+    p += ((size_t)N * 4 + 15) / 16 * 16;
+  }
+  if (!b_dev) {
+    CK(cudaMemcpyAsync(p, bids, (size_t)N * 4, cudaMemcpyHostToDevice, st));
+    ta.bids = (const float*)p;
+    p += ((size_t)N * 4 + 15) / 16 * 16;
+  }
+  if (!o_dev) {
+    CK(cudaMemcpyAsync(p, ad_offsets_host, (size_t)(R + 1) * 4, cudaMemcpyHostToDevice, st));
+    ta.ad_offsets = (const int32_t*)p;
+  }
+  ta.R = R;
+  ta.K = K;
+  ta.idx = out_dev ? idx_out : (int32_t*)c->d_topk_out;
+  ta.key = out_dev ? key_out : (float*)((uint8_t*)c->d_topk_out + (size_t)R * K * 4);
+  c->mark_begin(st);
+  launch_topk(ta, st);
+  c->mark_end(COLD_PROF_TOPK, st);
+  CK(cudaGetLastError());
+  if (!out_dev) {
+    CK(cudaMemcpyAsync(idx_out, ta.idx, (size_t)R * K * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(key_out, ta.key, (size_t)R * K * 4, cudaMemcpyDeviceToHost, st));
+  }
+  return COLD_OK;
+}
+
+extern "C" cold_status cold_profile(cold_ctx* c, int32_t enable) {
+  if (!c) return fail(COLD_ERR_INVALID_ARG, "null ctx");
+  CK(cudaSetDevice(c->device));
+  if (enable) {
+    c->flush_profile();
+    for (int i = 0; i < COLD_PROF_KINDS; i++) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
+  }
+  c->prof = enable != 0;
+  return COLD_OK;
+}
+
+extern "C" cold_status cold_profile_read(cold_ctx* c, double* total_ms, int64_t* launches) {
+  if (!c || !total_ms || !launches) return fail(COLD_ERR_INVALID_ARG, "null");
+  CK(cudaSetDevice(c->device));
+  c->flush_profile();
+  for (int i = 0; i < COLD_PROF_KINDS; i++) { total_ms[i] = c->prof_ms[i]; launches[i] = c->prof_n[i]; }
+  return COLD_OK;
+}
+
+extern "C" cold_status cold_get_info(const cold_ctx* c, cold_info* out) {
+  if (!c || !out) return fail(COLD_ERR_INVALID_ARG, "null");
+  out->version = c->version;
+  out->d_in = c->d_in;
+  out->d_user = c->d_u;
+  out->d_ad = c->d_ac;
+  out->chunk_ads = c->chunk;
+  out->kernels_per_chunk = 1 + (c->tensor ? c->L - 1 : 1);
+  out->kernels_per_call = 1;
+  out->tensor_core = c->tensor ? 1 : 0;
+  int64_t b = c->device_bytes;
+  for (int g = 0; g < c->M && g < (int)c->d_tables.size(); g++) b += c->groups[g].cardinality * c->k * c->elem();
+  out->device_bytes = b;
+  return COLD_OK;
+}

@@ -1,0 +1,106 @@
+// internal.h — launchers shared between the host runtime (cold_api.cu) and the kernel files.
+#pragma once
+#include <cuda.h>
+#include "common.cuh"
+
+namespace cold {
+
+struct UserArgs {
+  const DevGroup* groups;
+  BatchView bv;
+  int n_user;                      // selected USER groups
+  int user_g[COLD_MAX_GROUPS];     // their schema indices
+  int k;
+  const float* se_w;               // [M][k]
+  const float* se_b;               // [M]
+  int linear_log;
+  const float* w1u_t;              // [D_u][H] fp32 (W1 user columns, transposed)
+  const float* b1;                 // [H]
+  int H;                           // FC1 width
+  float* u1;                       // [R][H] out: b1 + W1_u x_u
+  float* xu;                       // [R][D_u] out: x_u
+  const int32_t* ad_offsets;       // [R+1] device
+  int32_t* req_of_ad;              // [N] out
+  int validate;
+  int* err;
+  // debug (nullable): user-group columns broadcast to every ad of the request
+  float* dbg_pooled;               // [N][n_sel][k]
+  float* dbg_feat;                 // [N][D_in]
+  int n_sel, d_in;
+};
+
+struct GatherArgs {
+  const DevGroup* groups;
+  BatchView bv;
+  int n_ac;                        // selected AD + CROSS groups
+  int ac_g[COLD_MAX_GROUPS];
+  int k;
+  const float* se_w;
+  const float* se_b;
+  int linear_log;
+  const int32_t* req_of_ad;        // call-global
+  int64_t a0;                      // first ad of the chunk (call-global index)
+  int64_t n;                       // ads in the chunk
+  void* X;                         // [n][ldx] storage dtype (chunk-local rows)
+  int ldx;
+  int validate;
+  int* err;
+  float* dbg_pooled;               // [N][n_sel][k] (call-global rows)
+  float* dbg_feat;                 // [N][D_in]
+  int n_sel, d_in;
+};
+
+struct RowsArgs {
+  const DevGroup* groups;
+  BatchView bv;
+  int g;
+  const int32_t* req_of_ad;
+  int64_t n;
+  int64_t* rows;
+  int max_rows;
+};
+
+// precision: 0 fp32, 1 fp16, 2 bf16 (storage dtype of tables and X)
+void launch_user(const UserArgs& a, int R, int precision, cudaStream_t s);
+void launch_gather(const GatherArgs& a, int precision, cudaStream_t s);
+void launch_rows(const RowsArgs& a, cudaStream_t s);
+
+// fp32 SIMT FC stack (no TF32): X -> scores
+struct MlpF32Args {
+  const float* X; int ldx; int d_ac;
+  const float* u1; int ld_u1;      // [R][W0] (user part + b1)
+  const int32_t* req_of_ad; int64_t a0; int64_t n;
+  int L;
+  const float* wt[COLD_MAX_LAYERS];  // layer 0: W1_ac^T [d_ac][W0]; l>0: W_l^T [in][out]
+  const float* b[COLD_MAX_LAYERS];   // layer 0 unused (inside u1)
+  int width[COLD_MAX_LAYERS];
+  int max_w;
+  float* scores;                   // chunk-local [n]
+};
+void launch_mlp_f32(const MlpF32Args& a, cudaStream_t s);
+
+// tcgen05 GEMM layer: out = act(A . B^T + bias [+ u1[req]]) or fused head -> scores
+struct EpiParams {
+  const float* bias;               // [N] or null
+  const float* u1; int ld_u1;      // FC1: per-request pre-activation [R][ld_u1]
+  const int32_t* req_of_ad; int64_t a0;
+  void* out; int ldo;              // [M][ldo] storage dtype (null with a head)
+  const float* head_w;             // [head_n][N] fp32
+  const float* head_b;             // [head_n]
+  int head_n;                      // 0: no head; 1 or 2: fused last layer + sigmoid
+  float* scores;                   // chunk-local [M]
+  int relu;
+};
+void launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, int bn,
+                 int bf16, const EpiParams& ep, int num_sms, cudaStream_t s);
+int gemm_smem_bytes(int bn);
+
+// top-K per request
+struct TopkArgs {
+  const float* scores; const float* bids; const int32_t* ad_offsets;
+  int R; int K;
+  int32_t* idx; float* key;
+};
+void launch_topk(const TopkArgs& a, cudaStream_t s);
+
+}  // namespace cold
