@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -59,6 +60,7 @@ struct cold_ctx {
   uint32_t flags = 0;
   std::vector<cold_group> groups;
   std::vector<int> sel, widths, sel_user, sel_ac, sel_pos;
+  std::vector<int> gather_order;     // sel_ac positions, heaviest (cross over a user bag) first
   int d_u = 0, d_ac = 0, d_ac_pad = 0, d_in = 0;
   int64_t max_ads = 0;
   int max_req = 0, chunk = 0, num_sms = 148;
@@ -86,6 +88,11 @@ struct cold_ctx {
   void* d_X = nullptr;
   void* d_H[COLD_MAX_LAYERS] = {nullptr};
   CUtensorMap tmA[COLD_MAX_LAYERS];
+  CUtensorMap tmC[COLD_MAX_LAYERS];  // epilogue TMA-store maps (32 x 32 boxes)
+  int cs[COLD_MAX_LAYERS] = {0};     // cluster size (weight-tile multicast) per GEMM layer
+  bool resb[COLD_MAX_LAYERS] = {false};  // weight slice resident in shared memory (K x BN <= 128 KB)
+  bool use_tail = false;             // last three hidden layers + head in one fused kernel
+  bool pdl = true;                   // programmatic dependent launch between the GEMM kernels
   int* d_err = nullptr;
   float* d_scores_stage = nullptr;  // [2][chunk] for host outputs
   int32_t* d_adoff = nullptr;       // [max_req+1] staged ad offsets
@@ -216,16 +223,19 @@ static int pick_bn(int n) {
   return 64;
 }
 
+// 2-D row-major [rows][inner] 16-bit tensor; box {box_cols, box_rows}; operands use 64-col boxes with
+// 128 B swizzle (tcgen05 SW128 K-major atoms), epilogue outputs 32-col boxes with 64 B swizzle.
 static cold_status make_tmap(CUtensorMap* tm, void* ptr, int precision, uint64_t inner, uint64_t rows,
-                             uint32_t box_rows) {
+                             uint32_t box_rows, uint32_t box_cols = 64) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   cuuint64_t dims[2] = {inner, rows};
   cuuint64_t strides[1] = {inner * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = enc(tm, precision == COLD_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
-                   2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return COLD_OK;
@@ -290,6 +300,14 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     if (c->groups[g].side == COLD_USER) c->sel_user.push_back(g);
     else c->sel_ac.push_back(g);
   }
+  // heaviest-first dispatch order for the gather grid: cross groups over pooled bags first
+  for (int pass = 0; pass < 3; pass++)
+    for (size_t j = 0; j < c->sel_ac.size(); j++) {
+      const cold_group& G = c->groups[c->sel_ac[j]];
+      // class 0: cross groups (a user bag x ad id: L rows each); 1: ad bags; 2: single ad ids
+      const int cls = G.side == COLD_CROSS ? 0 : (G.pooled ? 1 : 2);
+      if (cls == pass) c->gather_order.push_back((int)j);
+    }
   c->d_u = (int)c->sel_user.size() * c->k;
   c->d_ac = (int)c->sel_ac.size() * c->k;
   c->d_in = c->d_u + c->d_ac;
@@ -343,11 +361,33 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   }
   cudaMemset(c->d_X, 0, (size_t)c->chunk * c->d_ac_pad * c->elem());  // pad columns stay 0
   if (c->tensor) {
+    const char* env_cs = getenv("COLD_GEMM_CS");
+    const int cs_default = env_cs ? atoi(env_cs) : 1;
+    const char* env_tail = getenv("COLD_TAIL");
+    const char* env_resb = getenv("COLD_RESB");
+    const char* env_pdl = getenv("COLD_PDL");
+    c->pdl = !(env_pdl && atoi(env_pdl) == 0);
+    const int Lg = c->L - 1;   // GEMM layers (the last layer is fused as the head)
+    if (Lg >= 3 && !(env_tail && atoi(env_tail) == 0)) {
+      const int k3 = (Lg - 3 == 0) ? c->d_ac_pad : c->widths[Lg - 4];
+      c->use_tail = tail_supported(c->widths[Lg - 3], c->widths[Lg - 2], c->widths[Lg - 1], k3);
+    }
     for (int l = 0; l < c->L - 1; l++) {
       void* in = (l == 0) ? c->d_X : c->d_H[l - 1];
       int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
       cold_status s = make_tmap(&c->tmA[l], in, c->precision, K, c->chunk, 128);
       if (s) { delete c; return s; }
+      if (l < c->L - 2) {
+        s = make_tmap(&c->tmC[l], c->d_H[l], c->precision, c->widths[l], c->chunk, 32, 32);
+        if (s) { delete c; return s; }
+      } else {
+        c->tmC[l] = c->tmA[l];   // unused by the head epilogue
+      }
+      int cs = cs_default;
+      while (cs > 1 && (c->bn[l] / cs) % 8 != 0) cs >>= 1;   // B slices must be whole 8-row swizzle atoms
+      c->cs[l] = (cs == 4 || cs == 2) ? cs : 1;
+      if (c->use_tail && l >= Lg - 3) c->cs[l] = 1;          // the tail kernel loads whole weight tiles
+      c->resb[l] = c->cs[l] == 1 && gemm_resident_ok(c->bn[l], K) && !(env_resb && atoi(env_resb) == 0);
     }
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -506,7 +546,7 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
         s = upload(c, (void**)&c->d_b[l], sizeof(float) * out, [&](uint8_t* h) { memcpy(h, p->fc_b[l], sizeof(float) * out); });
         if (s) return s;
       }
-      s = make_tmap(&c->tmB[l], c->d_w[l], c->precision, Kp, out, c->bn[l]);
+      s = make_tmap(&c->tmB[l], c->d_w[l], c->precision, Kp, out, c->bn[l] / c->cs[l]);
       if (s) return s;
     }
     const int hl = c->L - 1, hin = c->widths[hl - 1], hout = c->widths[hl];
@@ -712,7 +752,7 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
   ga.groups = c->d_groups;
   ga.bv = bv;
   ga.n_ac = (int)c->sel_ac.size();
-  for (int j = 0; j < ga.n_ac; j++) ga.ac_g[j] = c->sel_ac[j];
+  for (int j = 0; j < ga.n_ac; j++) { ga.ac_g[j] = c->sel_ac[j]; ga.order[j] = c->gather_order[j]; }
   ga.k = c->k;
   ga.se_w = c->d_se_w;
   ga.se_b = c->d_se_b;
@@ -759,7 +799,8 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, c
     c->mark_end(COLD_PROF_FC, st);
     return;
   }
-  for (int l = 0; l < c->L - 1; l++) {
+  const int n_gemm = c->use_tail ? c->L - 4 : c->L - 1;
+  for (int l = 0; l < n_gemm; l++) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
     ep.relu = 1;
@@ -783,9 +824,25 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, c
     }
     const int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
     c->mark_begin(st);
-    launch_gemm(&c->tmA[l], &c->tmB[l], (int)n, c->widths[l], K, c->bn[l], c->precision == COLD_BF16 ? 1 : 0, ep,
-                c->num_sms, st);
+    launch_gemm(&c->tmA[l], &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
+                c->precision == COLD_BF16 ? 1 : 0, c->cs[l], c->resb[l], ep, c->num_sms, c->pdl && !c->prof, st);
     c->mark_end(COLD_PROF_FC + l, st);
+  }
+  if (c->use_tail) {
+    const int l3 = c->L - 4;
+    TailParams tp;
+    tp.b3 = c->d_b[l3];
+    tp.b4 = c->d_b[l3 + 1];
+    tp.b5 = c->d_b[l3 + 2];
+    tp.head_w = c->d_head_w;
+    tp.head_b = c->d_head_b;
+    tp.head_n = c->widths[c->L - 1];
+    tp.scores = scores_out;
+    const int K3 = (l3 == 0) ? c->d_ac_pad : c->widths[l3 - 1];
+    c->mark_begin(st);
+    launch_tail(&c->tmA[l3], &c->tmB[l3], &c->tmB[l3 + 1], &c->tmB[l3 + 2], (int)n, K3,
+                c->precision == COLD_BF16 ? 1 : 0, tp, c->num_sms, c->pdl && !c->prof, st);
+    c->mark_end(COLD_PROF_FC + l3, st);
   }
 }
 
@@ -1028,7 +1085,7 @@ extern "C" cold_status cold_get_info(const cold_ctx* c, cold_info* out) {
   out->d_user = c->d_u;
   out->d_ad = c->d_ac;
   out->chunk_ads = c->chunk;
-  out->kernels_per_chunk = 1 + (c->tensor ? c->L - 1 : 1);
+  out->kernels_per_chunk = 1 + (c->tensor ? (c->use_tail ? c->L - 3 : c->L - 1) : 1);
   out->kernels_per_call = 1;
   out->tensor_core = c->tensor ? 1 : 0;
   int64_t b = c->device_bytes;

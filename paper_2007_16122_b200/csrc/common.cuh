@@ -28,6 +28,24 @@ __device__ __forceinline__ float sigmoid(float z) {
   return e / (1.0f + e);
 }
 
+// 16-bit storage paths (2e-2 tolerance) use the MUFU intrinsics: __logf has <= 2^-21.4 absolute error on
+// the arguments (> 1) it sees here, __expf a few ulp; the fp32 path keeps logf / expf (1e-5 tolerance).
+template <bool FAST>
+__device__ __forceinline__ float linear_log_t(float x) {
+  if constexpr (FAST) {
+    const float ax = fabsf(x);
+    const float l = __logf(ax) + 1.0f;
+    return ax > 1.0f ? copysignf(l, x) : x;
+  } else {
+    return linear_log(x);
+  }
+}
+template <bool FAST>
+__device__ __forceinline__ float sigmoid_t(float z) {
+  if constexpr (FAST) return __fdividef(1.0f, 1.0f + __expf(-z));
+  else return sigmoid(z);
+}
+
 // MurmurHash3 fmix64 and the cross-feature row (DESIGN.md AMB-9):
 // row = floor(fmix64(fmix64(x ^ salt_g) ^ y) * C / 2^64), salt_g = (g+1) * 0x9E3779B97F4A7C15.
 __device__ __forceinline__ uint64_t fmix64(uint64_t k) {

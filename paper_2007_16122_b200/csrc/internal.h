@@ -34,6 +34,7 @@ struct GatherArgs {
   BatchView bv;
   int n_ac;                        // selected AD + CROSS groups
   int ac_g[COLD_MAX_GROUPS];
+  int order[COLD_MAX_GROUPS];      // blockIdx.y -> index into ac_g, heaviest group first
   int k;
   const float* se_w;
   const float* se_b;
@@ -84,16 +85,28 @@ struct EpiParams {
   const float* bias;               // [N] or null
   const float* u1; int ld_u1;      // FC1: per-request pre-activation [R][ld_u1]
   const int32_t* req_of_ad; int64_t a0;
-  void* out; int ldo;              // [M][ldo] storage dtype (null with a head)
+  void* out; int ldo;              // [M][ldo] storage dtype (null with a head); written through tmC
   const float* head_w;             // [head_n][N] fp32
   const float* head_b;             // [head_n]
   int head_n;                      // 0: no head; 1 or 2: fused last layer + sigmoid
   float* scores;                   // chunk-local [M]
   int relu;
 };
-void launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, int bn,
-                 int bf16, const EpiParams& ep, int num_sms, cudaStream_t s);
-int gemm_smem_bytes(int bn);
+cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N, int K,
+                        int bn, int bf16, int cs, bool resb, const EpiParams& ep, int num_sms, bool pdl,
+                        cudaStream_t s);
+bool gemm_resident_ok(int bn, int K);
+
+// fused FC(L-4) .. FC(L-2) + head (paper widths 256, 128, 64 -> 2)
+struct TailParams {
+  const float* b3; const float* b4; const float* b5;
+  const float* head_w; const float* head_b; int head_n;
+  float* scores;                   // chunk-local [M]
+};
+bool tail_supported(int n3, int n4, int n5, int k3);
+cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const CUtensorMap* tmB4,
+                        const CUtensorMap* tmB5, int M, int K3, int bf16, const TailParams& tp, int num_sms, bool pdl,
+                        cudaStream_t s);
 
 // top-K per request
 struct TopkArgs {

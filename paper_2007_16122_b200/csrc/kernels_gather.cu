@@ -90,13 +90,20 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// ad + cross side: grid = (ceil(n / 128), n_ac), block = 128 threads, one thread per (ad, group)
-template <typename T, int K>
+// ad + cross side: grid = (ceil(n / 128), n_ac), block = 128 threads, one thread per (ad, group).
+// blockIdx.y walks the selected AD/CROSS groups heaviest-first (cross groups over user bags carry
+// 16 rows per ad) so the long blocks start first. A cross group's user-side half of the hash,
+// hx = fmix64(x ^ salt_g), depends only on the request: a block whose 128 ads belong to one request
+// computes it once into shared memory (AMB-9: row = hi64(fmix64(hx ^ y) * C)).
+constexpr int HX_SMEM = 512;
+
+template <typename T, int K, bool FAST>
 __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a) {
+  __shared__ uint64_t s_hx[HX_SMEM];
   const int64_t local = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (local >= a.n) return;
-  const int64_t ad = a.a0 + local;
-  const int j = blockIdx.y;
+  const bool in_range = local < a.n;
+  const int64_t ad = a.a0 + (in_range ? local : a.n - 1);
+  const int j = a.order[blockIdx.y];
   const int g = a.ac_g[j];
   const DevGroup G = a.groups[g];
   const T* tab = reinterpret_cast<const T*>(G.table);
@@ -105,6 +112,7 @@ __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a) {
   for (int d = 0; d < K; d++) e[d] = 0.0f;
 
   if (G.side == 1) {                      // AD group
+    if (!in_range) return;
     const BatchGroup& B = a.bv.g[g];
     if (!G.pooled) {
       add_row<T, K>(tab, checked(B.ids[ad - B.id_shift], G.card, a.validate, a.err), e);
@@ -114,30 +122,64 @@ __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a) {
       for (int64_t i = o0; i < o1; i++) add_row<T, K>(tab, checked(B.ids[i], G.card, a.validate, a.err), e);
     }
   } else {                                // CROSS group: rows = hash(user bag x ad bag), x-major
-    const int r = a.req_of_ad[ad];
     const DevGroup U = a.groups[G.user_ref];
     const DevGroup A = a.groups[G.ad_ref];
     const BatchGroup& BU = a.bv.g[G.user_ref];
     const BatchGroup& BA = a.bv.g[G.ad_ref];
-    const int64_t u0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
-    const int64_t u1 = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift;
-    int64_t y0, y1;
-    const int32_t* yids;
-    if (!A.pooled) {
-      yids = BA.ids; y0 = ad - BA.id_shift; y1 = y0 + 1;
-    } else {
-      yids = BA.ids;
-      y0 = (int64_t)BA.offs[ad - BA.offs_shift] - BA.val_shift;
-      y1 = (int64_t)BA.offs[ad + 1 - BA.offs_shift] - BA.val_shift;
-    }
     const uint64_t salt = cross_salt(g);
     const uint64_t card = (uint64_t)G.card;
-    for (int64_t i = u0; i < u1; i++) {
-      const uint64_t x = (uint64_t)checked(BU.ids[i], U.card, a.validate, a.err);
-      const uint64_t hx = fmix64(x ^ salt);
-      for (int64_t q = y0; q < y1; q++) {
-        const uint64_t y = (uint64_t)checked(yids[q], A.card, a.validate, a.err);
-        add_row<T, K>(tab, cross_row_from_hx(hx, y, card), e);
+    // block-uniform request? then hash the user bag once into shared memory
+    const int64_t blk0 = a.a0 + (int64_t)blockIdx.x * blockDim.x;
+    const int64_t blk_end = (int64_t)(blockIdx.x + 1) * blockDim.x;
+    const int64_t blk1 = a.a0 + (blk_end < a.n ? blk_end : a.n) - 1;
+    const int rb = a.req_of_ad[blk0];
+    const int64_t ub0 = (int64_t)BU.offs[rb - BU.offs_shift] - BU.val_shift;
+    const int64_t ub1 = (int64_t)BU.offs[rb + 1 - BU.offs_shift] - BU.val_shift;
+    const bool shared_hx = (a.req_of_ad[blk1] == rb) && (ub1 - ub0 <= HX_SMEM);
+    if (shared_hx) {
+      for (int64_t i = threadIdx.x; i < ub1 - ub0; i += blockDim.x)
+        s_hx[i] = fmix64((uint64_t)checked(BU.ids[ub0 + i], U.card, a.validate, a.err) ^ salt);
+      __syncthreads();
+    }
+    if (!in_range) return;
+    const int r = shared_hx ? rb : a.req_of_ad[ad];
+    const int64_t u0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
+    const int64_t u1 = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift;
+    const int L = (int)(u1 - u0);
+    auto hx_at = [&](int i) -> uint64_t {
+      return shared_hx ? s_hx[i] : fmix64((uint64_t)checked(BU.ids[u0 + i], U.card, a.validate, a.err) ^ salt);
+    };
+    if (!A.pooled) {
+      const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
+      int i = 0;
+      constexpr int U4 = 4;               // 4 rows in flight per thread, then summed in bag order
+      for (; i + U4 <= L; i += U4) {
+        int64_t rows[U4];
+#pragma unroll
+        for (int t = 0; t < U4; t++) rows[t] = cross_row_from_hx(hx_at(i + t), y, card);
+        float v[U4][K];
+#pragma unroll
+        for (int t = 0; t < U4; t++) {
+#pragma unroll
+          for (int d = 0; d < K; d++) v[t][d] = 0.0f;
+          add_row<T, K>(tab, rows[t], v[t]);
+        }
+#pragma unroll
+        for (int t = 0; t < U4; t++) {
+#pragma unroll
+          for (int d = 0; d < K; d++) e[d] += v[t][d];
+        }
+      }
+      for (; i < L; i++) add_row<T, K>(tab, cross_row_from_hx(hx_at(i), y, card), e);
+    } else {
+      const int64_t y0 = (int64_t)BA.offs[ad - BA.offs_shift] - BA.val_shift;
+      const int64_t y1 = (int64_t)BA.offs[ad + 1 - BA.offs_shift] - BA.val_shift;
+      for (int i = 0; i < L; i++) {
+        const uint64_t hx = hx_at(i);
+        for (int64_t q = y0; q < y1; q++) {
+          const uint64_t y = (uint64_t)checked(BA.ids[q], A.card, a.validate, a.err);
+          add_row<T, K>(tab, cross_row_from_hx(hx, y, card), e);
+        }
       }
     }
   }
@@ -149,12 +191,12 @@ __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a) {
   // linear_log -> SE gate s = sigma(w . ê + b) -> v = s ê (fp32), then RNE to storage
   if (a.linear_log) {
 #pragma unroll
-    for (int d = 0; d < K; d++) e[d] = linear_log(e[d]);
+    for (int d = 0; d < K; d++) e[d] = linear_log_t<FAST>(e[d]);
   }
   float z = 0.0f;
 #pragma unroll
   for (int d = 0; d < K; d++) z = fmaf(__ldg(a.se_w + g * K + d), e[d], z);
-  const float s = sigmoid(z + __ldg(a.se_b + g));
+  const float s = sigmoid_t<FAST>(z + __ldg(a.se_b + g));
   alignas(16) T out[K];
 #pragma unroll
   for (int d = 0; d < K; d++) out[d] = Store<T>::from_f(s * e[d]);
@@ -228,23 +270,23 @@ void launch_user(const UserArgs& a, int R, int precision, cudaStream_t s) {
   else user_dispatch<__nv_bfloat16>(a, R, s);
 }
 
-template <typename T>
+template <typename T, bool FAST>
 static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
   dim3 grid((unsigned)((a.n + 127) / 128), (unsigned)a.n_ac);
   switch (a.k) {
-    case 2: gather_kernel<T, 2><<<grid, 128, 0, s>>>(a); break;
-    case 4: gather_kernel<T, 4><<<grid, 128, 0, s>>>(a); break;
-    case 8: gather_kernel<T, 8><<<grid, 128, 0, s>>>(a); break;
-    case 16: gather_kernel<T, 16><<<grid, 128, 0, s>>>(a); break;
-    case 32: gather_kernel<T, 32><<<grid, 128, 0, s>>>(a); break;
+    case 2: gather_kernel<T, 2, FAST><<<grid, 128, 0, s>>>(a); break;
+    case 4: gather_kernel<T, 4, FAST><<<grid, 128, 0, s>>>(a); break;
+    case 8: gather_kernel<T, 8, FAST><<<grid, 128, 0, s>>>(a); break;
+    case 16: gather_kernel<T, 16, FAST><<<grid, 128, 0, s>>>(a); break;
+    case 32: gather_kernel<T, 32, FAST><<<grid, 128, 0, s>>>(a); break;
   }
 }
 
 void launch_gather(const GatherArgs& a, int precision, cudaStream_t s) {
   if (a.n <= 0 || a.n_ac <= 0) return;
-  if (precision == 0) gather_dispatch<float>(a, s);
-  else if (precision == 1) gather_dispatch<__half>(a, s);
-  else gather_dispatch<__nv_bfloat16>(a, s);
+  if (precision == 0) gather_dispatch<float, false>(a, s);
+  else if (precision == 1) gather_dispatch<__half, true>(a, s);
+  else gather_dispatch<__nv_bfloat16, true>(a, s);
 }
 
 void launch_rows(const RowsArgs& a, cudaStream_t s) {

@@ -5,171 +5,102 @@
 // PAPER.md L328 (§4.1): FCN D_in x 1024 x 512 x 256 x 128 x 64 x 2; L276 "fully-connected layers
 // use Float16"; L517 (Doc C) "involves almost only dense matrix multiplication, which needs
 // extreme optimization". The paper ran fp16 HMMA on a T4 through an in-house engine; here each
-// layer is a persistent, warp-specialised tcgen05 kernel:
-//   warp 0      : TMA producer  (cp.async.bulk.tensor, 128 B swizzle, mbarrier complete_tx)
-//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per op)
-//   warps 2..5  : epilogue — tcgen05.ld (32x32b) -> +bias [+ u1[request]] -> ReLU -> RNE cast
-//                 -> global; for the penultimate layer the last (1- or 2-wide) layer and the
-//                 sigmoid are fused here and only the fp32 score leaves the kernel.
+// layer is a persistent, warp-specialised tcgen05 kernel launched as clusters of CS CTAs:
+//   warp 0      : TMA producer. A (own 128 rows) is loaded per CTA; the weight tile B is split in
+//                 CS row slices, each CTA loads one slice and multicasts it to the whole cluster,
+//                 so L2 serves every weight byte once per cluster instead of once per CTA (the
+//                 1-CTA kernel was L2-bandwidth bound: 87 FLOP/B at K=1024).
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16 per op).
+//                 Its tcgen05.commit arrives on the stage's "empty" barrier of every CTA of the
+//                 cluster (a slice is only overwritten once all CTAs have consumed it).
+//   warps 2..9  : epilogue, two warps per TMEM lane quadrant (each owns half the columns):
+//                 tcgen05.ld (32x32b) -> +bias [+ u1[request]] -> ReLU -> RNE cast -> 64B-swizzled
+//                 shared tile -> TMA store (coalesced lines, rows past M clipped by the TMA unit).
+//                 For the penultimate layer the last (1- or 2-wide) layer and the sigmoid are fused
+//                 here instead and only the fp32 score leaves the kernel.
 // The fp32 accumulator is double-buffered in TMEM (2 x BN columns) so the epilogue of tile t
 // overlaps the mainloop of tile t+1.
 #include <cuda.h>
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace cold {
 
-constexpr int BM = 128;        // UMMA M (cta_group::1)
-constexpr int BK = 64;         // K per stage: 64 x 16-bit = 128 B rows = one SW128 atom
-constexpr int UMMA_K = 16;
-constexpr int GEMM_THREADS = 192;
+constexpr int EPI_WARPS = 8;
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int EPI_COLS = 32;   // columns per TMEM load / TMA store box
+constexpr int STAGE_OUT_BYTES = 32 * EPI_COLS * 2;   // one 32-row x 32-col fp16 box (2 KB)
+constexpr int SMEM_LIMIT = 232448;                   // 227 KB opt-in per CTA
+constexpr int RES_B_BYTES = 128 * 1024;              // resident weight slice budget
 
-template <int BN> struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+// RESB = false: A and B stream through a ring of stages (B optionally multicast in a cluster).
+// RESB = true : the CTA owns one n-tile for the whole launch; its K x BN weight slice (<= 128 KB)
+//               is loaded into shared memory once and only A streams (FC1: K=256, BN=256).
+template <int BN, bool RESB> struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGE_BYTES = RESB ? A_BYTES : A_BYTES + B_BYTES;
+  static constexpr int RES_BYTES = RESB ? RES_B_BYTES : 0;
+  static constexpr int OUT_BYTES = EPI_WARPS * 2 * STAGE_OUT_BYTES;          // double-buffered per warp
+  static constexpr int STAGES_FIT = (SMEM_LIMIT - RES_BYTES - OUT_BYTES - 1024 - 512) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN;  // power of two >= 32
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-};
-
-// ---- PTX wrappers ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t addr = smem_u32(bar);
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// SMEM matrix descriptor, K-major, 128 B swizzle (tcgen05 "version 1" format):
-// start>>4 [0,14) | LBO>>4 [16,30) (unused for swizzled K-major, 1) | SBO>>4 [32,46) = 1024 B
-// (8 rows x 128 B) | version 1 [46,48) | base offset 0 | layout SWIZZLE_128B = 2 at [61,64).
-__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)(1024 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-
-// Instruction descriptor, kind::f16: D fp32 [4,6)=1, A/B format [7,10)/[10,13) (0 f16, 1 bf16),
-// K-major A and B, N>>3 at [17,23), M>>4 at [24,29).
-template <int BN, bool BF16>
-__device__ __forceinline__ constexpr uint32_t idesc_f16() {
-  return (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) | ((uint32_t)(BN >> 3) << 17) |
-         ((uint32_t)(BM >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-               : "memory");
-}
-
-#define TMEM_LD32(taddr, v)                                                                                  \
-  asm volatile(                                                                                              \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"       \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                             \
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),      \
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), \
-        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),           \
-        "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),           \
-        "=r"(v[30]), "=r"(v[31])                                                                             \
-      : "r"(taddr))
-
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-template <bool BF16> struct Pack;
-template <> struct Pack<false> {
-  static __device__ __forceinline__ uint32_t two(float a, float b) {
-    __half2 h = __floats2half2_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
-};
-template <> struct Pack<true> {
-  static __device__ __forceinline__ uint32_t two(float a, float b) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-  }
+  static constexpr int SMEM = RES_BYTES + STAGES * STAGE_BYTES + OUT_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 // ---------------------------------------------------------------------------------------------
-template <int BN, bool BF16>
+template <int BN, bool BF16, int CS, bool RESB>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                int K, EpiParams ep) {
-  using Cfg = GemmCfg<BN>;
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, int M, int N, int K, EpiParams ep) {
+  using Cfg = GemmCfg<BN, RESB>;
+  static_assert(!RESB || CS == 1, "resident-B mode runs without clusters");
+  constexpr int B_SLICE_ROWS = BN / CS;
+  constexpr int B_SLICE_BYTES = B_SLICE_ROWS * BK * 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sRes = smem;                                   // resident B: [K/64][BN rows x 128 B]
+  uint8_t* sA = smem + Cfg::RES_BYTES;
+  uint8_t* sB = sA + Cfg::STAGES * Cfg::A_BYTES;          // streaming B (RESB = false)
+  uint8_t* sOut = smem + Cfg::RES_BYTES + Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + Cfg::OUT_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + Cfg::STAGES;
   uint64_t* tfull = bars + 2 * Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* bres = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + BM - 1) / BM, num_n = N / BN;
-  const int num_tiles = num_m * num_n;
   const int kb_count = K / BK;
+  // work decomposition. streaming: items = (CS m-tiles) x n-tile, clusters walk the item list.
+  // resident: CTA -> fixed n-tile (blockIdx % num_n), m-tiles strided by the CTAs sharing it.
+  const uint32_t crank = (CS > 1) ? cluster_rank() : 0;
+  int first, stride, count;
+  if (RESB) {
+    const int groups = gridDim.x / num_n;
+    first = blockIdx.x / num_n;
+    stride = groups;
+    count = num_m;
+  } else {
+    first = (CS > 1) ? (int)cluster_id_x() : blockIdx.x;
+    stride = (CS > 1) ? (int)num_clusters_x() : gridDim.x;
+    count = ((num_m + CS - 1) / CS) * num_n;
+  }
+  auto tile_of = [&](int it, int& mb, int& nb) {
+    if (RESB) { mb = it; nb = blockIdx.x % num_n; }
+    else { mb = (it / num_n) * CS + (int)crank; nb = it % num_n; }
+  };
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; s++) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], CS); }
+    for (int s = 0; s < 2; s++) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
+    mbar_init(bres, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+    if (ep.out) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmC) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -178,24 +109,41 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  if (CS > 1) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();   // everything below reads or writes memory shared with the previous kernels
 
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer =====
-      const uint64_t pol_a = policy_evict_first();   // activations: streamed once per N tile
+      const uint64_t pol_a = policy_evict_first();   // activations: streamed
       const uint64_t pol_b = policy_evict_last();    // weights: reused by every M tile
+      if (RESB) {
+        int nb0, mb0;
+        tile_of(first, mb0, nb0);
+        mbar_expect_tx(bres, (uint32_t)(kb_count * Cfg::B_BYTES));
+        for (int kb = 0; kb < kb_count; kb++)
+          tma_load_2d(sRes + kb * Cfg::B_BYTES, &tmB, bres, kb * BK, nb0 * BN, pol_b);
+      }
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-        const int mb = t / num_n, nb = t % num_n;
+      for (int it = first; it < count; it += stride) {
+        int mb, nb;
+        tile_of(it, mb, nb);
         for (int kb = 0; kb < kb_count; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
           tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK, mb * BM, pol_a);
-          tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, nb * BN, pol_b);
+          if (!RESB) {
+            uint8_t* dstB = sB + s * Cfg::B_BYTES + crank * B_SLICE_BYTES;
+            if (CS > 1)
+              tma_load_2d_mc(dstB, &tmB, &full[s], kb * BK, nb * BN + (int)crank * B_SLICE_ROWS,
+                             (uint16_t)((1u << CS) - 1u), pol_b);
+            else
+              tma_load_2d(dstB, &tmB, &full[s], kb * BK, nb * BN, pol_b);
+          }
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -204,10 +152,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       // ===== MMA issuer (one thread) =====
       constexpr uint32_t idesc = idesc_f16<BN, BF16>();
+      if (RESB) mbar_wait(bres, 0);
       int s = 0;
       uint32_t ph = 0;
       int lt = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, lt++) {
+      for (int it = first; it < count; it += stride, lt++) {
         const int acc = lt & 1;
         mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -216,26 +165,37 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + s * Cfg::A_BYTES));
-          const uint64_t bd = sdesc_sw128(smem_u32(sB + s * Cfg::B_BYTES));
+          const uint64_t bd = sdesc_sw128(smem_u32(RESB ? sRes + kb * Cfg::B_BYTES : sB + s * Cfg::B_BYTES));
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; kk++)   // +32 B along K inside the swizzle atom
             umma_f16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
-          umma_commit(&empty[s]);
+          if (CS > 1) umma_commit_mc(&empty[s], (uint16_t)((1u << CS) - 1u));
+          else umma_commit(&empty[s]);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
         umma_commit(&tfull[acc]);
       }
     }
   } else {
-    // ===== epilogue warps 2..5: TMEM lanes [32*(warp%4), +32) =====
+    // ===== epilogue warps 2..9: TMEM lane quadrant q, column half h =====
+    const int ew = warp - 2;
     const int q = warp & 3;
+    const int h = ew >> 2;
+    const bool head = ep.head_n != 0;
+    // with a fused head one warp per quadrant walks all columns (the row's dot product stays in-thread)
+    const int c_begin = head ? 0 : h * (BN / 2);
+    const int c_end = head ? (h == 0 ? BN : 0) : (h + 1) * (BN / 2);
+    uint8_t* my_out = sOut + ew * 2 * STAGE_OUT_BYTES;
+    int ob = 0;
     int lt = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, lt++) {
-      const int mb = t / num_n, nb = t % num_n;
+    for (int it = first; it < count; it += stride, lt++) {
+      int mb, nb;
+      tile_of(it, mb, nb);
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
+      const int row0 = mb * BM + q * 32;
+      const int row = row0 + lane;
       const bool valid = row < M;
       const float* u1row = nullptr;
       if (ep.u1) {
@@ -245,7 +205,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       float z0 = 0.0f, z1 = 0.0f;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = c_begin; c < c_end; c += EPI_COLS) {
         uint32_t v[32];
         TMEM_LD32(taddr + c, v);
         tmem_wait_ld();
@@ -271,39 +231,51 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 32; i++) f[i] = fmaxf(f[i], 0.0f);
         }
-        if (ep.head_n) {
+        if (head) {
 #pragma unroll
           for (int i = 0; i < 32; i++) z0 = fmaf(__ldg(ep.head_w + col0 + i), f[i], z0);
           if (ep.head_n == 2) {
 #pragma unroll
             for (int i = 0; i < 32; i++) z1 = fmaf(__ldg(ep.head_w + N + col0 + i), f[i], z1);
           }
-        } else if (valid) {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(ep.out) + (int64_t)row * ep.ldo + col0);
+        } else {
+          // 32 x 32 box, 64 B rows, SWIZZLE_64B: 16 B chunk j of row r sits at j ^ ((r >> 1) & 3)
+          uint8_t* buf = my_out + ob * STAGE_OUT_BYTES;
+          if (lane == 0) bulk_wait_read<1>();   // the store issued from this buffer 2 boxes ago has read it
+          __syncwarp();
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
+          for (int j = 0; j < 4; j++) {
             uint4 w;
-            w.x = Pack<BF16>::two(f[i], f[i + 1]);
-            w.y = Pack<BF16>::two(f[i + 2], f[i + 3]);
-            w.z = Pack<BF16>::two(f[i + 4], f[i + 5]);
-            w.w = Pack<BF16>::two(f[i + 6], f[i + 7]);
-            dst[i / 8] = w;
+            w.x = Pack<BF16>::two(f[8 * j + 0], f[8 * j + 1]);
+            w.y = Pack<BF16>::two(f[8 * j + 2], f[8 * j + 3]);
+            w.z = Pack<BF16>::two(f[8 * j + 4], f[8 * j + 5]);
+            w.w = Pack<BF16>::two(f[8 * j + 6], f[8 * j + 7]);
+            const int phys = j ^ ((lane >> 1) & 3);
+            *reinterpret_cast<uint4*>(buf + lane * 64 + phys * 16) = w;
           }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmC, buf, col0, row0);
+            bulk_commit();
+          }
+          ob ^= 1;
         }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (ep.head_n && valid) {
+      if (head && h == 0 && valid) {
         float z;
         if (ep.head_n == 2) z = (z1 + ep.head_b[1]) - (z0 + ep.head_b[0]);
         else z = z0 + ep.head_b[0];
         ep.scores[row] = sigmoid(z);
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
-  __syncthreads();
+  if (CS > 1) cluster_sync(); else __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS)
@@ -311,39 +283,97 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-int gemm_smem_bytes(int bn) {
-  switch (bn) {
-    case 256: return GemmCfg<256>::SMEM;
-    case 128: return GemmCfg<128>::SMEM;
-    default: return GemmCfg<64>::SMEM;
-  }
-}
-
-template <int BN, bool BF16>
-static void launch_t(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, const EpiParams& ep,
-                     int num_sms, cudaStream_t s) {
+template <int BN, bool BF16, int CS, bool RESB>
+static cudaError_t launch_t(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N,
+                            int K, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s) {
+  using Cfg = GemmCfg<BN, RESB>;
   static bool attr = false;
+  auto kern = gemm_kernel<BN, BF16, CS, RESB>;
   if (!attr) {
-    cudaFuncSetAttribute(gemm_kernel<BN, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, GemmCfg<BN>::SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (CS > 1) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * (N / BN);
-  const int grid = tiles < num_sms ? tiles : num_sms;
-  gemm_kernel<BN, BF16><<<grid, GEMM_THREADS, GemmCfg<BN>::SMEM, s>>>(*tmA, *tmB, M, N, K, ep);
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = N / BN;
+  int grid;
+  if (RESB) {
+    int groups = num_sms / num_n;
+    if (groups > num_m) groups = num_m;
+    if (groups < 1) groups = 1;
+    grid = groups * num_n;
+  } else {
+    const int items = ((num_m + CS - 1) / CS) * num_n;
+    static int max_clusters = 0;
+    if (max_clusters == 0) {
+      max_clusters = num_sms / CS;
+      if (CS > 1) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(CS * max_clusters);
+        q.blockDim = dim3(GEMM_THREADS);
+        q.dynamicSmemBytes = Cfg::SMEM;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = CS;
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        q.attrs = qa;
+        q.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &q) == cudaSuccess && n > 0) max_clusters = n;
+        cudaGetLastError();
+      }
+    }
+    grid = CS * (items < max_clusters ? items : max_clusters);
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[2];
+  int na = 0;
+  if (CS > 1) {
+    attrs[na].id = cudaLaunchAttributeClusterDimension;
+    attrs[na].val.clusterDim.x = CS;
+    attrs[na].val.clusterDim.y = 1;
+    attrs[na].val.clusterDim.z = 1;
+    na++;
+  }
+  if (pdl) {
+    attrs[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[na].val.programmaticStreamSerializationAllowed = 1;
+    na++;
+  }
+  cfg.attrs = attrs;
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, *tmC, M, N, K, ep);
 }
 
-void launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, int M, int N, int K, int bn, int bf16,
-                 const EpiParams& ep, int num_sms, cudaStream_t s) {
-  if (M <= 0) return;
+bool gemm_resident_ok(int bn, int K) { return (int64_t)bn * K * 2 <= RES_B_BYTES; }
+
+template <int BN, bool BF16>
+static cudaError_t launch_mode(int cs, bool resb, const CUtensorMap* tmA, const CUtensorMap* tmB,
+                               const CUtensorMap* tmC, int M, int N, int K, const EpiParams& ep, int num_sms, bool pdl,
+                               cudaStream_t s) {
+  if (resb) return launch_t<BN, BF16, 1, true>(tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
+  if (cs == 4) return launch_t<BN, BF16, 4, false>(tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
+  if (cs == 2) return launch_t<BN, BF16, 2, false>(tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
+  return launch_t<BN, BF16, 1, false>(tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
+}
+
+cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N, int K,
+                        int bn, int bf16, int cs, bool resb, const EpiParams& ep, int num_sms, bool pdl,
+                        cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
   if (bf16) {
-    if (bn == 256) launch_t<256, true>(tmA, tmB, M, N, K, ep, num_sms, s);
-    else if (bn == 128) launch_t<128, true>(tmA, tmB, M, N, K, ep, num_sms, s);
-    else launch_t<64, true>(tmA, tmB, M, N, K, ep, num_sms, s);
-  } else {
-    if (bn == 256) launch_t<256, false>(tmA, tmB, M, N, K, ep, num_sms, s);
-    else if (bn == 128) launch_t<128, false>(tmA, tmB, M, N, K, ep, num_sms, s);
-    else launch_t<64, false>(tmA, tmB, M, N, K, ep, num_sms, s);
+    if (bn == 256) return launch_mode<256, true>(cs, resb, tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
+    if (bn == 128) return launch_mode<128, true>(cs, resb, tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
+    return launch_mode<64, true>(cs, resb, tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
   }
+  if (bn == 256) return launch_mode<256, false>(cs, resb, tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
+  if (bn == 128) return launch_mode<128, false>(cs, resb, tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
+  return launch_mode<64, false>(cs, resb, tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);
 }
 
 }  // namespace cold
