@@ -233,7 +233,8 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2007_16122_b200 import Batch, Context
-    from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER, PROF_KINDS, PROF_TOPK, PROF_USER
+    from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER, PROF_TOPK, PROF_USER
+    from paper_2007_16122_b200.dist import gather_topk, request_block
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -246,8 +247,7 @@ def main():
     sch = schema_for(args)
     t_setup = time.perf_counter()
     params = coldgen.make_params(sch, seed=args.seed, precision=args.precision)
-    r0 = rank * args.requests
-    batch = coldgen.make_batch(sch, range(r0, r0 + args.requests), args.ads, seed=args.seed + 1)
+    batch = coldgen.make_batch(sch, request_block(args.requests, rank), args.ads, seed=args.seed + 1)
     N = batch.n_ads
     ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, device=local, max_ads=N,
                   max_requests=args.requests, chunk_ads=args.chunk)
@@ -266,8 +266,7 @@ def main():
         ctx.score_batch(b, scores)
         ctx.topk(scores, db.ad_offsets, batch.ad_offsets, K, out_idx, out_key)
         if world > 1:
-            dist.all_gather_into_tensor(g_idx, idx)
-            dist.all_gather_into_tensor(g_key, key)
+            gather_topk(idx, key, g_idx, g_key)
 
     def timed(b, out_idx, out_key, steps, sampler=None, profile=False):
         for _ in range(args.warmup):
@@ -382,8 +381,7 @@ def main():
             ctx.score_batch(hb, scores)
             ctx.topk(scores, db.ad_offsets, batch.ad_offsets, K, h_idx, h_key)
             if world > 1:
-                dist.all_gather_into_tensor(g_idx, idx)
-                dist.all_gather_into_tensor(g_key, key)
+                gather_topk(idx, key, g_idx, g_key)
 
         # same procedure as `timed`
         for _ in range(args.warmup):

@@ -337,7 +337,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   } else {
     c->d_ac_pad = std::max(1, c->d_ac);
   }
-  int chunk = cfg->chunk_ads > 0 ? cfg->chunk_ads : c->num_sms * 128 * 2;
+  int chunk = cfg->chunk_ads > 0 ? cfg->chunk_ads : c->num_sms * 128 * 8;
   if (c->tensor) chunk = (chunk + 127) / 128 * 128;
   c->chunk = (int)std::min<int64_t>(chunk, std::max<int64_t>(c->max_ads, 128));
   if (c->tensor) c->chunk = (c->chunk + 127) / 128 * 128;
