@@ -25,6 +25,7 @@
 using namespace cold;
 
 static thread_local std::string g_last_error;
+static unsigned long long* g_instr = nullptr;   // debug wait-cycle counters (COLD_INSTR)
 
 static cold_status fail(cold_status s, const std::string& msg) {
   g_last_error = msg;
@@ -91,11 +92,13 @@ struct cold_ctx {
   CUtensorMap tmC[COLD_MAX_LAYERS];  // epilogue TMA-store maps (32 x 32 boxes)
   int cs[COLD_MAX_LAYERS] = {0};     // cluster size (weight-tile multicast) per GEMM layer
   bool resb[COLD_MAX_LAYERS] = {false};  // weight slice resident in shared memory (K x BN <= 128 KB)
+  bool pair[COLD_MAX_LAYERS] = {false};  // CTA-pair (cta_group::2) GEMM
   bool use_tail = false;             // last three hidden layers + head in one fused kernel
   bool pdl = true;                   // programmatic dependent launch between the GEMM kernels
   int* d_err = nullptr;
   float* d_scores_stage = nullptr;  // [2][chunk] for host outputs
   int32_t* d_adoff = nullptr;       // [max_req+1] staged ad offsets
+  const int32_t* cur_adoff = nullptr;  // device ad offsets of the call in flight
   // host-batch staging
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
@@ -388,6 +391,13 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       c->cs[l] = (cs == 4 || cs == 2) ? cs : 1;
       if (c->use_tail && l >= Lg - 3) c->cs[l] = 1;          // the tail kernel loads whole weight tiles
       c->resb[l] = c->cs[l] == 1 && gemm_resident_ok(c->bn[l], K) && !(env_resb && atoi(env_resb) == 0);
+      // CTA pairs for the 256-wide layers that are not fused into the tail (FC1, FC2)
+      const char* env_pair = getenv("COLD_PAIR");
+      const int pair_mode = env_pair ? atoi(env_pair) : 1;   // 0 off, 1 non-resident 256-wide, 2 all 256-wide
+      const bool in_tail = c->use_tail && l >= Lg - 3;
+      c->pair[l] = !in_tail && l < Lg - 1 && c->bn[l] == 256 &&
+                   (pair_mode == 2 || (pair_mode == 1 && !c->resb[l]));
+      if (c->pair[l]) { c->resb[l] = false; c->cs[l] = 1; }
     }
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -546,7 +556,8 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
         s = upload(c, (void**)&c->d_b[l], sizeof(float) * out, [&](uint8_t* h) { memcpy(h, p->fc_b[l], sizeof(float) * out); });
         if (s) return s;
       }
-      s = make_tmap(&c->tmB[l], c->d_w[l], c->precision, Kp, out, c->bn[l] / c->cs[l]);
+      s = make_tmap(&c->tmB[l], c->d_w[l], c->precision, Kp, out,
+                    c->pair[l] ? c->bn[l] / 2 : c->bn[l] / c->cs[l]);
       if (s) return s;
     }
     const int hl = c->L - 1, hin = c->widths[hl - 1], hout = c->widths[hl];
@@ -800,6 +811,11 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, c
     return;
   }
   const int n_gemm = c->use_tail ? c->L - 4 : c->L - 1;
+  static bool instr_on = getenv("COLD_INSTR") != nullptr;
+  if (instr_on && !g_instr) {
+    cudaMalloc(&g_instr, 8 * 8 * COLD_MAX_LAYERS);
+    cudaMemset(g_instr, 0, 8 * 8 * COLD_MAX_LAYERS);
+  }
   for (int l = 0; l < n_gemm; l++) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
@@ -809,6 +825,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, c
       ep.ld_u1 = c->widths[0];
       ep.req_of_ad = c->d_req;
       ep.a0 = a0;
+      ep.ad_offsets = c->cur_adoff;
     } else {
       ep.bias = c->d_b[l];
     }
@@ -823,9 +840,14 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, c
       ep.ldo = c->widths[l];
     }
     const int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
+    ep.instr = instr_on ? g_instr + 8 * l : nullptr;
     c->mark_begin(st);
-    launch_gemm(&c->tmA[l], &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
-                c->precision == COLD_BF16 ? 1 : 0, c->cs[l], c->resb[l], ep, c->num_sms, c->pdl && !c->prof, st);
+    if (c->pair[l])
+      launch_gemm_pair(&c->tmA[l], &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
+                       c->precision == COLD_BF16 ? 1 : 0, ep, c->num_sms, c->pdl && !c->prof, st);
+    else
+      launch_gemm(&c->tmA[l], &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
+                  c->precision == COLD_BF16 ? 1 : 0, c->cs[l], c->resb[l], ep, c->num_sms, c->pdl && !c->prof, st);
     c->mark_end(COLD_PROF_FC + l, st);
   }
   if (c->use_tail) {
@@ -863,6 +885,7 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
     d_adoff = c->d_adoff;
   }
   const bool scores_dev = mode == RUN_SCORE && is_device_ptr(scores);
+  c->cur_adoff = d_adoff;
   UserArgs ua = make_user_args(c, pl, d_adoff, dbg);
   c->mark_begin(st);
   launch_user(ua, pl.R, c->precision, st);
@@ -1057,6 +1080,17 @@ extern "C" cold_status cold_topk(cold_ctx* c, const float* scores, const int32_t
     CK(cudaMemcpyAsync(key_out, ta.key, (size_t)R * K * 4, cudaMemcpyDeviceToHost, st));
   }
   return COLD_OK;
+}
+
+// debug: read (and reset) the GEMM wait-cycle counters recorded when COLD_INSTR is set.
+// out[8 * layer + i]: 0 producer empty-wait, 1 MMA full-wait, 2 MMA tmem-empty-wait, 3 MMA resident-B
+// wait, 4 epilogue tmem-full-wait (per warp), 5 epilogue u1 wait, 6 epilogue warps, 7 producer total.
+extern "C" int cold_debug_instr(unsigned long long* out, int n) {
+  if (!g_instr) return 0;
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, g_instr, sizeof(unsigned long long) * (size_t)n, cudaMemcpyDeviceToHost);
+  cudaMemset(g_instr, 0, sizeof(unsigned long long) * 8 * COLD_MAX_LAYERS);
+  return 1;
 }
 
 extern "C" cold_status cold_profile(cold_ctx* c, int32_t enable) {

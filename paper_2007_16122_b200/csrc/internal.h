@@ -85,17 +85,22 @@ struct EpiParams {
   const float* bias;               // [N] or null
   const float* u1; int ld_u1;      // FC1: per-request pre-activation [R][ld_u1]
   const int32_t* req_of_ad; int64_t a0;
+  const int32_t* ad_offsets;       // FC1: call-global [R+1] (request boundary inside a tile)
   void* out; int ldo;              // [M][ldo] storage dtype (null with a head); written through tmC
   const float* head_w;             // [head_n][N] fp32
   const float* head_b;             // [head_n]
   int head_n;                      // 0: no head; 1 or 2: fused last layer + sigmoid
   float* scores;                   // chunk-local [M]
   int relu;
+  unsigned long long* instr;       // debug: per-role wait-cycle counters [8] (null = off)
 };
 cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N, int K,
                         int bn, int bf16, int cs, bool resb, const EpiParams& ep, int num_sms, bool pdl,
                         cudaStream_t s);
 bool gemm_resident_ok(int bn, int K);
+// CTA-pair (cta_group::2) variant: 256-row tiles, each CTA stages half of the weight tile
+cudaError_t launch_gemm_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N,
+                             int K, int bn, int bf16, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s);
 
 // fused FC(L-4) .. FC(L-2) + head (paper widths 256, 128, 64 -> 2)
 struct TailParams {

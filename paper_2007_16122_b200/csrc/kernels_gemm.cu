@@ -42,11 +42,22 @@ template <int BN, bool RESB> struct GemmCfg {
   static constexpr int STAGE_BYTES = RESB ? A_BYTES : A_BYTES + B_BYTES;
   static constexpr int RES_BYTES = RESB ? RES_B_BYTES : 0;
   static constexpr int OUT_BYTES = EPI_WARPS * 2 * STAGE_OUT_BYTES;          // double-buffered per warp
-  static constexpr int STAGES_FIT = (SMEM_LIMIT - RES_BYTES - OUT_BYTES - 1024 - 512) / STAGE_BYTES;
+  // staged u1 rows of FC1 (resident-weight mode only; streaming mode reads u1 from global)
+  static constexpr int U1_BYTES = RESB ? 2 /*acc buffers*/ * 2 /*requests*/ * BN * 4 : 0;
+  static constexpr int STAGES_FIT = (SMEM_LIMIT - RES_BYTES - OUT_BYTES - U1_BYTES - 1024 - 512) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN;  // power of two >= 32
-  static constexpr int SMEM = RES_BYTES + STAGES * STAGE_BYTES + OUT_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int SMEM =
+      RES_BYTES + STAGES * STAGE_BYTES + OUT_BYTES + U1_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 };
+
+// debug instrumentation: cycles a role spent blocked in a barrier wait
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, unsigned long long& acc, bool on) {
+  if (!on) { mbar_wait(bar, parity); return; }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  acc += (unsigned long long)(clock64() - t0);
+}
 
 // ---------------------------------------------------------------------------------------------
 template <int BN, bool BF16, int CS, bool RESB>
@@ -63,13 +74,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* sA = smem + Cfg::RES_BYTES;
   uint8_t* sB = sA + Cfg::STAGES * Cfg::A_BYTES;          // streaming B (RESB = false)
   uint8_t* sOut = smem + Cfg::RES_BYTES + Cfg::STAGES * Cfg::STAGE_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + Cfg::OUT_BYTES);
+  float* sU1 = reinterpret_cast<float*>(sOut + Cfg::OUT_BYTES);              // [2 acc][2 req][BN]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + Cfg::OUT_BYTES + Cfg::U1_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + Cfg::STAGES;
   uint64_t* tfull = bars + 2 * Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* bres = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
+  uint64_t* u1full = bres + 1;                                              // [2]
+  int32_t* u1hdr = reinterpret_cast<int32_t*>(u1full + 2);                  // [2]: row boundary or -1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u1hdr + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (M + BM - 1) / BM, num_n = N / BN;
@@ -97,6 +111,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], CS); }
     for (int s = 0; s < 2; s++) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
     mbar_init(bres, 1);
+    mbar_init(&u1full[0], 1);
+    mbar_init(&u1full[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
@@ -129,11 +145,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       int s = 0;
       uint32_t ph = 0;
-      for (int it = first; it < count; it += stride) {
+      int lt = 0;
+      const bool ins = ep.instr != nullptr;
+      unsigned long long w_empty = 0;
+      const long long t_start = clock64();
+      for (int it = first; it < count; it += stride, lt++) {
         int mb, nb;
         tile_of(it, mb, nb);
         for (int kb = 0; kb < kb_count; kb++) {
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_t(&empty[s], ph ^ 1, w_empty, ins);
           mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
           tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK, mb * BM, pol_a);
           if (!RESB) {
@@ -146,23 +166,48 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
+        if (RESB && ep.u1) {
+          // FC1: stage this tile's u1 row slice(s) [nb*BN, +BN) into smem (<= 2 requests per tile;
+          // more -> epilogue falls back to global loads). Buffer `acc` is free once tempty[acc] flips.
+          const int acc = lt & 1;
+          mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+          const int rlo = mb * BM, rhi = min(M, rlo + BM) - 1;
+          const int r0 = rlo < M ? ep.req_of_ad[ep.a0 + rlo] : 0;
+          const int r1 = rlo < M ? ep.req_of_ad[ep.a0 + rhi] : 0;
+          float* dst = sU1 + acc * 2 * BN;
+          if (rlo < M && r1 - r0 <= 1) {
+            u1hdr[acc] = (r1 != r0) ? (int)(ep.ad_offsets[r1] - ep.a0 - rlo) : BM;
+            mbar_expect_tx(&u1full[acc], (uint32_t)(BN * 4 * (1 + (r1 != r0))));
+            bulk_load(dst, ep.u1 + (int64_t)r0 * ep.ld_u1 + nb * BN, BN * 4, &u1full[acc]);
+            if (r1 != r0) bulk_load(dst + BN, ep.u1 + (int64_t)r1 * ep.ld_u1 + nb * BN, BN * 4, &u1full[acc]);
+          } else {
+            u1hdr[acc] = -1;
+            mbar_arrive(&u1full[acc]);
+          }
+        }
+      }
+      if (ins) {
+        atomicAdd(ep.instr + 0, w_empty);
+        atomicAdd(ep.instr + 7, (unsigned long long)(clock64() - t_start));
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ===== MMA issuer (one thread) =====
       constexpr uint32_t idesc = idesc_f16<BN, BF16>();
-      if (RESB) mbar_wait(bres, 0);
+      const bool ins = ep.instr != nullptr;
+      unsigned long long w_full = 0, w_tempty = 0, w_bres = 0;
+      if (RESB) mbar_wait_t(bres, 0, w_bres, ins);
       int s = 0;
       uint32_t ph = 0;
       int lt = 0;
       for (int it = first; it < count; it += stride, lt++) {
         const int acc = lt & 1;
-        mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+        mbar_wait_t(&tempty[acc], ((lt >> 1) & 1) ^ 1, w_tempty, ins);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
         for (int kb = 0; kb < kb_count; kb++) {
-          mbar_wait(&full[s], ph);
+          mbar_wait_t(&full[s], ph, w_full, ins);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + s * Cfg::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(RESB ? sRes + kb * Cfg::B_BYTES : sB + s * Cfg::B_BYTES));
@@ -174,6 +219,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
         umma_commit(&tfull[acc]);
+      }
+      if (ins) {
+        atomicAdd(ep.instr + 1, w_full);
+        atomicAdd(ep.instr + 2, w_tempty);
+        atomicAdd(ep.instr + 3, w_bres);
       }
     }
   } else {
@@ -188,31 +238,44 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint8_t* my_out = sOut + ew * 2 * STAGE_OUT_BYTES;
     int ob = 0;
     int lt = 0;
+    const bool ins = ep.instr != nullptr && lane == 0;
+    unsigned long long w_tfull = 0, w_u1 = 0;
     for (int it = first; it < count; it += stride, lt++) {
       int mb, nb;
       tile_of(it, mb, nb);
       const int acc = lt & 1;
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      mbar_wait_t(&tfull[acc], (lt >> 1) & 1, w_tfull, ins);
       tc_fence_after();
       const int row0 = mb * BM + q * 32;
       const int row = row0 + lane;
       const bool valid = row < M;
-      const float* u1row = nullptr;
+      const float* u1row = nullptr;      // points at column nb*BN of this row's u1 (smem or global)
       if (ep.u1) {
-        const int req = valid ? ep.req_of_ad[ep.a0 + row] : 0;
-        u1row = ep.u1 + (int64_t)req * ep.ld_u1;
+        int bnd = -1;
+        if (RESB) {
+          mbar_wait_t(&u1full[acc], (lt >> 1) & 1, w_u1, ins);
+          bnd = u1hdr[acc];
+        }
+        if (bnd >= 0) {
+          u1row = sU1 + acc * 2 * BN + ((q * 32 + lane) < bnd ? 0 : BN);
+        } else {
+          const int req = valid ? ep.req_of_ad[ep.a0 + row] : 0;
+          u1row = ep.u1 + (int64_t)req * ep.ld_u1 + nb * BN;
+        }
       }
       float z0 = 0.0f, z1 = 0.0f;
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
+      // software-pipelined TMEM drain: the load of columns c+32 is in flight while c is processed
+      uint32_t v[32];
+      if (c_begin < c_end) TMEM_LD32(taddr + c_begin, v);
       for (int c = c_begin; c < c_end; c += EPI_COLS) {
-        uint32_t v[32];
-        TMEM_LD32(taddr + c, v);
         tmem_wait_ld();
         const int col0 = nb * BN + c;
         float f[32];
 #pragma unroll
         for (int i = 0; i < 32; i++) f[i] = __uint_as_float(v[i]);
+        if (c + EPI_COLS < c_end) TMEM_LD32(taddr + c + EPI_COLS, v);
         if (ep.bias) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
@@ -223,7 +286,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (u1row) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 b = __ldg(reinterpret_cast<const float4*>(u1row + col0 + i));
+            const float4 b = *reinterpret_cast<const float4*>(u1row + c + i);
             f[i] += b.x; f[i + 1] += b.y; f[i + 2] += b.z; f[i + 3] += b.w;
           }
         }
@@ -273,6 +336,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
     if (lane == 0) bulk_wait_all();
+    if (ins) {
+      atomicAdd(ep.instr + 4, w_tfull);
+      atomicAdd(ep.instr + 5, w_u1);
+      atomicAdd(ep.instr + 6, 1ull);
+    }
   }
   tc_fence_before();
   if (CS > 1) cluster_sync(); else __syncthreads();

@@ -173,10 +173,8 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     const int r = q * 32 + lane;                 // row inside the tile
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
     // bias + ReLU + RNE cast of 32 accumulator columns into a swizzled activation tile in smem
-    auto drain_to_smem = [&](uint32_t tcol, const float* bias, int c0, uint8_t* sAct) {
-      uint32_t v[32];
-      TMEM_LD32(lane_base + tcol, v);
-      tmem_wait_ld();
+    // bias + ReLU + RNE cast of 32 accumulator columns (already loaded in v) into smem
+    auto drain_regs = [&](const uint32_t* v, const float* bias, int c0, uint8_t* sAct) {
       float f[32];
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
@@ -198,10 +196,23 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         *reinterpret_cast<uint4*>(atom + sw128_offset(r, j0 + j)) = w;
       }
     };
+    // columns [c_lo, c_hi) of the accumulator at TMEM column tbase -> activation tile sAct
+    auto drain_range = [&](uint32_t tbase, int c_lo, int c_hi, const float* bias, uint8_t* sAct) {
+      uint32_t v[32];
+      TMEM_LD32(lane_base + tbase + c_lo, v);
+      for (int c = c_lo; c < c_hi; c += 32) {
+        tmem_wait_ld();
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) w[i] = v[i];
+        if (c + 32 < c_hi) TMEM_LD32(lane_base + tbase + c + 32, v);
+        drain_regs(w, bias, c, sAct);
+      }
+    };
     auto epi3 = [&](int lt) {
       mbar_wait(&tfull[0], lt & 1);
       tc_fence_after();
-      for (int c = h * (T_N3 / 2); c < (h + 1) * (T_N3 / 2); c += 32) drain_to_smem(c, tp.b3, c, sH3);
+      drain_range(0, h * (T_N3 / 2), (h + 1) * (T_N3 / 2), tp.b3, sH3);
       fence_async_smem();      // generic-proxy smem writes -> visible to the tensor core (async proxy)
       tc_fence_before();
       __syncwarp();
@@ -210,7 +221,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     auto epi4 = [&](int lt) {
       mbar_wait(&tfull[1], lt & 1);
       tc_fence_after();
-      for (int c = h * (T_N4 / 2); c < (h + 1) * (T_N4 / 2); c += 32) drain_to_smem(T_N3 + c, tp.b4, c, sH4);
+      drain_range(T_N3, h * (T_N4 / 2), (h + 1) * (T_N4 / 2), tp.b4, sH4);
       fence_async_smem();
       tc_fence_before();
       __syncwarp();
