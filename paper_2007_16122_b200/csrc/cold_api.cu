@@ -89,11 +89,15 @@ struct cold_ctx {
   void* d_X = nullptr;
   void* d_H[COLD_MAX_LAYERS] = {nullptr};
   CUtensorMap tmA[COLD_MAX_LAYERS];
+  std::vector<CUtensorMap> tmAX;     // layer-0 A maps, one per chunk slot of the gather span
+  int gspan = 1;                     // chunks per column-wise gather pass (X_ac holds gspan * chunk rows)
   CUtensorMap tmC[COLD_MAX_LAYERS];  // epilogue TMA-store maps (32 x 32 boxes)
   int cs[COLD_MAX_LAYERS] = {0};     // cluster size (weight-tile multicast) per GEMM layer
   bool resb[COLD_MAX_LAYERS] = {false};  // weight slice resident in shared memory (K x BN <= 128 KB)
   bool pair[COLD_MAX_LAYERS] = {false};  // CTA-pair (cta_group::2) GEMM
-  bool use_tail = false;             // last three hidden layers + head in one fused kernel
+  int tail_mode = 0;                 // 0: every layer a GEMM (head fused into the last); 1: FC(L-3..L-1) +
+                                     // head fused (tail_kernel); 2: FC(L-2..L-1) + head fused (tail45_kernel)
+  int n_tail = 0;                    // hidden layers inside the fused tail (0, 3 or 2)
   bool pdl = true;                   // programmatic dependent launch between the GEMM kernels
   int* d_err = nullptr;
   float* d_scores_stage = nullptr;  // [2][chunk] for host outputs
@@ -344,6 +348,16 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   if (c->tensor) chunk = (chunk + 127) / 128 * 128;
   c->chunk = (int)std::min<int64_t>(chunk, std::max<int64_t>(c->max_ads, 128));
   if (c->tensor) c->chunk = (c->chunk + 127) / 128 * 128;
+  {
+    // Column-wise gather over a span of several chunks ("column based computation"): one
+    // group column is gathered for every ad of the span before the next group starts, so each
+    // table's hot rows are fetched from HBM once per span and then served by L2.
+    const char* env_span = getenv("COLD_GSPAN");
+    int span = env_span ? atoi(env_span) : 4;
+    if (span < 1) span = 1;
+    const int64_t need = (c->max_ads + c->chunk - 1) / c->chunk;
+    c->gspan = (int)std::min<int64_t>(span, std::max<int64_t>(need, 1));
+  }
 
   // ---- workspace ----
   const int W0 = c->widths[0];
@@ -351,7 +365,8 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   e = e ? e : c->alloc((void**)&c->d_u1, (size_t)c->max_req * W0 * 4);
   e = e ? e : c->alloc((void**)&c->d_xu, (size_t)c->max_req * std::max(1, c->d_u) * 4);
   e = e ? e : c->alloc((void**)&c->d_req, (size_t)c->max_ads * 4);
-  e = e ? e : c->alloc((void**)&c->d_X, (size_t)c->chunk * c->d_ac_pad * c->elem());
+  const size_t x_rows = (size_t)c->gspan * c->chunk;
+  e = e ? e : c->alloc((void**)&c->d_X, x_rows * c->d_ac_pad * c->elem());
   e = e ? e : c->alloc((void**)&c->d_err, 16);
   e = e ? e : c->alloc((void**)&c->d_scores_stage, (size_t)2 * c->chunk * 4);
   e = e ? e : c->alloc((void**)&c->d_adoff, (size_t)(c->max_req + 1) * 4);
@@ -362,7 +377,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     cudaGetLastError();
     return fail(COLD_ERR_OOM, std::string("workspace allocation failed: ") + cudaGetErrorString(e));
   }
-  cudaMemset(c->d_X, 0, (size_t)c->chunk * c->d_ac_pad * c->elem());  // pad columns stay 0
+  cudaMemset(c->d_X, 0, x_rows * c->d_ac_pad * c->elem());  // pad columns stay 0
   if (c->tensor) {
     const char* env_cs = getenv("COLD_GEMM_CS");
     const int cs_default = env_cs ? atoi(env_cs) : 1;
@@ -371,17 +386,33 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     const char* env_pdl = getenv("COLD_PDL");
     c->pdl = !(env_pdl && atoi(env_pdl) == 0);
     const int Lg = c->L - 1;   // GEMM layers (the last layer is fused as the head)
-    if (Lg >= 3 && !(env_tail && atoi(env_tail) == 0)) {
-      const int k3 = (Lg - 3 == 0) ? c->d_ac_pad : c->widths[Lg - 4];
-      c->use_tail = tail_supported(c->widths[Lg - 3], c->widths[Lg - 2], c->widths[Lg - 1], k3);
+    {
+      const int want = env_tail ? atoi(env_tail) : 2;
+      const int k4 = (Lg - 2 == 0) ? c->d_ac_pad : (Lg >= 3 ? c->widths[Lg - 3] : 0);
+      const int k3 = (Lg - 3 == 0) ? c->d_ac_pad : (Lg >= 4 ? c->widths[Lg - 4] : 0);
+      if (want == 2 && Lg >= 2 && tail45_supported(c->widths[Lg - 2], c->widths[Lg - 1], k4)) c->tail_mode = 2;
+      else if (want >= 1 && Lg >= 3 && tail_supported(c->widths[Lg - 3], c->widths[Lg - 2], c->widths[Lg - 1], k3))
+        c->tail_mode = 1;
+      c->n_tail = c->tail_mode == 1 ? 3 : (c->tail_mode == 2 ? 2 : 0);
     }
     for (int l = 0; l < c->L - 1; l++) {
       void* in = (l == 0) ? c->d_X : c->d_H[l - 1];
       int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
       cold_status s = make_tmap(&c->tmA[l], in, c->precision, K, c->chunk, 128);
       if (s) { delete c; return s; }
+      if (l == 0) {
+        c->tmAX.resize(c->gspan);
+        for (int j = 0; j < c->gspan; j++) {
+          s = make_tmap(&c->tmAX[j], (uint8_t*)c->d_X + (size_t)j * c->chunk * c->d_ac_pad * 2, c->precision, K,
+                        c->chunk, 128);
+          if (s) { delete c; return s; }
+        }
+      }
       if (l < c->L - 2) {
-        s = make_tmap(&c->tmC[l], c->d_H[l], c->precision, c->widths[l], c->chunk, 32, 32);
+        // epilogue store boxes: 32 rows x 64 columns (SW128) when each epilogue warp's column half is a
+        // multiple of 64 (epi.cuh), else 32 x 32 (SW64)
+        s = make_tmap(&c->tmC[l], c->d_H[l], c->precision, c->widths[l], c->chunk, 32,
+                      (c->bn[l] / 2) % 64 == 0 ? 64 : 32);
         if (s) { delete c; return s; }
       } else {
         c->tmC[l] = c->tmA[l];   // unused by the head epilogue
@@ -389,12 +420,12 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       int cs = cs_default;
       while (cs > 1 && (c->bn[l] / cs) % 8 != 0) cs >>= 1;   // B slices must be whole 8-row swizzle atoms
       c->cs[l] = (cs == 4 || cs == 2) ? cs : 1;
-      if (c->use_tail && l >= Lg - 3) c->cs[l] = 1;          // the tail kernel loads whole weight tiles
+      if (c->n_tail && l >= Lg - c->n_tail) c->cs[l] = 1;   // the tail kernels load whole weight tiles
       c->resb[l] = c->cs[l] == 1 && gemm_resident_ok(c->bn[l], K) && !(env_resb && atoi(env_resb) == 0);
       // CTA pairs for the 256-wide layers that are not fused into the tail (FC1, FC2)
       const char* env_pair = getenv("COLD_PAIR");
       const int pair_mode = env_pair ? atoi(env_pair) : 1;   // 0 off, 1 non-resident 256-wide, 2 all 256-wide
-      const bool in_tail = c->use_tail && l >= Lg - 3;
+      const bool in_tail = c->n_tail && l >= Lg - c->n_tail;
       c->pair[l] = !in_tail && l < Lg - 1 && c->bn[l] == 256 &&
                    (pair_mode == 2 || (pair_mode == 1 && !c->resb[l]));
       if (c->pair[l]) { c->resb[l] = false; c->cs[l] = 1; }
@@ -783,11 +814,12 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
 }
 
 // the network on one chunk: X (rows a0 .. a0+n) -> scores_out[0 .. n)
-static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, cudaStream_t st) {
+static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* scores_out, cudaStream_t st) {
+  auto tmA_of = [&](int l) -> const CUtensorMap* { return l == 0 ? &c->tmAX[xslot] : &c->tmA[l]; };
   if (!c->tensor) {
     MlpF32Args m;
     memset(&m, 0, sizeof(m));
-    m.X = (const float*)c->d_X;
+    m.X = (const float*)c->d_X + (size_t)xslot * c->chunk * c->d_ac_pad;
     m.ldx = c->d_ac_pad;
     m.d_ac = c->d_ac;
     m.u1 = c->d_u1;
@@ -810,7 +842,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, c
     c->mark_end(COLD_PROF_FC, st);
     return;
   }
-  const int n_gemm = c->use_tail ? c->L - 4 : c->L - 1;
+  const int n_gemm = c->L - 1 - c->n_tail;
   static bool instr_on = getenv("COLD_INSTR") != nullptr;
   if (instr_on && !g_instr) {
     cudaMalloc(&g_instr, 8 * 8 * COLD_MAX_LAYERS);
@@ -841,16 +873,35 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, c
     }
     const int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
     ep.instr = instr_on ? g_instr + 8 * l : nullptr;
+    {
+      static const char* env_dbg = getenv("COLD_DBG_GEMM");   // "<layer>:<mode>" timing experiments
+      if (env_dbg && atoi(env_dbg) == l && strchr(env_dbg, ':')) ep.dbg_mode = atoi(strchr(env_dbg, ':') + 1);
+    }
     c->mark_begin(st);
     if (c->pair[l])
-      launch_gemm_pair(&c->tmA[l], &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
+      launch_gemm_pair(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
                        c->precision == COLD_BF16 ? 1 : 0, ep, c->num_sms, c->pdl && !c->prof, st);
     else
-      launch_gemm(&c->tmA[l], &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
+      launch_gemm(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
                   c->precision == COLD_BF16 ? 1 : 0, c->cs[l], c->resb[l], ep, c->num_sms, c->pdl && !c->prof, st);
     c->mark_end(COLD_PROF_FC + l, st);
   }
-  if (c->use_tail) {
+  if (c->tail_mode == 2) {
+    const int l4 = c->L - 3;
+    TailParams tp;
+    memset(&tp, 0, sizeof(tp));
+    tp.b4 = c->d_b[l4];
+    tp.b5 = c->d_b[l4 + 1];
+    tp.head_w = c->d_head_w;
+    tp.head_b = c->d_head_b;
+    tp.head_n = c->widths[c->L - 1];
+    tp.scores = scores_out;
+    c->mark_begin(st);
+    launch_tail45(tmA_of(l4), &c->tmB[l4], &c->tmB[l4 + 1], (int)n, c->precision == COLD_BF16 ? 1 : 0, tp,
+                  c->num_sms, c->pdl && !c->prof, st);
+    c->mark_end(COLD_PROF_FC + l4, st);
+  }
+  if (c->tail_mode == 1) {
     const int l3 = c->L - 4;
     TailParams tp;
     tp.b3 = c->d_b[l3];
@@ -862,7 +913,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, float* scores_out, c
     tp.scores = scores_out;
     const int K3 = (l3 == 0) ? c->d_ac_pad : c->widths[l3 - 1];
     c->mark_begin(st);
-    launch_tail(&c->tmA[l3], &c->tmB[l3], &c->tmB[l3 + 1], &c->tmB[l3 + 2], (int)n, K3,
+    launch_tail(tmA_of(l3), &c->tmB[l3], &c->tmB[l3 + 1], &c->tmB[l3 + 2], (int)n, K3,
                 c->precision == COLD_BF16 ? 1 : 0, tp, c->num_sms, c->pdl && !c->prof, st);
     c->mark_end(COLD_PROF_FC + l3, st);
   }
@@ -892,11 +943,12 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
   c->mark_end(COLD_PROF_USER, st);
   CK(cudaGetLastError());
   const int64_t chunk = c->chunk;
-  const int64_t nchunks = (pl.N + chunk - 1) / chunk;
+  const int64_t span = chunk * c->gspan;            // ads per column-wise gather pass
+  const int64_t nspans = (pl.N + span - 1) / span;
   if (pl.host) {
     size_t need = 0;
-    for (int64_t ci = 0; ci < nchunks; ci++)
-      need = std::max(need, chunk_stage_bytes(c, b, pl, ci * chunk, std::min(pl.N, (ci + 1) * chunk)));
+    for (int64_t si = 0; si < nspans; si++)
+      need = std::max(need, chunk_stage_bytes(c, b, pl, si * span, std::min(pl.N, (si + 1) * span)));
     if (need > c->stage_bytes) {
       CK(cudaStreamSynchronize(st));
       CK(cudaStreamSynchronize(c->copy_stream));
@@ -912,31 +964,36 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
     CK(cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[0], 0));
     CK(cudaEventRecord(c->ev_consumed[1], st));
   }
-  for (int64_t ci = 0; ci < nchunks; ci++) {
-    const int64_t a0 = ci * chunk, a1 = std::min(pl.N, a0 + chunk), n = a1 - a0;
-    const int slot = (int)(ci & 1);
+  int64_t ci = 0;   // running chunk counter (score staging slots)
+  for (int64_t si = 0; si < nspans; si++) {
+    const int64_t s0 = si * span, s1 = std::min(pl.N, s0 + span);
+    const int slot = (int)(si & 1);
     BatchView bv = pl.bv;
     if (pl.host) {
-      if (ci >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[slot], 0));
-      s = stage_chunk(c, b, pl, a0, a1, slot, bv);
+      if (si >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[slot], 0));
+      s = stage_chunk(c, b, pl, s0, s1, slot, bv);
       if (s) return s;
       CK(cudaEventRecord(c->ev_copied[slot], c->copy_stream));
       CK(cudaStreamWaitEvent(st, c->ev_copied[slot], 0));
     }
-    GatherArgs ga = make_gather_args(c, bv, a0, n, dbg);
+    GatherArgs ga = make_gather_args(c, bv, s0, s1 - s0, dbg);
     c->mark_begin(st);
     launch_gather(ga, c->precision, st);
     c->mark_end(COLD_PROF_GATHER, st);
     if (pl.host) CK(cudaEventRecord(c->ev_consumed[slot], st));
     if (mode == RUN_SCORE) {
-      float* out = scores_dev ? scores + a0 : c->d_scores_stage + (int64_t)slot * chunk;
-      if (!scores_dev && ci >= 2) CK(cudaStreamWaitEvent(st, c->ev_drained[slot], 0));
-      run_network(c, a0, n, out, st);
-      if (!scores_dev) {
-        CK(cudaEventRecord(c->ev_scored[slot], st));
-        CK(cudaStreamWaitEvent(c->copy_stream, c->ev_scored[slot], 0));
-        CK(cudaMemcpyAsync(scores + a0, out, (size_t)n * 4, cudaMemcpyDeviceToHost, c->copy_stream));
-        CK(cudaEventRecord(c->ev_drained[slot], c->copy_stream));
+      for (int64_t a0 = s0; a0 < s1; a0 += chunk, ci++) {
+        const int64_t n = std::min(s1, a0 + chunk) - a0;
+        const int oslot = (int)(ci & 1);
+        float* out = scores_dev ? scores + a0 : c->d_scores_stage + (int64_t)oslot * chunk;
+        if (!scores_dev && ci >= 2) CK(cudaStreamWaitEvent(st, c->ev_drained[oslot], 0));
+        run_network(c, a0, n, (int)((a0 - s0) / chunk), out, st);
+        if (!scores_dev) {
+          CK(cudaEventRecord(c->ev_scored[oslot], st));
+          CK(cudaStreamWaitEvent(c->copy_stream, c->ev_scored[oslot], 0));
+          CK(cudaMemcpyAsync(scores + a0, out, (size_t)n * 4, cudaMemcpyDeviceToHost, c->copy_stream));
+          CK(cudaEventRecord(c->ev_drained[oslot], c->copy_stream));
+        }
       }
     }
     CK(cudaGetLastError());
@@ -1119,7 +1176,7 @@ extern "C" cold_status cold_get_info(const cold_ctx* c, cold_info* out) {
   out->d_user = c->d_u;
   out->d_ad = c->d_ac;
   out->chunk_ads = c->chunk;
-  out->kernels_per_chunk = 1 + (c->tensor ? (c->use_tail ? c->L - 3 : c->L - 1) : 1);
+  out->kernels_per_chunk = 1 + (c->tensor ? (c->L - 1 - c->n_tail + (c->n_tail ? 1 : 0)) : 1);
   out->kernels_per_call = 1;
   out->tensor_core = c->tensor ? 1 : 0;
   int64_t b = c->device_bytes;

@@ -93,6 +93,9 @@ struct EpiParams {
   float* scores;                   // chunk-local [M]
   int relu;
   unsigned long long* instr;       // debug: per-role wait-cycle counters [8] (null = off)
+  int dbg_mode;                    // timing experiments only (results invalid): 1 = epilogue only drains
+                                   // TMEM (no math / stores), 2 = MMA issuer skips the MMAs, 3 = epilogue
+                                   // math without smem / TMA stores, 4 = smem staging but no TMA store
 };
 cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N, int K,
                         int bn, int bf16, int cs, bool resb, const EpiParams& ep, int num_sms, bool pdl,
@@ -112,6 +115,11 @@ bool tail_supported(int n3, int n4, int n5, int k3);
 cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const CUtensorMap* tmB4,
                         const CUtensorMap* tmB5, int M, int K3, int bf16, const TailParams& tp, int num_sms, bool pdl,
                         cudaStream_t s);
+
+// fused FC(L-3) .. FC(L-2) + head after a GEMM FC(L-4) (paper widths 128, 64 -> 2), resident weights
+bool tail45_supported(int n4, int n5, int k4);
+cudaError_t launch_tail45(const CUtensorMap* tmA4, const CUtensorMap* tmB4, const CUtensorMap* tmB5, int M, int bf16,
+                          const TailParams& tp, int num_sms, bool pdl, cudaStream_t s);
 
 // top-K per request
 struct TopkArgs {

@@ -12,15 +12,35 @@
 
 namespace cold {
 
+// 256-bit global access (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256): a 32 B table row is one request
+// and one L1 sector lookup instead of two 16 B ones (the gather was L1TEX-throughput bound).
+__device__ __forceinline__ void ldg256(const void* p, uint4& a, uint4& b) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
+__device__ __forceinline__ void stg256(void* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z),
+               "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 template <typename T, int K>
 __device__ __forceinline__ void add_row(const T* __restrict__ table, int64_t row, float* e) {
   constexpr int BYTES = K * (int)sizeof(T);
   if constexpr (BYTES % 16 == 0) {          // 16 B vector loads (k=16 fp16: one 32 B sector)
     const uint4* p = reinterpret_cast<const uint4*>(table + row * K);
+    uint4 qv[BYTES / 16];
+    if constexpr (BYTES % 32 == 0) {
+#pragma unroll
+      for (int v = 0; v < BYTES / 16; v += 2) ldg256(p + v, qv[v], qv[v + 1]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < BYTES / 16; v++) qv[v] = __ldg(p + v);
+    }
 #pragma unroll
     for (int v = 0; v < BYTES / 16; v++) {
-      uint4 q = __ldg(p + v);
-      const T* t = reinterpret_cast<const T*>(&q);
+      const T* t = reinterpret_cast<const T*>(&qv[v]);
 #pragma unroll
       for (int i = 0; i < 16 / (int)sizeof(T); i++) e[v * (16 / sizeof(T)) + i] += Store<T>::to_f(t[i]);
     }
@@ -90,105 +110,50 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// ad + cross side: grid = (ceil(n / 128), n_ac), block = 128 threads, one thread per (ad, group).
-// blockIdx.y walks the selected AD/CROSS groups heaviest-first (cross groups over user bags carry
-// 16 rows per ad) so the long blocks start first. A cross group's user-side half of the hash,
-// hx = fmix64(x ^ salt_g), depends only on the request: a block whose 128 ads belong to one request
-// computes it once into shared memory (AMB-9: row = hi64(fmix64(hx ^ y) * C)).
-constexpr int HX_SMEM = 512;
+// ad + cross side: grid = (ceil(n / (128 * APT)), n_ac), block = 128 threads. blockIdx.y is one
+// selected AD/CROSS group (column-wise), walked heaviest-first; thread t of block b owns the
+// APT ads b*128*APT + t + i*128 (i < APT), so every id / X access of a warp stays coalesced.
+// The kernel is bound by memory-level parallelism (random 32 B rows; one row per thread in flight
+// left DRAM at 28% and L2 at 47% busy), so rows are fetched as raw 16 B vectors into registers, up to
+// RB rows per thread in flight, and only then summed — still sequentially in bag order (x-major for
+// cross bags), which keeps the fp32 pooled sums bit-identical to the oracle's fp32-ordered mode.
+// A cross group's user-side half of the hash, hx = fmix64(x ^ salt_g), depends only on the request:
+// a block spanning <= 2 requests hashes their user bags once into shared memory (AMB-9).
+constexpr int GATHER_APT = 4;       // ads per thread
+constexpr int HX_HALF = 256;        // user-bag hashes cached per request slot
 
-template <typename T, int K, bool FAST>
-__global__ void __launch_bounds__(128) gather_kernel(GatherArgs a) {
-  __shared__ uint64_t s_hx[HX_SMEM];
-  const int64_t local = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool in_range = local < a.n;
-  const int64_t ad = a.a0 + (in_range ? local : a.n - 1);
-  const int j = a.order[blockIdx.y];
-  const int g = a.ac_g[j];
-  const DevGroup G = a.groups[g];
-  const T* tab = reinterpret_cast<const T*>(G.table);
-  float e[K];
+template <typename T, int K>
+struct RawRow {
+  static constexpr int NV = K * (int)sizeof(T) / 16;   // 16 B vectors per row (>= 1 on the fast path)
+  uint4 q[NV > 0 ? NV : 1];
+  __device__ __forceinline__ void load(const T* __restrict__ table, int64_t row) {
+    const uint4* p = reinterpret_cast<const uint4*>(table + row * K);
+    if constexpr (NV % 2 == 0) {
 #pragma unroll
-  for (int d = 0; d < K; d++) e[d] = 0.0f;
-
-  if (G.side == 1) {                      // AD group
-    if (!in_range) return;
-    const BatchGroup& B = a.bv.g[g];
-    if (!G.pooled) {
-      add_row<T, K>(tab, checked(B.ids[ad - B.id_shift], G.card, a.validate, a.err), e);
+      for (int v = 0; v < NV; v += 2) ldg256(p + v, q[v], q[v + 1]);
     } else {
-      const int64_t o0 = (int64_t)B.offs[ad - B.offs_shift] - B.val_shift;
-      const int64_t o1 = (int64_t)B.offs[ad + 1 - B.offs_shift] - B.val_shift;
-      for (int64_t i = o0; i < o1; i++) add_row<T, K>(tab, checked(B.ids[i], G.card, a.validate, a.err), e);
-    }
-  } else {                                // CROSS group: rows = hash(user bag x ad bag), x-major
-    const DevGroup U = a.groups[G.user_ref];
-    const DevGroup A = a.groups[G.ad_ref];
-    const BatchGroup& BU = a.bv.g[G.user_ref];
-    const BatchGroup& BA = a.bv.g[G.ad_ref];
-    const uint64_t salt = cross_salt(g);
-    const uint64_t card = (uint64_t)G.card;
-    // block-uniform request? then hash the user bag once into shared memory
-    const int64_t blk0 = a.a0 + (int64_t)blockIdx.x * blockDim.x;
-    const int64_t blk_end = (int64_t)(blockIdx.x + 1) * blockDim.x;
-    const int64_t blk1 = a.a0 + (blk_end < a.n ? blk_end : a.n) - 1;
-    const int rb = a.req_of_ad[blk0];
-    const int64_t ub0 = (int64_t)BU.offs[rb - BU.offs_shift] - BU.val_shift;
-    const int64_t ub1 = (int64_t)BU.offs[rb + 1 - BU.offs_shift] - BU.val_shift;
-    const bool shared_hx = (a.req_of_ad[blk1] == rb) && (ub1 - ub0 <= HX_SMEM);
-    if (shared_hx) {
-      for (int64_t i = threadIdx.x; i < ub1 - ub0; i += blockDim.x)
-        s_hx[i] = fmix64((uint64_t)checked(BU.ids[ub0 + i], U.card, a.validate, a.err) ^ salt);
-      __syncthreads();
-    }
-    if (!in_range) return;
-    const int r = shared_hx ? rb : a.req_of_ad[ad];
-    const int64_t u0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
-    const int64_t u1 = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift;
-    const int L = (int)(u1 - u0);
-    auto hx_at = [&](int i) -> uint64_t {
-      return shared_hx ? s_hx[i] : fmix64((uint64_t)checked(BU.ids[u0 + i], U.card, a.validate, a.err) ^ salt);
-    };
-    if (!A.pooled) {
-      const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
-      int i = 0;
-      constexpr int U4 = 4;               // 4 rows in flight per thread, then summed in bag order
-      for (; i + U4 <= L; i += U4) {
-        int64_t rows[U4];
 #pragma unroll
-        for (int t = 0; t < U4; t++) rows[t] = cross_row_from_hx(hx_at(i + t), y, card);
-        float v[U4][K];
-#pragma unroll
-        for (int t = 0; t < U4; t++) {
-#pragma unroll
-          for (int d = 0; d < K; d++) v[t][d] = 0.0f;
-          add_row<T, K>(tab, rows[t], v[t]);
-        }
-#pragma unroll
-        for (int t = 0; t < U4; t++) {
-#pragma unroll
-          for (int d = 0; d < K; d++) e[d] += v[t][d];
-        }
-      }
-      for (; i < L; i++) add_row<T, K>(tab, cross_row_from_hx(hx_at(i), y, card), e);
-    } else {
-      const int64_t y0 = (int64_t)BA.offs[ad - BA.offs_shift] - BA.val_shift;
-      const int64_t y1 = (int64_t)BA.offs[ad + 1 - BA.offs_shift] - BA.val_shift;
-      for (int i = 0; i < L; i++) {
-        const uint64_t hx = hx_at(i);
-        for (int64_t q = y0; q < y1; q++) {
-          const uint64_t y = (uint64_t)checked(BA.ids[q], A.card, a.validate, a.err);
-          add_row<T, K>(tab, cross_row_from_hx(hx, y, card), e);
-        }
-      }
+      for (int v = 0; v < NV; v++) q[v] = __ldg(p + v);
     }
   }
+  __device__ __forceinline__ void add_to(float* e) const {
+#pragma unroll
+    for (int v = 0; v < NV; v++) {
+      const T* t = reinterpret_cast<const T*>(&q[v]);
+#pragma unroll
+      for (int i = 0; i < 16 / (int)sizeof(T); i++) e[v * (16 / sizeof(T)) + i] += Store<T>::to_f(t[i]);
+    }
+  }
+};
 
+// pooled e -> [debug] -> linear_log -> SE gate -> v = s ê -> RNE cast -> X_ac[local][slot]
+template <typename T, int K, bool FAST>
+__device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G, int g, int64_t local, float* e) {
+  const int64_t ad = a.a0 + local;
   if (a.dbg_pooled) {
 #pragma unroll
     for (int d = 0; d < K; d++) a.dbg_pooled[(ad * a.n_sel + G.sel_pos) * K + d] = e[d];
   }
-  // linear_log -> SE gate s = sigma(w . ê + b) -> v = s ê (fp32), then RNE to storage
   if (a.linear_log) {
 #pragma unroll
     for (int d = 0; d < K; d++) e[d] = linear_log_t<FAST>(e[d]);
@@ -202,7 +167,12 @@ __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a) {
   for (int d = 0; d < K; d++) out[d] = Store<T>::from_f(s * e[d]);
   T* dst = reinterpret_cast<T*>(a.X) + local * a.ldx + G.sel_slot * K;
   constexpr int BYTES = K * (int)sizeof(T);
-  if constexpr (BYTES % 16 == 0) {
+  if constexpr (BYTES % 32 == 0) {
+#pragma unroll
+    for (int v = 0; v < BYTES / 16; v += 2)
+      stg256(reinterpret_cast<uint4*>(dst) + v, reinterpret_cast<const uint4*>(out)[v],
+             reinterpret_cast<const uint4*>(out)[v + 1]);
+  } else if constexpr (BYTES % 16 == 0) {
 #pragma unroll
     for (int v = 0; v < BYTES / 16; v++)
       reinterpret_cast<uint4*>(dst)[v] = reinterpret_cast<const uint4*>(out)[v];
@@ -213,6 +183,161 @@ __global__ void __launch_bounds__(128) gather_kernel(GatherArgs a) {
   if (a.dbg_feat) {
 #pragma unroll
     for (int d = 0; d < K; d++) a.dbg_feat[ad * a.d_in + G.sel_pos * K + d] = Store<T>::to_f(out[d]);
+  }
+}
+
+template <typename T, int K, bool FAST>
+__global__ void __launch_bounds__(128, 4) gather_kernel(GatherArgs a) {
+  constexpr bool VEC = (K * (int)sizeof(T)) % 16 == 0;
+  constexpr int NV = K * (int)sizeof(T) / 16;
+  constexpr int GATHER_RB = NV <= 2 ? 8 : (NV == 4 ? 4 : 2);   // bag rows in flight (<= 16 vectors)
+  __shared__ uint64_t s_hx[2][HX_HALF];
+  const int j = a.order[blockIdx.y];
+  const int g = a.ac_g[j];
+  const DevGroup G = a.groups[g];
+  const T* tab = reinterpret_cast<const T*>(G.table);
+  const int64_t base = (int64_t)blockIdx.x * (128 * GATHER_APT);
+  int64_t loc[GATHER_APT];
+  bool ok[GATHER_APT];
+#pragma unroll
+  for (int i = 0; i < GATHER_APT; i++) {
+    const int64_t l = base + threadIdx.x + i * 128;
+    ok[i] = l < a.n;
+    loc[i] = ok[i] ? l : a.n - 1;           // clamped: loads stay in range, results are dropped
+  }
+
+  if (G.side == 1) {                        // ---------------- AD group ----------------
+    const BatchGroup& B = a.bv.g[g];
+    if (!G.pooled && VEC) {
+      int64_t row[GATHER_APT];
+#pragma unroll
+      for (int i = 0; i < GATHER_APT; i++) row[i] = checked(B.ids[a.a0 + loc[i] - B.id_shift], G.card, a.validate, a.err);
+      RawRow<T, K> raw[GATHER_APT];
+#pragma unroll
+      for (int i = 0; i < GATHER_APT; i++) raw[i].load(tab, row[i]);
+#pragma unroll
+      for (int i = 0; i < GATHER_APT; i++) {
+        float e[K];
+#pragma unroll
+        for (int d = 0; d < K; d++) e[d] = 0.0f;
+        raw[i].add_to(e);
+        if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e);
+      }
+    } else {
+      for (int i = 0; i < GATHER_APT; i++) {
+        const int64_t li = base + threadIdx.x + i * 128;   // (no register-array indexing in rolled loops)
+        if (li >= a.n) break;
+        const int64_t ad = a.a0 + li;
+        float e[K];
+#pragma unroll
+        for (int d = 0; d < K; d++) e[d] = 0.0f;
+        if (!G.pooled) {
+          add_row<T, K>(tab, checked(B.ids[ad - B.id_shift], G.card, a.validate, a.err), e);
+        } else {
+          const int64_t o0 = (int64_t)B.offs[ad - B.offs_shift] - B.val_shift;
+          const int64_t o1 = (int64_t)B.offs[ad + 1 - B.offs_shift] - B.val_shift;
+          for (int64_t q = o0; q < o1; q++) add_row<T, K>(tab, checked(B.ids[q], G.card, a.validate, a.err), e);
+        }
+        finish_ad<T, K, FAST>(a, G, g, li, e);
+      }
+    }
+    return;
+  }
+
+  // ---------------- CROSS group: rows = hash(user bag x ad bag), x-major ----------------
+  const DevGroup U = a.groups[G.user_ref];
+  const DevGroup A = a.groups[G.ad_ref];
+  const BatchGroup& BU = a.bv.g[G.user_ref];
+  const BatchGroup& BA = a.bv.g[G.ad_ref];
+  const uint64_t salt = cross_salt(g);
+  const uint64_t card = (uint64_t)G.card;
+  // requests of the block's first and last ad; <= 2 requests -> user-bag hashes in shared memory
+  const int64_t last = (base + 128 * GATHER_APT < a.n ? base + 128 * GATHER_APT : a.n) - 1;
+  const int rfirst = a.req_of_ad[a.a0 + base];
+  const int rlast = a.req_of_ad[a.a0 + last];
+  int64_t ub[2], ul[2];
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    const int r = q == 0 ? rfirst : rlast;
+    ub[q] = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
+    ul[q] = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift - ub[q];
+  }
+  const bool shared_hx = (rlast - rfirst <= 1) && ul[0] <= HX_HALF && ul[1] <= HX_HALF;
+  if (shared_hx) {
+    for (int q = 0; q < 2; q++)
+      for (int64_t i = threadIdx.x; i < ul[q]; i += blockDim.x)
+        s_hx[q][i] = fmix64((uint64_t)checked(BU.ids[ub[q] + i], U.card, a.validate, a.err) ^ salt);
+    __syncthreads();
+  }
+  if (shared_hx && !A.pooled && VEC && ul[0] == 1 && ul[1] == 1) {
+    // single-id user group x single-id ad group: one row per ad, all APT rows in flight
+    int64_t row[GATHER_APT];
+#pragma unroll
+    for (int i = 0; i < GATHER_APT; i++) {
+      const uint64_t y = (uint64_t)checked(BA.ids[a.a0 + loc[i] - BA.id_shift], A.card, a.validate, a.err);
+      const int sl = (a.req_of_ad[a.a0 + loc[i]] == rfirst) ? 0 : 1;
+      row[i] = cross_row_from_hx(s_hx[sl][0], y, card);
+    }
+    RawRow<T, K> raw[GATHER_APT];
+#pragma unroll
+    for (int i = 0; i < GATHER_APT; i++) raw[i].load(tab, row[i]);
+#pragma unroll
+    for (int i = 0; i < GATHER_APT; i++) {
+      float e[K];
+#pragma unroll
+      for (int d = 0; d < K; d++) e[d] = 0.0f;
+      raw[i].add_to(e);
+      if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e);
+    }
+    return;
+  }
+
+  for (int i = 0; i < GATHER_APT; i++) {
+    const int64_t li = base + threadIdx.x + i * 128;
+    if (li >= a.n) break;
+    const int64_t ad = a.a0 + li;
+    const int sl = (a.req_of_ad[ad] == rfirst) ? 0 : 1;
+    int64_t u0, L;
+    if (shared_hx) {
+      u0 = sl ? ub[1] : ub[0];
+      L = sl ? ul[1] : ul[0];
+    } else {
+      const int r = a.req_of_ad[ad];
+      u0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
+      L = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift - u0;
+    }
+    auto hx_at = [&](int64_t x) -> uint64_t {
+      return shared_hx ? s_hx[sl][x]
+                       : fmix64((uint64_t)checked(BU.ids[u0 + x], U.card, a.validate, a.err) ^ salt);
+    };
+    float e[K];
+#pragma unroll
+    for (int d = 0; d < K; d++) e[d] = 0.0f;
+    if (!A.pooled) {
+      const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
+      int64_t x = 0;
+      if constexpr (VEC) {
+        for (; x + GATHER_RB <= L; x += GATHER_RB) {     // RB rows in flight, then summed in bag order
+          RawRow<T, K> raw[GATHER_RB];
+#pragma unroll
+          for (int t = 0; t < GATHER_RB; t++) raw[t].load(tab, cross_row_from_hx(hx_at(x + t), y, card));
+#pragma unroll
+          for (int t = 0; t < GATHER_RB; t++) raw[t].add_to(e);
+        }
+      }
+      for (; x < L; x++) add_row<T, K>(tab, cross_row_from_hx(hx_at(x), y, card), e);
+    } else {
+      const int64_t y0 = (int64_t)BA.offs[ad - BA.offs_shift] - BA.val_shift;
+      const int64_t y1 = (int64_t)BA.offs[ad + 1 - BA.offs_shift] - BA.val_shift;
+      for (int64_t x = 0; x < L; x++) {
+        const uint64_t hx = hx_at(x);
+        for (int64_t q = y0; q < y1; q++) {
+          const uint64_t y = (uint64_t)checked(BA.ids[q], A.card, a.validate, a.err);
+          add_row<T, K>(tab, cross_row_from_hx(hx, y, card), e);
+        }
+      }
+    }
+    finish_ad<T, K, FAST>(a, G, g, li, e);
   }
 }
 
@@ -272,7 +397,7 @@ void launch_user(const UserArgs& a, int R, int precision, cudaStream_t s) {
 
 template <typename T, bool FAST>
 static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
-  dim3 grid((unsigned)((a.n + 127) / 128), (unsigned)a.n_ac);
+  dim3 grid((unsigned)((a.n + 128 * GATHER_APT - 1) / (128 * GATHER_APT)), (unsigned)a.n_ac);
   switch (a.k) {
     case 2: gather_kernel<T, 2, FAST><<<grid, 128, 0, s>>>(a); break;
     case 4: gather_kernel<T, 4, FAST><<<grid, 128, 0, s>>>(a); break;

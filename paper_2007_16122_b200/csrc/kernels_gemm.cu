@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include "internal.h"
 #include "ptx.cuh"
+#include "epi.cuh"
 
 namespace cold {
 
@@ -211,9 +212,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + s * Cfg::A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(RESB ? sRes + kb * Cfg::B_BYTES : sB + s * Cfg::B_BYTES));
+          if (ep.dbg_mode != 2) {
 #pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; kk++)   // +32 B along K inside the swizzle atom
-            umma_f16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / UMMA_K; kk++)   // +32 B along K inside the swizzle atom
+              umma_f16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+          }
           if (CS > 1) umma_commit_mc(&empty[s], (uint16_t)((1u << CS) - 1u));
           else umma_commit(&empty[s]);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
@@ -232,6 +235,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int q = warp & 3;
     const int h = ew >> 2;
     const bool head = ep.head_n != 0;
+    constexpr bool WIDE = (BN / 2) % EPI_WIDE_COLS == 0;   // 64-column SW128 store boxes
     // with a fused head one warp per quadrant walks all columns (the row's dot product stays in-thread)
     const int c_begin = head ? 0 : h * (BN / 2);
     const int c_end = head ? (h == 0 ? BN : 0) : (h + 1) * (BN / 2);
@@ -249,6 +253,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const int row0 = mb * BM + q * 32;
       const int row = row0 + lane;
       const bool valid = row < M;
+      uint32_t u1s = 0;                 // staged u1 row in shared memory (column nb*BN)
       const float* u1row = nullptr;      // points at column nb*BN of this row's u1 (smem or global)
       if (ep.u1) {
         int bnd = -1;
@@ -257,25 +262,36 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           bnd = u1hdr[acc];
         }
         if (bnd >= 0) {
-          u1row = sU1 + acc * 2 * BN + ((q * 32 + lane) < bnd ? 0 : BN);
+          u1s = smem_u32(sU1 + acc * 2 * BN + ((q * 32 + lane) < bnd ? 0 : BN));
         } else {
           const int req = valid ? ep.req_of_ad[ep.a0 + row] : 0;
           u1row = ep.u1 + (int64_t)req * ep.ld_u1 + nb * BN;
         }
       }
+      if (WIDE && !head) {
+        const int c_stop = ep.dbg_mode == 1 ? c_begin : c_end;
+        const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
+        epi_store_wide<BF16>(tbase, c_begin, c_stop, ep.bias, u1s, u1row, ep.relu,
+                             sOut + ew * EPI_WIDE_BOX, &tmC, nb * BN, row0, lane);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        continue;
+      }
       float z0 = 0.0f, z1 = 0.0f;
+      const int c_stop = ep.dbg_mode == 1 ? c_begin : c_end;   // debug: drain nothing
       const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
       // software-pipelined TMEM drain: the load of columns c+32 is in flight while c is processed
       uint32_t v[32];
-      if (c_begin < c_end) TMEM_LD32(taddr + c_begin, v);
-      for (int c = c_begin; c < c_end; c += EPI_COLS) {
+      if (c_begin < c_stop) TMEM_LD32(taddr + c_begin, v);
+      for (int c = c_begin; c < c_stop; c += EPI_COLS) {
         tmem_wait_ld();
         const int col0 = nb * BN + c;
         float f[32];
 #pragma unroll
         for (int i = 0; i < 32; i++) f[i] = __uint_as_float(v[i]);
-        if (c + EPI_COLS < c_end) TMEM_LD32(taddr + c + EPI_COLS, v);
+        if (c + EPI_COLS < c_stop) TMEM_LD32(taddr + c + EPI_COLS, v);
         if (ep.bias) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
@@ -283,10 +299,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             f[i] += b.x; f[i + 1] += b.y; f[i + 2] += b.z; f[i + 3] += b.w;
           }
         }
-        if (u1row) {
+        if (u1s) {
 #pragma unroll
           for (int i = 0; i < 32; i += 4) {
-            const float4 b = *reinterpret_cast<const float4*>(u1row + c + i);
+            const float4 b = lds128f(u1s + (uint32_t)(c + i) * 4u);
+            f[i] += b.x; f[i + 1] += b.y; f[i + 2] += b.z; f[i + 3] += b.w;
+          }
+        } else if (u1row) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 b = __ldg(reinterpret_cast<const float4*>(u1row + c + i));
             f[i] += b.x; f[i + 1] += b.y; f[i + 2] += b.z; f[i + 3] += b.w;
           }
         }
@@ -301,6 +323,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
             for (int i = 0; i < 32; i++) z1 = fmaf(__ldg(ep.head_w + N + col0 + i), f[i], z1);
           }
+        } else if (ep.dbg_mode == 3) {
+          float t = 0.0f;
+#pragma unroll
+          for (int i = 0; i < 32; i++) t += f[i];
+          if (t == 12345.678f) ep.scores[0] = t;   // keep the math alive
         } else {
           // 32 x 32 box, 64 B rows, SWIZZLE_64B: 16 B chunk j of row r sits at j ^ ((r >> 1) & 3)
           uint8_t* buf = my_out + ob * STAGE_OUT_BYTES;
@@ -314,11 +341,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             w.z = Pack<BF16>::two(f[8 * j + 4], f[8 * j + 5]);
             w.w = Pack<BF16>::two(f[8 * j + 6], f[8 * j + 7]);
             const int phys = j ^ ((lane >> 1) & 3);
-            *reinterpret_cast<uint4*>(buf + lane * 64 + phys * 16) = w;
+            sts128(smem_u32(buf) + (uint32_t)(lane * 64 + phys * 16), w);
           }
           fence_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && ep.dbg_mode != 4) {
             tma_store_2d(&tmC, buf, col0, row0);
             bulk_commit();
           }

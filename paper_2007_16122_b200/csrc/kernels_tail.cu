@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         w.y = Pack<BF16>::two(f[8 * j + 2], f[8 * j + 3]);
         w.z = Pack<BF16>::two(f[8 * j + 4], f[8 * j + 5]);
         w.w = Pack<BF16>::two(f[8 * j + 6], f[8 * j + 7]);
-        *reinterpret_cast<uint4*>(atom + sw128_offset(r, j0 + j)) = w;
+        sts128(smem_u32(atom) + sw128_offset(r, j0 + j), w);
       }
     };
     // columns [c_lo, c_hi) of the accumulator at TMEM column tbase -> activation tile sAct

@@ -179,6 +179,18 @@ template <> struct Pack<true> {
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// explicit shared-space 16 B accesses (generic pointers derived from the aligned dynamic smem base
+// compile to LD.E / ST.E through the generic path; these stay LDS / STS)
+__device__ __forceinline__ void sts128(uint32_t addr, const uint4& v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
 // byte offset of 16 B chunk `chunk16` of row r in a [rows][128 B] K-major tile with 128 B swizzle
 // (the layout TMA SWIZZLE_128B writes and the tcgen05 SW128 descriptor reads; tile 1024 B aligned)
 __device__ __forceinline__ uint32_t sw128_offset(int r, int chunk16) {

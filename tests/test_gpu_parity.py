@@ -121,6 +121,19 @@ def test_paper_stack_tensor_core(prec):
     _check_scores(got, p, z, prec, f"paper {prec}")
 
 
+@pytest.mark.parametrize("env", [{"COLD_TAIL": "2"}, {"COLD_TAIL": "1"}, {"COLD_TAIL": "0"}, {"COLD_PAIR": "2"},
+                                 {"COLD_PAIR": "0", "COLD_RESB": "0"}, {"COLD_GSPAN": "1"}, {"COLD_GSPAN": "3"}])
+def test_kernel_variants_match_oracle(env, monkeypatch):
+    """Every kernel variant the library can select (fused tail FC3-5 / FC4-5 / none, CTA-pair or
+    single-CTA GEMMs, gather spans of 1 or 3 chunks) on several chunks with a ragged tail."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    sch, params, batch = small_case("paper", R=4, n_ads=(1000, 129, 1, 700), precision="f16", cap=50000, seed=33)
+    ctx = make_ctx(sch, params, chunk_ads=512)
+    p, z = _oracle_scores(sch, params, batch)
+    _check_scores(gpu_scores(ctx, batch), p, z, "f16", f"variant {env}")
+
+
 @pytest.mark.parametrize("prec", ["f16", "bf16"])
 def test_chunking_and_batching_invariance(prec):
     """Scores do not depend on the chunk size nor on the other requests."""

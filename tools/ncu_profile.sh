@@ -1,19 +1,27 @@
 #!/bin/bash
-# Run under gpurun: launch list + one `--set full` capture of the FC2 GEMM and of the gather kernel.
-# Usage: bash tools/ncu_profile.sh <tag>
+# Run under gpurun: launch list + one `--set full` capture of each hot kernel (gather, FC1, FC2, tail).
+# Usage: bash tools/ncu_profile.sh <tag> [kernels...]   (default kernels: gather fc1 fc2 tail)
 set -x
 TAG=${1:-r01}
+shift
+KERNELS=${@:-gather fc1 fc2 tail}
 OUT=gpurun_out
-ARGS="--requests 32 --ads 10000 --steps 2 --warmup 1 --no-e2e --no-latency --no-cpu"
+# 32 requests x 9472 ads = 2 full 151552-ad chunks per step
+ARGS=${NCU_ARGS:-"--requests 32 --ads 9472 --steps 2 --warmup 1 --no-e2e --no-latency --no-cpu"}
 python -m paper_2007_16122_b200.build >/dev/null
 # 1. launch list (cold-cache, serialised: compare shares)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
   --log-file $OUT/launches_$TAG.csv python bench.py $ARGS > $OUT/ncu_launch_bench_$TAG.log 2>&1
-# 2. full capture of FC2 (the 2nd gemm launch of a chunk) and of the gather kernel
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 13 -c 1 \
-  -o $OUT/prof_fc2_$TAG python bench.py $ARGS > $OUT/ncu_fc2_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gather_kernel -s 3 -c 1 \
-  -o $OUT/prof_gather_$TAG python bench.py $ARGS > $OUT/ncu_gather_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_kernel -s 12 -c 1 \
-  -o $OUT/prof_fc1_$TAG python bench.py $ARGS > $OUT/ncu_fc1_$TAG.log 2>&1
+for k in $KERNELS; do
+  case $k in
+    gather) RX="regex:gather_kernel";;
+    fc1) RX="regex:^gemm_kernel";;
+    fc2) RX="regex:gemm_pair_kernel";;
+    tail) RX="regex:tail_kernel";;
+    *) RX="regex:$k";;
+  esac
+  timeout 900 ncu --set full --clock-control none --import-source on -k $RX -s 1 -c 1 \
+    -o $OUT/prof_${k}_$TAG python bench.py $ARGS > $OUT/ncu_${k}_$TAG.log 2>&1
+done
+for f in $OUT/prof_*_$TAG.ncu-rep; do python tools/ncu_summary.py $f; done > $OUT/ncu_summary_$TAG.txt 2>&1
 ls -la $OUT
