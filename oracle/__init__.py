@@ -85,6 +85,8 @@ def lib():
                                    C.c_void_p]
         L.orc_pooled_f32.restype = C.c_int32
         L.orc_pooled_f32.argtypes = [C.POINTER(_Model), C.POINTER(_Batch), C.c_void_p, C.c_int64, C.c_void_p]
+        L.orc_se_gates.restype = C.c_int32
+        L.orc_se_gates.argtypes = [C.POINTER(_Model), C.POINTER(_Batch), C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_topk.restype = C.c_int32
         L.orc_topk.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
         _lib = L
@@ -204,6 +206,29 @@ def pooled_f32(model: Model, batch: coldgen.Batch, ad_list=None):
     if rc:
         raise OracleError(rc)
     return out
+
+
+def se_gates(model: Model, batch: coldgen.Batch, ad_list=None):
+    """s_g of every schema group for the listed ads, [n, M] fp64."""
+    bv = BatchView(batch)
+    a, n = _ads(ad_list)
+    n_out = batch.n_ads if a is None else n
+    out = np.empty((n_out, len(model.schema.groups)), np.float64)
+    rc = lib().orc_se_gates(C.byref(model.m), C.byref(bv.b), None if a is None else a.ctypes.data, n,
+                            out.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return out
+
+
+def select_groups(mean_s, K: int):
+    """Feature group selection: rank the groups by importance weight and keep the K with the
+    top weights; ties keep schema order (AMB-16). Returned in ascending schema order."""
+    mean_s = np.asarray(mean_s, np.float64)
+    if not 1 <= K <= len(mean_s):
+        raise OracleError(3)
+    order = sorted(range(len(mean_s)), key=lambda g: (-mean_s[g], g))
+    return sorted(order[:K])
 
 
 def rows(model: Model, batch: coldgen.Batch, g: int, a: int) -> np.ndarray:

@@ -318,6 +318,34 @@ int32_t orc_features(const orc_model* m, const orc_batch* bt, const int64_t* ad_
   return err;
 }
 
+/* SE importance weights of EVERY schema group for the listed ads (§3.2 "Importance
+ * weight calculation" / "Feature group selection"): pool -> linear_log (AMB-3 order) ->
+ * s_g = sigma(w_g . e_g + b_g) (per-group reading AMB-1). s_out: [n_list][M]. The ranking of groups
+ * by the mean of s_g over a sample of ads (AMB-16) selects the top-K groups. */
+int32_t orc_se_gates(const orc_model* m, const orc_batch* bt, const int64_t* ad_list, int64_t n_list,
+                     double* s_out) {
+  if (!m || !bt || !s_out || m->M < 1 || m->k < 1 || m->k > 64 || m->se_dense) return ORC_ERR_ARG;
+  int64_t N = bt->ad_offsets[bt->R];
+  if (!ad_list) n_list = N;
+  int k = m->k;
+  for (int64_t i = 0; i < n_list; i++) {
+    int64_t a = ad_list ? ad_list[i] : i;
+    if (a < 0 || a >= N) return ORC_ERR_ARG;
+    int64_t r = request_of(bt, a);
+    for (int32_t g = 0; g < m->M; g++) {
+      double e[64];
+      int rc = pool(m, bt, g, r, a, e);
+      if (rc) return rc;
+      if (m->linear_log && !m->ll_after_se) for (int d = 0; d < k; d++) e[d] = orc_linear_log(e[d]);
+      double z = 0.0;
+      for (int d = 0; d < k; d++) z += m->se_w[(size_t)g * k + d] * e[d];
+      z += m->se_b[g];
+      s_out[(size_t)i * m->M + g] = orc_sigmoid(z);
+    }
+  }
+  return ORC_OK;
+}
+
 int32_t orc_pooled_f32(const orc_model* m, const orc_batch* bt, const int64_t* ad_list, int64_t n_list,
                        float* out) {
   int rc = check_model(m);

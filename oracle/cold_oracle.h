@@ -91,6 +91,12 @@ int32_t orc_features(const orc_model* m, const orc_batch* bt, const int64_t* ad_
 int32_t orc_pooled_f32(const orc_model* m, const orc_batch* bt, const int64_t* ad_list, int64_t n_list,
                        float* out);
 
+/* SE importance weights s_g of every schema group (selected or not) for the listed ads,
+ * pool -> linear_log -> sigma(w_g . e_g + b_g). out: [n_list][M]. Feature-group
+ * selection ranks groups by the mean over a sample of ads (AMB-16). */
+int32_t orc_se_gates(const orc_model* m, const orc_batch* bt, const int64_t* ad_list, int64_t n_list,
+                     double* s_out);
+
 /* Top-K of one request: stable order by (key desc, position asc), NaN last. */
 int32_t orc_topk(const double* key, int64_t n, int32_t K, int32_t* idx_out, double* key_out);
 

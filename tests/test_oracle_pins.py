@@ -106,6 +106,49 @@ def test_worked_example_features():
     np.testing.assert_allclose(x, s * eh, rtol=1e-14, atol=1e-15)
 
 
+# ---- SE importance weights and feature-group selection (F3) ---------------
+
+def test_se_gates_worked_example():
+    """s_g of ad A in the hand-computed worked example (P-4 golden values)."""
+    schema, params, batch, exp = worked_example("one")
+    s = oracle.se_gates(oracle.Model(schema, params), batch)
+    np.testing.assert_allclose(s[0], exp["adA_se_ll_on"], rtol=1e-14)
+
+
+def test_se_gates_planted_closed_form_and_selection():
+    """w_g = 0, b_g = 3 - 0.5 g: s_g = sigma(b_g) for every ad (P-11 closed form), so ranking by
+    mean s_g selects the first K groups of the schema; every s_g lies in (0, 1)."""
+    sch = coldgen.scaled_schema(coldgen.schema_full(), 2000)
+    params = coldgen.make_params(sch, seed=5, precision="f16", se="planted")
+    batch = coldgen.make_batch(sch, 2, [40, 25], seed=6)
+    s = oracle.se_gates(oracle.Model(sch, params), batch)
+    b = 3.0 - 0.5 * np.arange(len(sch.groups))
+    np.testing.assert_allclose(s, np.broadcast_to(1.0 / (1.0 + np.exp(-b)), s.shape), rtol=1e-15)
+    for K in (1, 8, 20, 32):
+        assert oracle.select_groups(s.mean(0), K) == list(range(K))
+
+
+def test_se_gates_planted_noisy_ranking():
+    """|w_g . ê_g| <= 16 * 0.01 * LL(8) < 0.5 = the b-gaps, so the empirical ranking keeps schema
+    order (P-11 empirical run) and the gates stay within their bounds."""
+    sch = coldgen.scaled_schema(coldgen.schema_full(), 2000)
+    params = coldgen.make_params(sch, seed=7, precision="f16", se="planted_noisy")
+    batch = coldgen.make_batch(sch, 3, [60, 60, 60], seed=8)
+    s = oracle.se_gates(oracle.Model(sch, params), batch)
+    assert np.all((s > 0) & (s < 1))
+    assert oracle.select_groups(s.mean(0), 12) == list(range(12))
+    b = 3.0 - 0.5 * np.arange(len(sch.groups))
+    lo, hi = 1 / (1 + np.exp(-(b - 0.5))), 1 / (1 + np.exp(-(b + 0.5)))
+    assert np.all((s >= lo) & (s <= hi))
+
+
+def test_select_groups_ties_and_range():
+    assert oracle.select_groups([0.5, 0.7, 0.5, 0.7], 3) == [0, 1, 3]
+    assert oracle.select_groups([0.1, 0.2], 2) == [0, 1]
+    with pytest.raises(oracle.OracleError):
+        oracle.select_groups([0.1, 0.2], 3)
+
+
 # ---- P-6 reduction to library routines (torch fp64) ---------------------------------
 
 def test_reduces_to_torch_embedding_bag_mlp():
