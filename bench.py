@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--latency-requests", type=int, default=1000)
     ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--se-sweep", action="store_true",
+                    help="BASELINE configs[3]: SE-selected group subsets of S-full, ads/s vs group count")
+    ap.add_argument("--se-sample", type=int, default=10000, help="ads in the SE statistics sample (AMB-16)")
     return ap.parse_args()
 
 
@@ -226,10 +229,91 @@ def config_dict(args, sch):
 
 
 # --------------------------------------------------------------------------------------------
+def run_se_sweep(args):
+    """BASELINE configs[3]: S-full (8 user + 8 ad + 16 cross groups), planted SE
+    importance (w ~ U(-.01,.01), b_g = 3 - 0.5 g). The GPU computes mean s_g of every group over a
+    10^4-ad sample (cold_se_stats), the top-K_g groups are selected, and each
+    lighter model (its own FC1 over D_in = 16 K_g) is timed on 512 requests x 4000 ads + top-500."""
+    import torch
+    from paper_2007_16122_b200 import Batch, Context, select_groups
+    from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER
+    import oracle
+    torch.cuda.set_device(0)
+    sch = coldgen.schema_full()
+    R, n_ads, K = 512, 4000, args.topk
+    full = coldgen.make_params(sch, seed=args.seed, precision=args.precision, se="planted_noisy")
+    sample = coldgen.make_batch(sch, range(2 * 10**7, 2 * 10**7 + max(1, -(-args.se_sample // n_ads))), n_ads,
+                                seed=args.seed + 2)
+    ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, max_ads=sample.n_ads,
+                  max_requests=sample.R)
+    load_ctx_params(ctx, full)
+    mean_s = ctx.se_stats(Batch.from_numpy(sample.ad_offsets, sample.ids, sample.offs))
+    ctx.close()
+    want = oracle.se_gates(oracle.Model(sch, full), sample).mean(0)   # same sample, fp64 (parity check)
+    batch = coldgen.make_batch(sch, range(R), n_ads, seed=args.seed + 1)
+    db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs)
+    dev = torch.device("cuda", 0)
+    scores = torch.empty(batch.n_ads, dtype=torch.float32, device=dev)
+    idx = torch.empty(R * K, dtype=torch.int32, device=dev)
+    key = torch.empty(R * K, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    rows = []
+    for kg in (8, 12, 16, 20, 24, 28, 32):
+        sel = select_groups(mean_s, kg)
+        params = coldgen.make_params(sch, seed=args.seed, precision=args.precision, se="planted_noisy",
+                                     d_in=kg * sch.k)
+        c = Context(sch.groups, sch.k, sch.widths, precision=args.precision, selected=sel, max_ads=batch.n_ads,
+                    max_requests=R)
+        load_ctx_params(c, params)
+
+        def step():
+            c.score_batch(db, scores)
+            c.topk(scores, db.ad_offsets, batch.ad_offsets, K, idx, key)
+
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        c.profile(True)
+        for _ in range(args.steps):
+            step()
+        pm, pn = c.profile_read()
+        c.profile(False)
+        info = c.info()
+        flops = fc_flops_per_ad(sch, info["d_ad"])
+        fc_ms = sum(pm[PROF_FC + l] for l in range(len(sch.widths)))
+        n_user = sum(1 for g in sel if sch.groups[g].side == coldgen.USER)
+        rows.append({"k_g": kg, "selected_user_ad_cross": [n_user, sum(1 for g in sel if sch.groups[g].side == coldgen.AD),
+                                                            sum(1 for g in sel if sch.groups[g].side == coldgen.CROSS)],
+                     "d_in": info["d_in"], "d_ad_cross": info["d_ad"], "ads_per_s": batch.n_ads / (ms / 1e3),
+                     "ms_per_step": ms, "fc_tflops": batch.n_ads * args.steps * sum(flops) / (fc_ms / 1e3) / 1e12,
+                     "gather_ms": float(pm[PROF_GATHER] / args.steps), "fc_ms": float(fc_ms / args.steps)})
+        c.close()
+    line = {"metric": METRIC, "value": rows[-1]["ads_per_s"], "unit": "ads/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "dtype": args.precision,
+            "data": "synthetic (seeded ids, tables, weights; planted SE importance)",
+            "config": {"workload": f"BASELINE configs[3]: S-full (M=32: 8 user + 8 ad + 16 cross), {R} requests x "
+                                   f"{n_ads} ads, top-{K}; groups selected by mean SE weight over a "
+                                   f"{sample.n_ads}-ad sample (cold_se_stats)"},
+            "se_mean_s": [round(float(x), 6) for x in mean_s],
+            "se_mean_s_oracle_maxdiff": float(np.max(np.abs(mean_s - want))),
+            "se_sweep": rows}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.se_sweep:
+        run_se_sweep(args)
         return
     import torch
     import torch.distributed as dist
@@ -435,6 +519,60 @@ def main():
                    "p99_ms": float(np.percentile(lat, 99)), "mean_ms": float(lat.mean()),
                    "timing": "device events per request (score + top-500), requests back to back on one stream"}
 
+    # ---- F1: one request's ads split across all ranks (world > 1), per-rank top-K, NCCL all-gather
+    # of the candidate lists, cold_merge_topk; p50 / p99 per request at N = args.ads ----
+    latency_split = None
+    if not args.no_latency and world > 1:
+        try:
+            from paper_2007_16122_b200.dist import slice_requests
+            nl = min(args.latency_requests, 500)
+            lb = coldgen.make_batch(sch, range(3 * 10**7, 3 * 10**7 + nl), args.ads, seed=args.seed + 3)
+            sides = [g.side for g in sch.groups]
+            mine = []
+            for i in range(nl):
+                one = coldgen.sub_batch(lb, [i])
+                ao_s, ids_s, offs_s, _ = slice_requests(one.ad_offsets, one.ids, one.offs, sides, world, rank)
+                mine.append(Batch.from_numpy(ao_s, ids_s, offs_s))
+            n_mine = int(ao_s[-1])
+            sscores = torch.empty(n_mine, dtype=torch.float32, device=dev)
+            lidx = torch.empty(K, dtype=torch.int32, device=dev)
+            lkey = torch.empty(K, dtype=torch.float32, device=dev)
+            cidx = torch.empty(world * K, dtype=torch.int32, device=dev)
+            ckey = torch.empty(world * K, dtype=torch.float32, device=dev)
+            midx = torch.empty(K, dtype=torch.int32, device=dev)
+            mkey = torch.empty(K, dtype=torch.float32, device=dev)
+            ao_full = np.asarray([0, args.ads], np.int32)
+            d_ao_full = torch.from_numpy(ao_full).to(dev)
+            ao_loc = np.asarray([0, n_mine], np.int32)
+
+            def split_request(b):
+                ctx.score_request(b, sscores)
+                ctx.topk(sscores, b.ad_offsets, ao_loc, K, lidx, lkey)
+                dist.all_gather_into_tensor(ckey, lkey)
+                dist.all_gather_into_tensor(cidx, lidx)
+                ctx.merge_topk(ckey, cidx, world, K, d_ao_full, ao_full, K, midx, mkey)
+
+            for i in range(min(10, nl)):
+                split_request(mine[i])
+            torch.cuda.synchronize()
+            dist.barrier()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
+            for i in range(nl):
+                evs[i][0].record(stream)
+                split_request(mine[i])
+                evs[i][1].record(stream)
+            torch.cuda.synchronize()
+            lat = torch.tensor([a.elapsed_time(b) for a, b in evs], dtype=torch.float64, device=dev)
+            dist.all_reduce(lat, op=dist.ReduceOp.MAX)
+            lat = lat.cpu().numpy()
+            latency_split = {"n_ads": args.ads, "requests": nl, "gpus": world, "p50_ms": float(np.percentile(lat, 50)),
+                             "p99_ms": float(np.percentile(lat, 99)), "mean_ms": float(lat.mean()),
+                             "ads_per_s": args.ads / (float(lat.mean()) / 1e3),
+                             "timing": "per request, max over ranks of device events: score own slice + top-K, "
+                                       "NCCL all-gather of the G candidate lists, cold_merge_topk (F1)"}
+        except Exception as exc:   # optional section: report, keep the headline line
+            latency_split = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_oracle_sample(sch, params, batch)
@@ -447,7 +585,7 @@ def main():
             "config": config_dict(args, sch),
             "roofline": roofline, "roofline_gather": roofline_gather, "fc_stack": fc_stack,
             "kernels": per_kernel, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
-            "clocks": clocks, "latency": latency, "setup_s": setup_s,
+            "clocks": clocks, "latency": latency, "latency_split": latency_split, "setup_s": setup_s,
             "profiled_region": {"ms_per_step": ms_prof / args.steps,
                                 "note": "per-kernel CUDA events (kernels, roofline) come from this second timed "
                                         "region of the same steps"},

@@ -161,7 +161,41 @@ cold_status cold_topk(cold_ctx* ctx, const float* scores, const int32_t* ad_offs
                       const int32_t* ad_offsets_host, int32_t R, int32_t K, const float* bids,
                       int32_t* idx_out, float* key_out, void* stream);
 
+/* ---- intra-request ad split across GPUs (P:248-250 / P:496-498: a query's
+ * ads are split, scored in parallel, and the partial results merged) --------------------------
+ * Split rule: rank g of G owns ads [floor(g * n_r / G), floor((g + 1) * n_r / G)) of request r
+ * (n_r = ad_offsets[r+1] - ad_offsets[r]). Each rank scores its slices and runs cold_topk with
+ * K = Kl on them; the G lists are all-gathered (e.g. NCCL all_gather_into_tensor) into
+ * cand_key / cand_idx of layout [G][R][Kl] (rank-major), cand_idx = positions inside the rank's
+ * slice as cold_topk returns them. cold_merge_topk then selects, per request, the K best of the
+ * G * Kl candidates by (key desc, position asc) — identical to cold_topk over the unsplit request
+ * whenever every slice has >= Kl ads and K <= Kl (ties: candidates are visited in rank order, and
+ * within a rank in position order, which is request position order).
+ * idx_out[r*K + i] = position within request r; key_out[r*K + i] = key. All buffers device memory
+ * except ad_offsets_host. Errors: COLD_ERR_K_RANGE if K > Kl or a slice has < Kl ads. */
+cold_status cold_merge_topk(cold_ctx* ctx, const float* cand_key, const int32_t* cand_idx, int32_t G, int32_t R,
+                            int32_t Kl, const int32_t* ad_offsets, const int32_t* ad_offsets_host, int32_t K,
+                            int32_t* idx_out, float* key_out, void* stream);
+
 cold_status cold_get_info(const cold_ctx* ctx, cold_info* out);
+
+/* ---- feature-group selection (§3.2 "Importance weight calculation" / "Feature group
+ * selection") ------------------------------------------------------------ */
+
+/* SE importance weights of EVERY schema group (selected or not) averaged over the ads of a
+ * batch: mean_s_out[g] = (1 / N_tot) * sum over ads of s_g, s_g = sigma(w_g . LL(e_g) + b_g)
+ * (per-group SE, AMB-1; a user group's s_g is shared by all ads of its request). The batch must
+ * be device memory and carry the ids of every non-cross group. mean_s_out: HOST [M] fp64.
+ * Runs on `stream` and synchronises it. Errors: as cold_score_batch; COLD_ERR_INVALID_ARG for a
+ * host batch. The per-ad sums are accumulated with fp64 atomics, so the last bits may vary run
+ * to run; the ranking below is insensitive to that except at exact ties. */
+cold_status cold_se_stats(cold_ctx* ctx, const cold_batch* batch, double* mean_s_out, void* stream);
+
+/* Host helper: the K groups with the largest mean_s (ties: lower schema index first), written
+ * in ascending schema order to selected_out[K] — the `selected` list of a lighter COLD
+ * ("select K groups of features with top weights"). Errors: COLD_ERR_K_RANGE unless
+ * 1 <= K <= M; COLD_ERR_INVALID_ARG for NULL pointers. */
+cold_status cold_select_groups(const double* mean_s, int32_t M, int32_t K, int32_t* selected_out);
 
 /* ---- per-kernel timing (bench) -------------------------------------------------------- */
 

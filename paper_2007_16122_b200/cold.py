@@ -26,7 +26,8 @@ STATUS = {0: "COLD_OK", 1: "COLD_ERR_INVALID_ARG", 2: "COLD_ERR_SHAPE", 3: "COLD
 
 EXPORTS = ["cold_create", "cold_destroy", "cold_load_params", "cold_score_batch", "cold_score_request",
            "cold_topk", "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
-           "cold_status_string", "cold_last_error", "cold_profile", "cold_profile_read"]
+           "cold_status_string", "cold_last_error", "cold_profile", "cold_profile_read", "cold_se_stats",
+           "cold_select_groups", "cold_merge_topk"]
 PROF_KINDS = 3 + 16
 PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC = 0, 1, 2, 3
 
@@ -93,6 +94,10 @@ def lib() -> C.CDLL:
         L.cold_debug_features.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_void_p, C.c_void_p]
         L.cold_debug_rows.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_int32, C.c_void_p, C.c_int32,
                                       C.c_void_p]
+        L.cold_se_stats.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_void_p, C.c_void_p]
+        L.cold_select_groups.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        L.cold_merge_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.cold_profile.argtypes = [C.c_void_p, C.c_int32]
         L.cold_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.cold_status_string.restype = C.c_char_p
@@ -100,7 +105,8 @@ def lib() -> C.CDLL:
         L.cold_last_error.restype = C.c_char_p
         for f in ["cold_create", "cold_load_params", "cold_score_batch", "cold_score_request", "cold_topk",
                   "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
-                  "cold_profile", "cold_profile_read"]:
+                  "cold_profile", "cold_profile_read", "cold_se_stats", "cold_select_groups",
+                  "cold_merge_topk"]:
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -235,6 +241,14 @@ class Context:
         _check(lib().cold_topk(self.ctx, _addr(scores), _addr(ad_offsets), aoh.ctypes.data, len(aoh) - 1, K,
                                _addr(bids), _addr(idx_out), _addr(key_out), _stream_handle(stream)))
 
+    def merge_topk(self, cand_key, cand_idx, G: int, Kl: int, ad_offsets, ad_offsets_host, K: int, idx_out, key_out,
+                   stream=None):
+        """Merge all-gathered per-rank top-Kl lists [G][R][Kl] into the per-request top-K (F1)."""
+        aoh = np.ascontiguousarray(ad_offsets_host, np.int32)
+        _check(lib().cold_merge_topk(self.ctx, _addr(cand_key), _addr(cand_idx), G, len(aoh) - 1, Kl,
+                                     _addr(ad_offsets), aoh.ctypes.data, K, _addr(idx_out), _addr(key_out),
+                                     _stream_handle(stream)))
+
     def info(self) -> dict:
         i = cold_info()
         _check(lib().cold_get_info(self.ctx, C.byref(i)))
@@ -250,6 +264,12 @@ class Context:
         _check(lib().cold_profile_read(self.ctx, ms.ctypes.data, n.ctypes.data))
         return ms, n
 
+    def se_stats(self, batch: Batch, stream=None) -> np.ndarray:
+        """Mean SE importance weight of every schema group over the batch's ads (cold_se_stats)."""
+        out = np.zeros(len(self._groups), np.float64)
+        _check(lib().cold_se_stats(self.ctx, C.byref(batch.c), out.ctypes.data, _stream_handle(stream)))
+        return out
+
     def debug_pooled(self, batch: Batch, out, stream=None):
         _check(lib().cold_debug_pooled(self.ctx, C.byref(batch.c), _addr(out), _stream_handle(stream)))
 
@@ -259,3 +279,11 @@ class Context:
     def debug_rows(self, batch: Batch, group: int, rows_out, max_rows: int, stream=None):
         _check(lib().cold_debug_rows(self.ctx, C.byref(batch.c), group, _addr(rows_out), max_rows,
                                      _stream_handle(stream)))
+
+
+def select_groups(mean_s, K: int):
+    """The K groups with the largest mean SE weight, ascending schema order (cold_select_groups)."""
+    m = np.ascontiguousarray(mean_s, np.float64)
+    out = np.empty(K, np.int32)
+    _check(lib().cold_select_groups(m.ctypes.data, len(m), K, out.ctypes.data))
+    return [int(x) for x in out]

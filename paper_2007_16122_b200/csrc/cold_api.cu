@@ -424,7 +424,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       c->resb[l] = c->cs[l] == 1 && gemm_resident_ok(c->bn[l], K) && !(env_resb && atoi(env_resb) == 0);
       // CTA pairs for the 256-wide layers that are not fused into the tail (FC1, FC2)
       const char* env_pair = getenv("COLD_PAIR");
-      const int pair_mode = env_pair ? atoi(env_pair) : 1;   // 0 off, 1 non-resident 256-wide, 2 all 256-wide
+      const int pair_mode = env_pair ? atoi(env_pair) : 2;   // 0 off, 1 non-resident 256-wide, 2 all 256-wide
       const bool in_tail = c->n_tail && l >= Lg - c->n_tail;
       c->pair[l] = !in_tail && l < Lg - 1 && c->bn[l] == 256 &&
                    (pair_mode == 2 || (pair_mode == 1 && !c->resb[l]));
@@ -636,7 +636,7 @@ struct CallPlan {
   BatchView bv;                 // device-mode view (host mode: per chunk)
 };
 
-static cold_status plan_batch(cold_ctx* c, const cold_batch* b, CallPlan& pl) {
+static cold_status plan_batch(cold_ctx* c, const cold_batch* b, CallPlan& pl, bool all_groups = false) {
   if (!b || !b->ad_offsets || !b->ad_offsets_host || !b->ids || !b->offs)
     return fail(COLD_ERR_INVALID_ARG, "batch arrays missing");
   const int R = b->num_requests;
@@ -650,7 +650,12 @@ static cold_status plan_batch(cold_ctx* c, const cold_batch* b, CallPlan& pl) {
   pl.N = ao[R];
   if (pl.N > c->max_ads) return fail(COLD_ERR_CAPACITY, "more ads than max_ads_per_call");
   std::vector<char> need(c->M, 0);
-  for (int g : c->sel) {
+  std::vector<int> groups_used = c->sel;
+  if (all_groups) {
+    groups_used.clear();
+    for (int g = 0; g < c->M; g++) groups_used.push_back(g);
+  }
+  for (int g : groups_used) {
     if (c->groups[g].side == COLD_CROSS) { need[c->groups[g].user_ref] = 1; need[c->groups[g].ad_ref] = 1; }
     else need[g] = 1;
   }
@@ -1067,6 +1072,69 @@ extern "C" cold_status cold_debug_rows(cold_ctx* c, const cold_batch* b, int32_t
 }
 
 // ---------------------------------------------------------------------------------------------
+// feature-group selection statistics
+extern "C" cold_status cold_se_stats(cold_ctx* c, const cold_batch* b, double* mean_s_out, void* stream) {
+  if (!c || !mean_s_out) return fail(COLD_ERR_INVALID_ARG, "null ctx / output");
+  if (!c->loaded) return fail(COLD_ERR_NOT_LOADED, "cold_load_params has not been called");
+  CallPlan pl;
+  cold_status s = plan_batch(c, b, pl, true);
+  if (s) return s;
+  if (pl.host) return fail(COLD_ERR_INVALID_ARG, "cold_se_stats takes a device batch");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  cudaGetLastError();
+  double* d_stats = nullptr;
+  if (cudaMallocAsync((void**)&d_stats, sizeof(double) * c->M, st) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(COLD_ERR_OOM, "stats buffer");
+  }
+  CK(cudaMemsetAsync(d_stats, 0, sizeof(double) * c->M, st));
+  if (c->flags & COLD_VALIDATE_IDS) CK(cudaMemsetAsync(c->d_err, 0, 4, st));
+  // user side: every USER group of the schema, s_g weighted by the request's ad count
+  UserArgs ua = make_user_args(c, pl, b->ad_offsets, DebugOut());
+  ua.n_user = 0;
+  for (int g = 0; g < c->M; g++)
+    if (c->groups[g].side == COLD_USER) ua.user_g[ua.n_user++] = g;
+  ua.stats = d_stats;
+  launch_user(ua, pl.R, c->precision, st);   // also builds the ad -> request map
+  // ad + cross side: every non-user group, column-wise over all ads of the batch
+  GatherArgs ga = make_gather_args(c, pl.bv, 0, pl.N, DebugOut());
+  ga.n_ac = 0;
+  for (int pass = 0; pass < 3; pass++)
+    for (int g = 0; g < c->M; g++) {
+      const cold_group& G = c->groups[g];
+      if (G.side == COLD_USER) continue;
+      const int cls = G.side == COLD_CROSS ? 0 : (G.pooled ? 1 : 2);
+      if (cls == pass) ga.ac_g[ga.n_ac++] = g;
+    }
+  for (int j = 0; j < ga.n_ac; j++) ga.order[j] = j;
+  ga.X = nullptr;
+  ga.stats = d_stats;
+  launch_gather(ga, c->precision, st);
+  CK(cudaGetLastError());
+  std::vector<double> h(c->M);
+  CK(cudaMemcpyAsync(h.data(), d_stats, sizeof(double) * c->M, cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d_stats, st));
+  CK(cudaStreamSynchronize(st));
+  s = check_err(c, st);
+  if (s) return s;
+  for (int g = 0; g < c->M; g++) mean_s_out[g] = h[g] / (double)pl.N;
+  return COLD_OK;
+}
+
+extern "C" cold_status cold_select_groups(const double* mean_s, int32_t M, int32_t K, int32_t* selected_out) {
+  if (!mean_s || !selected_out) return fail(COLD_ERR_INVALID_ARG, "null pointer");
+  if (M < 1 || K < 1 || K > M) return fail(COLD_ERR_K_RANGE, "K must be in [1, M]");
+  std::vector<int> order(M);
+  for (int g = 0; g < M; g++) order[g] = g;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return mean_s[x] > mean_s[y]; });
+  std::vector<int> top(order.begin(), order.begin() + K);
+  std::sort(top.begin(), top.end());
+  for (int i = 0; i < K; i++) selected_out[i] = top[i];
+  return COLD_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
 extern "C" cold_status cold_topk(cold_ctx* c, const float* scores, const int32_t* ad_offsets,
                                  const int32_t* ad_offsets_host, int32_t R, int32_t K, const float* bids,
                                  int32_t* idx_out, float* key_out, void* stream) {
@@ -1126,6 +1194,9 @@ extern "C" cold_status cold_topk(cold_ctx* c, const float* scores, const int32_t
   }
   ta.R = R;
   ta.K = K;
+  ta.G = 0;
+  ta.Kl = 0;
+  ta.cand_idx = nullptr;
   ta.idx = out_dev ? idx_out : (int32_t*)c->d_topk_out;
   ta.key = out_dev ? key_out : (float*)((uint8_t*)c->d_topk_out + (size_t)R * K * 4);
   c->mark_begin(st);
@@ -1136,6 +1207,50 @@ extern "C" cold_status cold_topk(cold_ctx* c, const float* scores, const int32_t
     CK(cudaMemcpyAsync(idx_out, ta.idx, (size_t)R * K * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(key_out, ta.key, (size_t)R * K * 4, cudaMemcpyDeviceToHost, st));
   }
+  return COLD_OK;
+}
+
+// F1: merge of per-rank top-K lists when one request's ads are split across G GPUs
+extern "C" cold_status cold_merge_topk(cold_ctx* c, const float* cand_key, const int32_t* cand_idx, int32_t G,
+                                       int32_t R, int32_t Kl, const int32_t* ad_offsets,
+                                       const int32_t* ad_offsets_host, int32_t K, int32_t* idx_out, float* key_out,
+                                       void* stream) {
+  if (!c) return fail(COLD_ERR_INVALID_ARG, "null ctx");
+  if (!cand_key || !cand_idx || !ad_offsets || !ad_offsets_host || !idx_out || !key_out)
+    return fail(COLD_ERR_INVALID_ARG, "null pointer");
+  if (G < 1 || R < 1 || Kl < 1) return fail(COLD_ERR_INVALID_ARG, "G, R, Kl must be >= 1");
+  if ((int64_t)G * Kl > (1 << 30)) return fail(COLD_ERR_INVALID_ARG, "too many candidates");
+  if (K < 1 || K > Kl) return fail(COLD_ERR_K_RANGE, "K must be in [1, Kl]");
+  if (K > 4096) return fail(COLD_ERR_UNSUPPORTED, "K > 4096");
+  if (ad_offsets_host[0] != 0) return fail(COLD_ERR_INVALID_ARG, "ad_offsets[0] must be 0");
+  for (int r = 0; r < R; r++) {
+    const int64_t n = (int64_t)ad_offsets_host[r + 1] - ad_offsets_host[r];
+    for (int g = 0; g < G; g++) {   // every slice must have supplied Kl real candidates
+      const int64_t sl = (int64_t)(g + 1) * n / G - (int64_t)g * n / G;
+      if (sl < Kl) return fail(COLD_ERR_K_RANGE, "a rank's slice of a request has fewer than Kl ads");
+    }
+  }
+  for (const void* p : {(const void*)cand_key, (const void*)cand_idx, (const void*)ad_offsets, (const void*)idx_out,
+                        (const void*)key_out})
+    if (!is_device_ptr(p)) return fail(COLD_ERR_INVALID_ARG, "cold_merge_topk takes device buffers");
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaSetDevice(c->device));
+  cudaGetLastError();
+  TopkArgs ta;
+  memset(&ta, 0, sizeof(ta));
+  ta.scores = cand_key;
+  ta.ad_offsets = ad_offsets;
+  ta.R = R;
+  ta.K = K;
+  ta.G = G;
+  ta.Kl = Kl;
+  ta.cand_idx = cand_idx;
+  ta.idx = idx_out;
+  ta.key = key_out;
+  c->mark_begin(st);
+  launch_topk(ta, st);
+  c->mark_end(COLD_PROF_TOPK, st);
+  CK(cudaGetLastError());
   return COLD_OK;
 }
 

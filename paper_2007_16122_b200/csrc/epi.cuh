@@ -17,13 +17,19 @@ constexpr int EPI_WIDE_BOX = 32 * EPI_WIDE_COLS * 2;   // 4 KB, single-buffered 
 template <bool BF16>
 __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int c_end, const float* __restrict__ bias,
                                                uint32_t u1s, const float* __restrict__ u1g, int relu, uint8_t* buf,
-                                               const CUtensorMap* tmC, int col_base, int row0, int lane) {
+                                               const CUtensorMap* tmC, int col_base, int row0, int lane,
+                                               int dbg = 0) {
   const uint32_t sbuf = smem_u32(buf);
   for (int c = c_begin; c < c_end; c += EPI_WIDE_COLS) {
     uint32_t v[64];
-    TMEM_LD32(taddr + c, v);
-    TMEM_LD32(taddr + c + 32, (v + 32));
-    tmem_wait_ld();
+    if (dbg != 5) {
+      TMEM_LD32(taddr + c, v);
+      TMEM_LD32(taddr + c + 32, (v + 32));
+      tmem_wait_ld();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; i++) v[i] = (uint32_t)(lane + i);
+    }
     const int col0 = col_base + c;
     float f[64];
 #pragma unroll
@@ -55,6 +61,13 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
     uint32_t pk[32];
 #pragma unroll
     for (int i = 0; i < 32; i++) pk[i] = Pack<BF16>::two(f[2 * i], f[2 * i + 1]);
+    if (dbg == 3) {                       // timing experiment: no smem staging / store
+      uint32_t t = 0;
+#pragma unroll
+      for (int i = 0; i < 32; i++) t ^= pk[i];
+      if (t == 0x12345678u) asm volatile("st.global.u32 [%0], %1;" ::"l"(bias), "r"(t));
+      continue;
+    }
     if (lane == 0) bulk_wait_read<0>();   // the previous box of this warp has left shared memory
     __syncwarp();
     const uint32_t rowp = sbuf + (uint32_t)lane * 128u;
@@ -63,7 +76,7 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
       sts128(rowp + (uint32_t)((j ^ (lane & 7)) << 4), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
     fence_async_smem();
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && dbg != 4) {
       tma_store_2d(tmC, buf, col0, row0);
       bulk_commit();
     }

@@ -27,6 +27,8 @@ struct UserArgs {
   float* dbg_pooled;               // [N][n_sel][k]
   float* dbg_feat;                 // [N][D_in]
   int n_sel, d_in;
+  double* stats;                   // SE statistics mode (cold_se_stats): [M] += s_g * ads of the request;
+                                   // x_u / u1 are not written
 };
 
 struct GatherArgs {
@@ -49,6 +51,7 @@ struct GatherArgs {
   float* dbg_pooled;               // [N][n_sel][k] (call-global rows)
   float* dbg_feat;                 // [N][D_in]
   int n_sel, d_in;
+  double* stats;                   // SE statistics mode: [M] += s_g per ad; X is not written
 };
 
 struct RowsArgs {
@@ -126,6 +129,11 @@ struct TopkArgs {
   const float* scores; const float* bids; const int32_t* ad_offsets;
   int R; int K;
   int32_t* idx; float* key;
+  // merge mode (G > 0, cold_merge_topk): `scores` holds the all-gathered per-rank top-Kl keys
+  // [G][R][Kl], `cand_idx` their positions inside each rank's slice; request r's candidates are
+  // (g, j) in rank order; the output position is cand_idx + the slice start floor(g * n_r / G)
+  int G, Kl;
+  const int32_t* cand_idx;
 };
 void launch_topk(const TopkArgs& a, cudaStream_t s);
 

@@ -8,6 +8,8 @@
 //                  AD/CROSS group, threads = consecutive ads. Cross rows are hashed from the user
 //                  bag x the ad bag (AMB-9), rows gathered with 16 B vector loads, pooled in fp32
 //                  in bag order, linear_log -> SE gate -> v -> RNE cast into X_ac (A3-A5).
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace cold {
@@ -85,6 +87,10 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
 #pragma unroll
     for (int off = 16; off; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
     const float s = sigmoid(z + a.se_b[g]);
+    if (a.stats) {                          // SE statistics: every ad of the request shares s_g
+      if (lane == 0) atomicAdd(a.stats + g, (double)s * (double)(a.ad_offsets[r + 1] - a.ad_offsets[r]));
+      continue;
+    }
     if (lane < K) {
       const float v = s * e;
       xs[j * K + lane] = v;
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
   }
   __syncthreads();
   // u1[r][o] = b1[o] + sum_i W1u[o][i] x_u[i]   (W1u stored transposed: coalesced over o)
-  for (int o = threadIdx.x; o < a.H; o += blockDim.x) {
+  for (int o = threadIdx.x; o < a.H && !a.stats; o += blockDim.x) {
     float acc = a.b1[o];
     for (int i = 0; i < d_u; i++) acc = fmaf(a.w1u_t[(int64_t)i * a.H + o], xs[i], acc);
     a.u1[(int64_t)r * a.H + o] = acc;
@@ -162,6 +168,10 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
 #pragma unroll
   for (int d = 0; d < K; d++) z = fmaf(__ldg(a.se_w + g * K + d), e[d], z);
   const float s = sigmoid_t<FAST>(z + __ldg(a.se_b + g));
+  if (a.stats) {                            // SE statistics mode (cold_se_stats)
+    atomicAdd(a.stats + g, (double)s);
+    return;
+  }
   alignas(16) T out[K];
 #pragma unroll
   for (int d = 0; d < K; d++) out[d] = Store<T>::from_f(s * e[d]);
@@ -186,11 +196,13 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
   }
 }
 
-template <typename T, int K, bool FAST>
-__global__ void __launch_bounds__(128, 4) gather_kernel(GatherArgs a) {
+template <typename T, int K, bool FAST, int MINB = 4>
+__global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
   constexpr bool VEC = (K * (int)sizeof(T)) % 16 == 0;
   constexpr int NV = K * (int)sizeof(T) / 16;
-  constexpr int GATHER_RB = NV <= 2 ? 8 : (NV == 4 ? 4 : 2);   // bag rows in flight (<= 16 vectors)
+  // bag rows in flight per thread (<= 16 vectors of raw registers; halved when the register budget
+  // is halved for twice the resident warps)
+  constexpr int GATHER_RB = (NV <= 2 ? 8 : (NV == 4 ? 4 : 2)) / (MINB >= 8 ? 2 : 1);
   __shared__ uint64_t s_hx[2][HX_HALF];
   const int j = a.order[blockIdx.y];
   const int g = a.ac_g[j];
@@ -402,7 +414,12 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
     case 2: gather_kernel<T, 2, FAST><<<grid, 128, 0, s>>>(a); break;
     case 4: gather_kernel<T, 4, FAST><<<grid, 128, 0, s>>>(a); break;
     case 8: gather_kernel<T, 8, FAST><<<grid, 128, 0, s>>>(a); break;
-    case 16: gather_kernel<T, 16, FAST><<<grid, 128, 0, s>>>(a); break;
+    case 16: {
+      static const int minb = getenv("COLD_GATHER_MINB") ? atoi(getenv("COLD_GATHER_MINB")) : 8;
+      if (minb >= 8) gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
+      else gather_kernel<T, 16, FAST><<<grid, 128, 0, s>>>(a);
+      break;
+    }
     case 32: gather_kernel<T, 32, FAST><<<grid, 128, 0, s>>>(a); break;
   }
 }

@@ -31,12 +31,18 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
   extern __shared__ unsigned long long cand[];            // [P] composites, P = pow2 >= K
 
   const int r = blockIdx.x;
-  const int64_t base = a.ad_offsets[r];
-  const int n = (int)(a.ad_offsets[r + 1] - base);
+  const bool merge = a.G > 0;
+  const int64_t base = merge ? 0 : a.ad_offsets[r];
+  const int n = merge ? a.G * a.Kl : (int)(a.ad_offsets[r + 1] - base);
   const int K = a.K;
+  // merge mode: candidate i = (rank g, slot j) lives at [(g * R + r) * Kl + j]
+  auto addr = [&](int i) -> int64_t {
+    return merge ? ((int64_t)(i / a.Kl) * a.R + r) * a.Kl + (i % a.Kl) : base + i;
+  };
   auto key_at = [&](int i) -> uint32_t {
-    float v = a.scores[base + i];
-    if (a.bids) v *= a.bids[base + i];
+    const int64_t ai = addr(i);
+    float v = a.scores[ai];
+    if (a.bids && !merge) v *= a.bids[ai];
     return orderable(v);
   };
 
@@ -116,9 +122,16 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
       __syncthreads();
     }
   }
+  const int n_r = merge ? (int)(a.ad_offsets[r + 1] - a.ad_offsets[r]) : 0;
   for (int i = threadIdx.x; i < K; i += blockDim.x) {
     const unsigned long long c = cand[i];
-    a.idx[(int64_t)r * K + i] = (int32_t)(0xffffffffu - (uint32_t)(c & 0xffffffffu));
+    const int w = (int)(0xffffffffu - (uint32_t)(c & 0xffffffffu));
+    int32_t pos = w;
+    if (merge) {   // slice-local position -> position within the request (split rule of cold_merge_topk)
+      const int g = w / a.Kl;
+      pos = a.cand_idx[addr(w)] + (int32_t)(((int64_t)g * n_r) / a.G);
+    }
+    a.idx[(int64_t)r * K + i] = pos;
     a.key[(int64_t)r * K + i] = from_orderable((uint32_t)(c >> 32));
   }
 }

@@ -43,18 +43,42 @@ def gather_topk(idx: torch.Tensor, key: torch.Tensor, out_idx: torch.Tensor = No
     return out_idx, out_key
 
 
-def merge_topk(keys: torch.Tensor, pos: torch.Tensor, K: int) -> Tuple[torch.Tensor, torch.Tensor]:
-    """Merge G partial top-K lists of ONE request (rows of `keys` / `pos`, [G, K'], each sorted by
-    (key desc, position asc)) into its top-K, same order, NaN last. Used when one request's ads
-    are split across ranks."""
-    k = keys.reshape(-1).double()
-    p = pos.reshape(-1).long()
-    nan = torch.isnan(k)
-    # lexicographic (nan, -key, position): sort by position, then stable by key desc, then nan last
-    order = torch.argsort(p, stable=True)
-    k, p, nan = k[order], p[order], nan[order]
-    kk = torch.where(nan, torch.zeros_like(k), -k)
-    o2 = torch.argsort(kk, stable=True)
-    k, p, nan = k[o2], p[o2], nan[o2]
-    o3 = torch.argsort(nan.to(torch.int8), stable=True)
-    return k[o3][:K], p[o3][:K]
+def ad_slice(n: int, world: int, rank: int) -> range:
+    """F1 split rule (include/cold.h, cold_merge_topk): rank g of G owns ads
+    [floor(g n / G), floor((g + 1) n / G)) of a request with n ads."""
+    return range(rank * n // world, (rank + 1) * n // world)
+
+
+def slice_requests(ad_offsets, ids, offs, sides, world: int, rank: int):
+    """This rank's share of every request when each request's ads are split across `world` ranks
+    (P:248-250 / P:498 split one query's ads into parallel inference calls).
+    Columnar arrays in the cold_batch layout (numpy): USER groups keep their per-request bags,
+    AD groups keep the ids (single: ids[N]; bag: CSR offs[N+1] rebased) of the rank's ads,
+    CROSS groups carry nothing. `sides[g]` is 0 user / 1 ad / 2 cross.
+    Returns (ad_offsets, ids, offs, starts) with starts[r] = first ad of the slice in request r."""
+    import numpy as np
+    ao = np.asarray(ad_offsets, np.int64)
+    R = len(ao) - 1
+    sel, new_ao, starts = [], [0], []
+    for r in range(R):
+        sl = ad_slice(int(ao[r + 1] - ao[r]), world, rank)
+        sel.append(np.arange(ao[r] + sl.start, ao[r] + sl.stop))
+        new_ao.append(new_ao[-1] + len(sl))
+        starts.append(sl.start)
+    sel = np.concatenate(sel) if sel else np.zeros(0, np.int64)
+    out_ids, out_offs = [], []
+    for g, side in enumerate(sides):
+        if side != 1:
+            out_ids.append(ids[g])
+            out_offs.append(offs[g])
+        elif offs[g] is None:
+            out_ids.append(np.ascontiguousarray(np.asarray(ids[g])[sel], np.int32))
+            out_offs.append(None)
+        else:
+            o = np.asarray(offs[g], np.int64)
+            lens = o[sel + 1] - o[sel]
+            no = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+            idx = np.concatenate([np.arange(o[a], o[a + 1]) for a in sel]) if len(sel) else np.zeros(0, np.int64)
+            out_ids.append(np.ascontiguousarray(np.asarray(ids[g])[idx], np.int32))
+            out_offs.append(no)
+    return np.asarray(new_ao, np.int32), out_ids, out_offs, np.asarray(starts, np.int64)

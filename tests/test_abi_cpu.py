@@ -120,3 +120,19 @@ def test_sm100a_code_in_library():
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass and "UTMASTG" in sass
     elf = subprocess.run(["cuobjdump", "-lelf", cold.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in elf
+
+
+def test_select_groups_host_helper():
+    """cold_select_groups is host-only: top-K by mean SE weight, ties to the lower schema index,
+    ascending output, checked against the oracle's definition."""
+    import numpy as np
+
+    import oracle
+    _lib()
+    rng = np.random.default_rng(3)
+    for M in (1, 5, 32):
+        s = np.round(rng.uniform(0, 1, M), 1)          # rounding forces ties
+        for K in sorted({1, max(1, M // 2), M}):
+            assert cold.select_groups(s, K) == oracle.select_groups(s, K)
+    with pytest.raises(cold.ColdError):
+        cold.select_groups(np.zeros(4), 5)

@@ -304,3 +304,60 @@ def test_errors():
     with pytest.raises(ColdError) as e:
         Context(sch.groups, sch.k, (100, 2), precision="f16")
     assert e.value.name == "COLD_ERR_UNSUPPORTED"
+
+
+# ---- F3: SE importance statistics and feature-group selection --------------------
+
+@pytest.mark.parametrize("se", ["planted", "planted_noisy", "random"])
+def test_se_stats_and_selection_match_oracle(se):
+    """cold_se_stats (mean s_g of every group over the batch's ads) vs the oracle's fp64 gates, and
+    the top-K_g selection built on it (planted SE: the known schema-order ranking, P-11)."""
+    from paper_2007_16122_b200 import select_groups
+    sch = coldgen.scaled_schema(coldgen.schema_full(), 50000)
+    params = coldgen.make_params(sch, seed=81, precision="f16", se=se)
+    batch = coldgen.make_batch(sch, 3, [1000, 300, 77], seed=82)
+    ctx = make_ctx(sch, params)
+    got = ctx.se_stats(device_batch(batch))
+    want = oracle.se_gates(oracle.Model(sch, params), batch).mean(0)
+    np.testing.assert_allclose(got, want, rtol=1e-4, atol=1e-9)
+    for K in (8, 16, 24, 32):
+        sel = select_groups(got, K)
+        assert sel == oracle.select_groups(want, K)
+        if se != "random":
+            assert sel == list(range(K))
+
+
+# ---- F1: one request's ads split across G ranks, per-rank top-K merged (P:248-250) ------------
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_split_request_merge_topk_equals_unsplit(G):
+    """Rank g scores the slice [floor(g n/G), floor((g+1) n/G)) of every request and keeps its top-K;
+    cold_merge_topk over the rank-major [G][R][K] lists must equal cold_topk over the whole
+    request, also with heavy key ties (scores rounded to 3 decimals)."""
+    import torch
+    sch, params, batch = small_case("paper", R=3, n_ads=(2000, 1501, 4003), precision="f16", cap=20000, seed=91)
+    ctx = make_ctx(sch, params)
+    scores = gpu_scores(ctx, batch)
+    ao = np.asarray(batch.ad_offsets, np.int64)
+    R, K = batch.R, 100
+    for keys in (scores, np.round(scores, 3)):
+        full_idx, full_key = gpu_topk(ctx, keys, batch.ad_offsets, K)
+        cand_key = np.zeros((G, R, K), np.float32)
+        cand_idx = np.zeros((G, R, K), np.int32)
+        for g in range(G):
+            parts, offs = [], [0]
+            for r in range(R):
+                n = ao[r + 1] - ao[r]
+                s0, s1 = g * n // G, (g + 1) * n // G
+                parts.append(keys[ao[r] + s0:ao[r] + s1])
+                offs.append(offs[-1] + (s1 - s0))
+            li, lk = gpu_topk(ctx, np.concatenate(parts), np.asarray(offs, np.int32), K)
+            cand_idx[g], cand_key[g] = li, lk
+        out_idx = torch.empty(R * K, dtype=torch.int32, device="cuda")
+        out_key = torch.empty(R * K, dtype=torch.float32, device="cuda")
+        ctx.merge_topk(torch.from_numpy(cand_key).cuda(), torch.from_numpy(cand_idx).cuda(), G, K,
+                       torch.from_numpy(np.asarray(batch.ad_offsets, np.int32)).cuda(), batch.ad_offsets, K,
+                       out_idx, out_key)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(out_idx.cpu().numpy().reshape(R, K), full_idx)
+        np.testing.assert_array_equal(out_key.cpu().numpy().reshape(R, K), full_key)
