@@ -431,11 +431,15 @@ def main():
     dom = PROF_FC + 1 if 1 in covers else PROF_FC
     peak_tf = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
     achieved = per_kernel[names[dom]]["tflops"]
-    traffic = None
+    traffic, traffic_g = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("fc2_dram_bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("fc2_dram_bytes_per_launch")
+        if tj.get("gather_dram_bytes_per_ad") and prof_n[PROF_GATHER]:
+            # the capture's gather launch covered a different span: scale per ad to this run's launches
+            traffic_g = tj["gather_dram_bytes_per_ad"] * N * args.steps / float(prof_n[PROF_GATHER])
     roofline = {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": peak_tf,
                 "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
                 "peak_source": f"bf16_tflops_sustained {peak_src} (fp16 runs at the bf16 rate; kernel timed "
@@ -446,7 +450,10 @@ def main():
         hb = float(peaks["hbm_gbs"])
         ga = per_kernel["gather"]["gbs"]
         roofline_gather = {"bound": "hbm", "kernel": "gather", "achieved": ga, "peak": hb, "unit": "GB/s",
-                           "frac": ga / hb, "traffic": None,
+                           "frac": ga / hb, "traffic": traffic_g,
+                           "traffic_note": "ncu dram read+write bytes per ad (profiles/ncu_traffic.json) x ads per "
+                                           "launch: below the algorithmic bytes because L2 serves repeated rows of "
+                                           "the column-wise gather",
                            "algorithmic": f"{gb_per_ad:.0f} B/ad ({rows_per_ad:.0f} rows x {sch.k} x 2 B + ids "
                                           f"+ X_ac write)"}
     fc_total_ms = sum(prof_ms[PROF_FC + l] for l in covers)

@@ -177,6 +177,18 @@ cold_status cold_merge_topk(cold_ctx* ctx, const float* cand_key, const int32_t*
                             int32_t Kl, const int32_t* ad_offsets, const int32_t* ad_offsets_host, int32_t K,
                             int32_t* idx_out, float* key_out, void* stream);
 
+/* ---- the vector-product based pre-ranking model COLD is compared with (
+ * PAPER.md L160-166 §2.2: p = sigma(v_u^T v_a), Table tab:sys) -------------------------------
+ * Serving form: v_a precomputed per ad (ad tower), v_u per request (user tower). For every ad a of
+ * request r: scores[a] = sigma(user_vecs[r] . ad_vecs[ad_ids[a]]), fp32 accumulation in index order.
+ * ad_vecs: [num_vecs][d] of vec_dtype (COLD_FP32 / COLD_FP16 / COLD_BF16 bits), 32 B aligned;
+ * user_vecs: [R][d] fp32; ad_ids: [N_tot]; ad_offsets: [R+1] (device) + its host copy; scores:
+ * [N_tot] fp32. All device memory. d in {16, 32, 64, 128, 256}. Ids outside [0, num_vecs) are
+ * clamped. Stateless: no ctx. Top-K of the result: cold_topk. */
+cold_status cold_vps_score(const void* ad_vecs, int32_t vec_dtype, int64_t num_vecs, int32_t d, const float* user_vecs,
+                           const int32_t* ad_ids, const int32_t* ad_offsets, const int32_t* ad_offsets_host,
+                           int32_t R, float* scores, void* stream);
+
 cold_status cold_get_info(const cold_ctx* ctx, cold_info* out);
 
 /* ---- feature-group selection (§3.2 "Importance weight calculation" / "Feature group

@@ -87,6 +87,9 @@ def lib():
         L.orc_pooled_f32.argtypes = [C.POINTER(_Model), C.POINTER(_Batch), C.c_void_p, C.c_int64, C.c_void_p]
         L.orc_se_gates.restype = C.c_int32
         L.orc_se_gates.argtypes = [C.POINTER(_Model), C.POINTER(_Batch), C.c_void_p, C.c_int64, C.c_void_p]
+        L.orc_vps_score.restype = C.c_int32
+        L.orc_vps_score.argtypes = [C.c_int32, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p,
+                                    C.c_void_p, C.c_void_p]
         L.orc_topk.restype = C.c_int32
         L.orc_topk.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]
         _lib = L
@@ -219,6 +222,22 @@ def se_gates(model: Model, batch: coldgen.Batch, ad_list=None):
     if rc:
         raise OracleError(rc)
     return out
+
+
+def vps_score(ad_table, table_dtype: str, user_vecs, ad_offsets, ad_ids):
+    """Vector-product model: p[a] = sigma(user_vecs[r] . ad_table[ad_ids[a]]), fp64.
+    ad_table holds the stored values (float32, or uint16 bit patterns for 'f16' / 'bf16')."""
+    dt = {"f32": 0, "f16": 1, "bf16": 2}[table_dtype]
+    tab = np.ascontiguousarray(ad_table, np.float32 if dt == 0 else np.uint16)
+    u = np.ascontiguousarray(user_vecs, np.float64)
+    ao = np.ascontiguousarray(ad_offsets, np.int32)
+    ids = np.ascontiguousarray(ad_ids, np.int32)
+    p = np.empty(int(ao[-1]), np.float64)
+    rc = lib().orc_vps_score(int(tab.shape[1]), tab.ctypes.data, dt, int(tab.shape[0]), u.ctypes.data, len(ao) - 1,
+                             ao.ctypes.data, ids.ctypes.data, p.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return p
 
 
 def select_groups(mean_s, K: int):

@@ -386,6 +386,30 @@ static int kp_cmp(const void* pa, const void* pb) {
   return (a->pos > b->pos) - (a->pos < b->pos);  /* ties: ascending position */
 }
 
+/* Vector-product based pre-ranking model (§2.2): p = sigma(v_u^T v_a), v_u per request
+ * (user tower output), v_a per ad looked up by id in the precomputed ad-tower table (stored values,
+ * any storage dtype). fp64 dot product in index order. */
+int32_t orc_vps_score(int32_t d, const void* ad_table, int32_t table_dtype, int64_t card, const double* user_vecs,
+                      int32_t R, const int32_t* ad_offsets, const int32_t* ad_ids, double* p_out) {
+  if (d < 1 || !ad_table || !user_vecs || !ad_offsets || !ad_ids || !p_out || R < 1 || card < 1) return ORC_ERR_ARG;
+  orc_group G;
+  G.side = ORC_AD;
+  G.card = card;
+  G.user_ref = -1;
+  G.ad_ref = -1;
+  G.table_dtype = table_dtype;
+  G.table = ad_table;
+  for (int32_t r = 0; r < R; r++)
+    for (int64_t a = ad_offsets[r]; a < ad_offsets[r + 1]; a++) {
+      int64_t id = ad_ids[a];
+      if (id < 0 || id >= card) return ORC_ERR_ID_RANGE;
+      double z = 0.0;
+      for (int k = 0; k < d; k++) z += user_vecs[(size_t)r * d + k] * table_value(&G, id, k, d);
+      p_out[a] = orc_sigmoid(z);
+    }
+  return ORC_OK;
+}
+
 int32_t orc_topk(const double* key, int64_t n, int32_t K, int32_t* idx_out, double* key_out) {
   if (n < 1) return ORC_ERR_ARG;
   if (K < 1 || K > n) return ORC_ERR_K_RANGE;

@@ -97,6 +97,11 @@ int32_t orc_pooled_f32(const orc_model* m, const orc_batch* bt, const int64_t* a
 int32_t orc_se_gates(const orc_model* m, const orc_batch* bt, const int64_t* ad_list, int64_t n_list,
                      double* s_out);
 
+/* Vector-product based model: p[a] = sigma(user_vecs[r] . table[ad_ids[a]]) for every ad a of
+ * request r; table: [card][d] stored values of table_dtype (F4 baseline of SURVEY §8(f)). */
+int32_t orc_vps_score(int32_t d, const void* ad_table, int32_t table_dtype, int64_t card, const double* user_vecs,
+                      int32_t R, const int32_t* ad_offsets, const int32_t* ad_ids, double* p_out);
+
 /* Top-K of one request: stable order by (key desc, position asc), NaN last. */
 int32_t orc_topk(const double* key, int64_t n, int32_t K, int32_t* idx_out, double* key_out);
 

@@ -27,7 +27,7 @@ STATUS = {0: "COLD_OK", 1: "COLD_ERR_INVALID_ARG", 2: "COLD_ERR_SHAPE", 3: "COLD
 EXPORTS = ["cold_create", "cold_destroy", "cold_load_params", "cold_score_batch", "cold_score_request",
            "cold_topk", "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
            "cold_status_string", "cold_last_error", "cold_profile", "cold_profile_read", "cold_se_stats",
-           "cold_select_groups", "cold_merge_topk"]
+           "cold_select_groups", "cold_merge_topk", "cold_vps_score"]
 PROF_KINDS = 3 + 16
 PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC = 0, 1, 2, 3
 
@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
         L.cold_select_groups.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         L.cold_merge_topk.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                                       C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.cold_vps_score.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.cold_profile.argtypes = [C.c_void_p, C.c_int32]
         L.cold_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.cold_status_string.restype = C.c_char_p
@@ -106,7 +108,7 @@ def lib() -> C.CDLL:
         for f in ["cold_create", "cold_load_params", "cold_score_batch", "cold_score_request", "cold_topk",
                   "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
                   "cold_profile", "cold_profile_read", "cold_se_stats", "cold_select_groups",
-                  "cold_merge_topk"]:
+                  "cold_merge_topk", "cold_vps_score"]:
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -287,3 +289,12 @@ def select_groups(mean_s, K: int):
     out = np.empty(K, np.int32)
     _check(lib().cold_select_groups(m.ctypes.data, len(m), K, out.ctypes.data))
     return [int(x) for x in out]
+
+
+def vps_score(ad_vecs, vec_dtype: str, user_vecs, ad_ids, ad_offsets, ad_offsets_host, scores, stream=None):
+    """Vector-product baseline (F4): scores = sigma(v_u[request] . v_a[id]) (cold_vps_score)."""
+    aoh = np.ascontiguousarray(ad_offsets_host, np.int32)
+    d = int(user_vecs.shape[-1])
+    _check(lib().cold_vps_score(_addr(ad_vecs), PRECISION[vec_dtype], int(ad_vecs.shape[0]), d, _addr(user_vecs),
+                                _addr(ad_ids), _addr(ad_offsets), aoh.ctypes.data, len(aoh) - 1, _addr(scores),
+                                _stream_handle(stream)))

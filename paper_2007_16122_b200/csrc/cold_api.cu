@@ -90,6 +90,12 @@ struct cold_ctx {
   void* d_H[COLD_MAX_LAYERS] = {nullptr};
   CUtensorMap tmA[COLD_MAX_LAYERS];
   std::vector<CUtensorMap> tmAX;     // layer-0 A maps, one per chunk slot of the gather span
+  bool u1mma = false;                // FC1 adds u1[request(row)] on the tensor core (kernels_gemm2.cu)
+  int u1_terms = 0, u1t_ld = 0;
+  uint16_t* d_u1t = nullptr;         // [u1_terms * H][u1t_ld] 16-bit terms of u1 (written by user_kernel)
+  uint16_t* d_ohot = nullptr;        // [gspan * chunk][16] one-hot u1 operand rows (written by gather)
+  CUtensorMap tmU1T;
+  std::vector<CUtensorMap> tmOH;     // per chunk slot of the span
   int gspan = 1;                     // chunks per column-wise gather pass (X_ac holds gspan * chunk rows)
   CUtensorMap tmC[COLD_MAX_LAYERS];  // epilogue TMA-store maps (32 x 32 boxes)
   int cs[COLD_MAX_LAYERS] = {0};     // cluster size (weight-tile multicast) per GEMM layer
@@ -245,6 +251,22 @@ static cold_status make_tmap(CUtensorMap* tm, void* ptr, int precision, uint64_t
                    box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return COLD_OK;
+}
+
+// 2-D 16-bit tensor, no swizzle: box rows of box_cols * 2 bytes land contiguously (the FC1 u1 operand)
+static cold_status make_tmap_plain(CUtensorMap* tm, void* ptr, int precision, uint64_t inner, uint64_t rows,
+                                   uint32_t box_rows, uint32_t box_cols) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(tm, precision == COLD_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   2, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled (plain) failed: " + std::to_string((int)r));
   return COLD_OK;
 }
 
@@ -429,6 +451,27 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       c->pair[l] = !in_tail && l < Lg - 1 && c->bn[l] == 256 &&
                    (pair_mode == 2 || (pair_mode == 1 && !c->resb[l]));
       if (c->pair[l]) { c->resb[l] = false; c->cs[l] = 1; }
+    }
+  }
+  if (c->tensor && c->pair[0] && c->n_tail < c->L - 1) {
+    const char* env_u1 = getenv("COLD_U1MMA");
+    c->u1mma = !(env_u1 && atoi(env_u1) == 0);
+  }
+  if (c->u1mma) {
+    c->u1_terms = c->precision == COLD_BF16 ? 3 : 2;
+    c->u1t_ld = (c->max_req + 7) / 8 * 8;
+    const size_t u1t_bytes = (size_t)c->u1_terms * W0 * c->u1t_ld * 2;
+    const size_t oh_bytes = (size_t)c->gspan * c->chunk * 16 * 2;
+    cudaError_t e2 = c->alloc((void**)&c->d_u1t, u1t_bytes);
+    if (e2 == cudaSuccess) e2 = c->alloc((void**)&c->d_ohot, oh_bytes);
+    if (e2 != cudaSuccess) { delete c; cudaGetLastError(); return fail(COLD_ERR_OOM, "u1 operand buffers"); }
+    cudaMemset(c->d_u1t, 0, u1t_bytes);   // slots past the last request stay finite (0 x value = 0)
+    cold_status s = make_tmap_plain(&c->tmU1T, c->d_u1t, c->precision, c->u1t_ld, (uint64_t)c->u1_terms * W0, 128, 8);
+    if (s) { delete c; return s; }
+    c->tmOH.resize(c->gspan);
+    for (int j = 0; j < c->gspan; j++) {
+      s = make_tmap_plain(&c->tmOH[j], c->d_ohot + (size_t)j * c->chunk * 16, c->precision, 16, c->chunk, 128, 8);
+      if (s) { delete c; return s; }
     }
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -790,6 +833,10 @@ static UserArgs make_user_args(cold_ctx* c, const CallPlan& pl, const int32_t* d
   ua.dbg_feat = dbg.feat;
   ua.n_sel = (int)c->sel.size();
   ua.d_in = c->d_in;
+  ua.u1t = c->u1mma ? c->d_u1t : nullptr;
+  ua.u1t_ld = c->u1t_ld;
+  ua.u1_terms = c->u1_terms;
+  ua.bf16 = c->precision == COLD_BF16 ? 1 : 0;
   return ua;
 }
 
@@ -815,6 +862,10 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
   ga.dbg_feat = dbg.feat;
   ga.n_sel = (int)c->sel.size();
   ga.d_in = c->d_in;
+  ga.ohot = (c->u1mma && !dbg.pooled && !dbg.feat) ? c->d_ohot : nullptr;
+  ga.chunk = c->chunk;
+  ga.nslot = U1_NSLOT;
+  ga.bf16 = c->precision == COLD_BF16 ? 1 : 0;
   return ga;
 }
 
@@ -885,7 +936,8 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     c->mark_begin(st);
     if (c->pair[l])
       launch_gemm_pair(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
-                       c->precision == COLD_BF16 ? 1 : 0, ep, c->num_sms, c->pdl && !c->prof, st);
+                       c->precision == COLD_BF16 ? 1 : 0, ep, c->num_sms, c->pdl && !c->prof, st,
+                       (l == 0 && c->u1mma) ? &c->tmOH[xslot] : nullptr, (l == 0 && c->u1mma) ? &c->tmU1T : nullptr);
     else
       launch_gemm(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
                   c->precision == COLD_BF16 ? 1 : 0, c->cs[l], c->resb[l], ep, c->num_sms, c->pdl && !c->prof, st);
@@ -1109,6 +1161,7 @@ extern "C" cold_status cold_se_stats(cold_ctx* c, const cold_batch* b, double* m
     }
   for (int j = 0; j < ga.n_ac; j++) ga.order[j] = j;
   ga.X = nullptr;
+  ga.ohot = nullptr;
   ga.stats = d_stats;
   launch_gather(ga, c->precision, st);
   CK(cudaGetLastError());
@@ -1251,6 +1304,40 @@ extern "C" cold_status cold_merge_topk(cold_ctx* c, const float* cand_key, const
   launch_topk(ta, st);
   c->mark_end(COLD_PROF_TOPK, st);
   CK(cudaGetLastError());
+  return COLD_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// F4: the vector-product based pre-ranking model, precomputed towers
+extern "C" cold_status cold_vps_score(const void* ad_vecs, int32_t vec_dtype, int64_t num_vecs, int32_t d,
+                                      const float* user_vecs, const int32_t* ad_ids, const int32_t* ad_offsets,
+                                      const int32_t* ad_offsets_host, int32_t R, float* scores, void* stream) {
+  if (!ad_vecs || !user_vecs || !ad_ids || !ad_offsets || !ad_offsets_host || !scores)
+    return fail(COLD_ERR_INVALID_ARG, "null pointer");
+  if (vec_dtype < COLD_FP32 || vec_dtype > COLD_BF16) return fail(COLD_ERR_INVALID_ARG, "bad vec_dtype");
+  if (d != 16 && d != 32 && d != 64 && d != 128 && d != 256) return fail(COLD_ERR_UNSUPPORTED, "d must be 16..256, pow2");
+  if (num_vecs < 1 || R < 1) return fail(COLD_ERR_INVALID_ARG, "num_vecs and R must be >= 1");
+  if (ad_offsets_host[0] != 0) return fail(COLD_ERR_INVALID_ARG, "ad_offsets[0] must be 0");
+  int max_n = 0;
+  for (int r = 0; r < R; r++) {
+    const int n = ad_offsets_host[r + 1] - ad_offsets_host[r];
+    if (n < 1) return fail(COLD_ERR_INVALID_ARG, "every request needs >= 1 ad");
+    max_n = std::max(max_n, n);
+  }
+  for (const void* p : {ad_vecs, (const void*)user_vecs, (const void*)ad_ids, (const void*)ad_offsets, (const void*)scores})
+    if (!is_device_ptr(p)) return fail(COLD_ERR_INVALID_ARG, "cold_vps_score takes device buffers");
+  if ((reinterpret_cast<uintptr_t>(ad_vecs) & 31) != 0) return fail(COLD_ERR_INVALID_ARG, "ad_vecs must be 32 B aligned");
+  VpsArgs a;
+  a.ad_vecs = ad_vecs;
+  a.num_vecs = num_vecs;
+  a.d = d;
+  a.user_vecs = user_vecs;
+  a.ad_ids = ad_ids;
+  a.ad_offsets = ad_offsets;
+  a.R = R;
+  a.scores = scores;
+  cudaGetLastError();
+  CK(launch_vps(a, vec_dtype, max_n, (cudaStream_t)stream));
   return COLD_OK;
 }
 

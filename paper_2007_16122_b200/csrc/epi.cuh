@@ -18,8 +18,15 @@ template <bool BF16>
 __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int c_end, const float* __restrict__ bias,
                                                uint32_t u1s, const float* __restrict__ u1g, int relu, uint8_t* buf,
                                                const CUtensorMap* tmC, int col_base, int row0, int lane,
-                                               int dbg = 0) {
+                                               int dbg = 0, unsigned long long* tacc = nullptr) {
   const uint32_t sbuf = smem_u32(buf);
+  // debug timing (tacc != null, lane 0): cycles in [0] TMEM load+wait, [1] math+pack, [2] wait for the
+  // staging buffer, [3] smem writes + fence, [4] store issue
+  long long tc0 = 0, tsum[5] = {0, 0, 0, 0, 0};
+  auto tick = [&](int k) {
+    if (tacc) { const long long t = clock64(); if (k >= 0) tsum[k] += t - tc0; tc0 = t; }
+  };
+  tick(-1);
   for (int c = c_begin; c < c_end; c += EPI_WIDE_COLS) {
     uint32_t v[64];
     if (dbg != 5) {
@@ -30,6 +37,7 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
 #pragma unroll
       for (int i = 0; i < 64; i++) v[i] = (uint32_t)(lane + i);
     }
+    tick(0);
     const int col0 = col_base + c;
     float f[64];
 #pragma unroll
@@ -54,13 +62,14 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
         f[i] += b.x; f[i + 1] += b.y; f[i + 2] += b.z; f[i + 3] += b.w;
       }
     }
+    uint32_t pk[32];
     if (relu) {
 #pragma unroll
-      for (int i = 0; i < 64; i++) f[i] = fmaxf(f[i], 0.0f);
-    }
-    uint32_t pk[32];
+      for (int i = 0; i < 32; i++) pk[i] = Pack<BF16>::two_relu(f[2 * i], f[2 * i + 1]);
+    } else {
 #pragma unroll
-    for (int i = 0; i < 32; i++) pk[i] = Pack<BF16>::two(f[2 * i], f[2 * i + 1]);
+      for (int i = 0; i < 32; i++) pk[i] = Pack<BF16>::two(f[2 * i], f[2 * i + 1]);
+    }
     if (dbg == 3) {                       // timing experiment: no smem staging / store
       uint32_t t = 0;
 #pragma unroll
@@ -68,19 +77,25 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
       if (t == 0x12345678u) asm volatile("st.global.u32 [%0], %1;" ::"l"(bias), "r"(t));
       continue;
     }
+    tick(1);
     if (lane == 0) bulk_wait_read<0>();   // the previous box of this warp has left shared memory
     __syncwarp();
+    tick(2);
     const uint32_t rowp = sbuf + (uint32_t)lane * 128u;
 #pragma unroll
     for (int j = 0; j < 8; j++)
       sts128(rowp + (uint32_t)((j ^ (lane & 7)) << 4), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
     fence_async_smem();
     __syncwarp();
+    tick(3);
     if (lane == 0 && dbg != 4) {
       tma_store_2d(tmC, buf, col0, row0);
       bulk_commit();
     }
+    tick(4);
   }
+  if (tacc && lane == 0)
+    for (int k = 0; k < 5; k++) atomicAdd(tacc + k, (unsigned long long)tsum[k]);
 }
 
 }  // namespace cold

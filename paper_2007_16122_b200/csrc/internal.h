@@ -29,6 +29,9 @@ struct UserArgs {
   int n_sel, d_in;
   double* stats;                   // SE statistics mode (cold_se_stats): [M] += s_g * ads of the request;
                                    // x_u / u1 are not written
+  uint16_t* u1t;                   // FC1 u1 operand (nullable): [u1_terms * H][u1t_ld] f16/bf16 bits, the
+                                   // 2 (f16) or 3 (bf16) RNE terms of u1[r][o] at [t * H + o][r]
+  int u1t_ld, u1_terms, bf16;
 };
 
 struct GatherArgs {
@@ -52,6 +55,11 @@ struct GatherArgs {
   float* dbg_feat;                 // [N][D_in]
   int n_sel, d_in;
   double* stats;                   // SE statistics mode: [M] += s_g per ad; X is not written
+  uint16_t* ohot;                  // FC1 u1 operand (nullable): [n][16] span-local rows, the one-hot slot of
+                                   // the row's request in its 256-row CTA-pair tile, repeated in k 0-7 / 8-15
+  int chunk;                       // rows per FC chunk (pair tiles are 256-row aligned inside a chunk)
+  int nslot;                       // max requests per pair tile folded into the MMA (else all-zero rows)
+  int bf16;
 };
 
 struct RowsArgs {
@@ -105,8 +113,13 @@ cudaError_t launch_gemm(const CUtensorMap* tmA, const CUtensorMap* tmB, const CU
                         cudaStream_t s);
 bool gemm_resident_ok(int bn, int K);
 // CTA-pair (cta_group::2) variant: 256-row tiles, each CTA stages half of the weight tile
+// FC1 (ep.u1 set): tmOH = one-hot rows of the chunk ([rows][16], box 8 x 128), tmU1T = u1 terms
+// ([terms * H][R_pad], box 8 requests x 128 columns); the kernel adds u1[request(row)] with one (f16) or
+// two (bf16) extra K = 16 MMAs per tile (kernels_gemm2.cu)
+constexpr int U1_NSLOT = 8;
 cudaError_t launch_gemm_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N,
-                             int K, int bn, int bf16, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s);
+                             int K, int bn, int bf16, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s,
+                             const CUtensorMap* tmOH = nullptr, const CUtensorMap* tmU1T = nullptr);
 
 // fused FC(L-4) .. FC(L-2) + head (paper widths 256, 128, 64 -> 2)
 struct TailParams {
@@ -123,6 +136,17 @@ cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const 
 bool tail45_supported(int n4, int n5, int k4);
 cudaError_t launch_tail45(const CUtensorMap* tmA4, const CUtensorMap* tmB4, const CUtensorMap* tmB5, int M, int bf16,
                           const TailParams& tp, int num_sms, bool pdl, cudaStream_t s);
+
+// vector-product baseline (F4): scores[ad] = sigma(user_vecs[request] . ad_vecs[ad_ids[ad]])
+struct VpsArgs {
+  const void* ad_vecs; int64_t num_vecs; int d;
+  const float* user_vecs;          // [R][d] fp32
+  const int32_t* ad_ids;           // [N]
+  const int32_t* ad_offsets;       // [R+1]
+  int R;
+  float* scores;                   // [N]
+};
+cudaError_t launch_vps(const VpsArgs& a, int precision, int max_n, cudaStream_t s);
 
 // top-K per request
 struct TopkArgs {

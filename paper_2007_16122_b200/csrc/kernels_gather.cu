@@ -110,6 +110,22 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
     float acc = a.b1[o];
     for (int i = 0; i < d_u; i++) acc = fmaf(a.w1u_t[(int64_t)i * a.H + o], xs[i], acc);
     a.u1[(int64_t)r * a.H + o] = acc;
+    if (a.u1t) {   // u1 = term_0 + term_1 (+ term_2), each RNE in 16 bits: the FC1 tensor-core operand
+      float u = acc;
+      for (int t = 0; t < a.u1_terms; t++) {
+        uint16_t bits;
+        if (a.bf16) {
+          const __nv_bfloat16 q = __float2bfloat16_rn(u);
+          bits = __bfloat16_as_ushort(q);
+          u -= __bfloat162float(q);
+        } else {
+          const __half q = __float2half_rn(u);
+          bits = __half_as_ushort(q);
+          u -= __half2float(q);
+        }
+        a.u1t[((int64_t)t * a.H + o) * a.u1t_ld + r] = bits;
+      }
+    }
   }
   for (int64_t ad = a.ad_offsets[r] + threadIdx.x; ad < a.ad_offsets[r + 1]; ad += blockDim.x)
     a.req_of_ad[ad] = r;
@@ -196,8 +212,38 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
   }
 }
 
+// FC1 u1 operand rows: for span-local row i, slot = request(i) - base, base = the first request of its
+// 256-row CTA-pair tile rounded down to a multiple of 8 (tiles are 256-aligned inside each FC chunk);
+// 1.0 at k = slot and k = 8 + slot; all zero when the tile's requests do not fit in [base, base + 8)
+// (the FC1 epilogue then adds u1 itself).
+__device__ __forceinline__ void write_ohot(const GatherArgs& a, int64_t i, uint16_t one) {
+  const int64_t j = i / a.chunk, q = i - j * a.chunk;
+  const int64_t c_end = min((j + 1) * (int64_t)a.chunk, a.n);
+  const int64_t t0 = j * a.chunk + (q & ~(int64_t)255);
+  const int64_t t1 = min(t0 + 256, c_end) - 1;
+  const int r0 = a.req_of_ad[a.a0 + t0] & ~7;   // 8-aligned: the u1-term TMA box starts 16 B aligned
+  const int slot = a.req_of_ad[a.a0 + i] - r0;
+  const bool ok = a.req_of_ad[a.a0 + t1] - r0 < a.nslot;
+  uint32_t w[8];
+#pragma unroll
+  for (int c = 0; c < 8; c++) {
+    const int k0 = (2 * c) & 7, k1 = (2 * c + 1) & 7;
+    w[c] = (ok && k0 == slot ? one : 0u) | ((ok && k1 == slot ? (uint32_t)one : 0u) << 16);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(a.ohot + i * 16);
+  dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
 template <typename T, int K, bool FAST, int MINB = 4>
 __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
+  if ((int)blockIdx.y == a.n_ac) {          // the extra column: FC1's one-hot u1 operand rows
+    for (int i = 0; i < GATHER_APT; i++) {
+      const int64_t l = (int64_t)blockIdx.x * (128 * GATHER_APT) + threadIdx.x + i * 128;
+      if (l < a.n) write_ohot(a, l, a.bf16 ? 0x3F80u : 0x3C00u);
+    }
+    return;
+  }
   constexpr bool VEC = (K * (int)sizeof(T)) % 16 == 0;
   constexpr int NV = K * (int)sizeof(T) / 16;
   // bag rows in flight per thread (<= 16 vectors of raw registers; halved when the register budget
@@ -409,7 +455,7 @@ void launch_user(const UserArgs& a, int R, int precision, cudaStream_t s) {
 
 template <typename T, bool FAST>
 static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
-  dim3 grid((unsigned)((a.n + 128 * GATHER_APT - 1) / (128 * GATHER_APT)), (unsigned)a.n_ac);
+  dim3 grid((unsigned)((a.n + 128 * GATHER_APT - 1) / (128 * GATHER_APT)), (unsigned)(a.n_ac + (a.ohot ? 1 : 0)));
   switch (a.k) {
     case 2: gather_kernel<T, 2, FAST><<<grid, 128, 0, s>>>(a); break;
     case 4: gather_kernel<T, 4, FAST><<<grid, 128, 0, s>>>(a); break;
@@ -425,7 +471,7 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
 }
 
 void launch_gather(const GatherArgs& a, int precision, cudaStream_t s) {
-  if (a.n <= 0 || a.n_ac <= 0) return;
+  if (a.n <= 0 || (a.n_ac <= 0 && !a.ohot)) return;
   if (precision == 0) gather_dispatch<float, false>(a, s);
   else if (precision == 1) gather_dispatch<__half, true>(a, s);
   else gather_dispatch<__nv_bfloat16, true>(a, s);

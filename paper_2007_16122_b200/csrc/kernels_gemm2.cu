@@ -13,6 +13,19 @@
 // Roles per CTA: warp 0 = TMA producer (both CTAs; completion bytes land on the leader's "full"
 // barrier), warp 1 = TMEM allocator (both, cta_group::2) + MMA issuer (leader only), warps 2..9 =
 // epilogue (both CTAs, their own 128 rows; they release the accumulator on the leader's "tempty").
+//
+// FC1 (U1): the per-request user block u1[request(row)] (fp32, hoisted, DESIGN A2) is added by the
+// tensor core instead of the epilogue, as one extra K = 16 operand pair per tile:
+//   A_x[row][k] = 1 if k % 8 is the slot of row's request in the 256-row pair tile, else 0
+//   B_x[n][8 t + s] = t-th 16-bit term of u1[r_first + s][n]   (u1 = sum_t term_t to ~2^-22)
+// with s = request - base, base = the pair tile's first request rounded down to 8 (TMA boxes must start
+// 16 B aligned). D += A_x B_x^T = u1[request(row)][n]. A_x rows are written by the gather kernel (one-hot "column"),
+// the terms by the user kernel ([t * H + n][r] layout, so 8 consecutive requests of one column are
+// 16 contiguous bytes); both arrive by TMA like the other operands (box 8 x 128, no swizzle, K-major
+// core matrices of 8 rows x 16 B: SBO = 128 B, LBO = 2 KB). f16 uses 2 terms (one MMA), bf16 3 terms
+// (two MMAs, the 4th K chunk zero). The epilogue is then ReLU -> pack -> store only (the u1 loads and
+// adds had made it the FC1 bottleneck). A pair tile whose requests do not fit in [base, base + 8) has
+// all-zero A_x rows and its epilogue adds u1 from global memory instead.
 #include <cuda.h>
 #include "internal.h"
 #include "ptx.cuh"
@@ -30,13 +43,30 @@ template <int BN, bool U1> struct PairCfg {
   static constexpr int A_BYTES = BM * BK * 2;                 // own 128 rows
   static constexpr int B_BYTES = (BN / 2) * BK * 2;           // own half of the weight tile
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int OUT_BYTES = P_EPI_WARPS * 2 * P_OUT_BOX;
-  static constexpr int U1_BYTES = U1 ? 2 * 2 * BN * 4 : 0;
-  static constexpr int STAGES_FIT = (232448 - OUT_BYTES - U1_BYTES - 1024 - 512) / STAGE_BYTES;
+  static constexpr int OUT_BYTES = P_EPI_WARPS * 2 * P_OUT_BOX;   // = P_EPI_WARPS * EPI_WIDE_BOX
+  static constexpr int UXA_BYTES = BM * 32;                   // A_x: 128 rows x 16 halves (2 K chunks)
+  static constexpr int UXB_BYTES = (BN / 2) * 16 * 4;         // B_x: own BN/2 columns x 4 K chunks of 8
+  static constexpr int UX_BUF = UXA_BYTES + UXB_BYTES;
+  static constexpr int NUX = 2;
+  static constexpr int UX_BYTES = U1 ? NUX * UX_BUF : 0;
+  static constexpr int STAGES_FIT = (232448 - OUT_BYTES - UX_BYTES - 1024 - 512) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_BYTES + U1_BYTES + 1024 + 512;
+  static constexpr int THREADS = P_THREADS;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_BYTES + UX_BYTES + 1024 + 512;
 };
+
+// SMEM descriptor, K-major, no swizzle (the u1 operand): core matrices of 8 rows x 16 B; rows are
+// 16 B apart (one TMA box of 8 x 128), 8-row groups 128 B apart (SBO), K chunks 2 KB apart (LBO).
+// (probe: tools/probes/umma_k16_probe.cu checks the LBO / SBO roles.)
+__device__ __forceinline__ uint64_t sdesc_k16_plain(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(2048 >> 4) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;                                    // layout type 0 = SWIZZLE_NONE
+}
 
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                  uint64_t policy) {
@@ -80,25 +110,25 @@ __device__ __forceinline__ constexpr uint32_t idesc_pair() {
 }
 
 template <int BN, bool BF16, bool U1>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ CUtensorMap tmC, int M, int N, int K, EpiParams ep) {
+                     const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmOH,
+                     const __grid_constant__ CUtensorMap tmU1T, int M, int N, int K, EpiParams ep) {
   using Cfg = PairCfg<BN, U1>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
   uint8_t* sOut = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
-  float* sU1 = reinterpret_cast<float*>(sOut + Cfg::OUT_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + Cfg::OUT_BYTES + Cfg::U1_BYTES);
+  uint8_t* sUX = sOut + Cfg::OUT_BYTES;                        // [NUX][A_x | B_x]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sUX + Cfg::UX_BYTES);
   uint64_t* full = bars;                          // leader: A+B bytes of both CTAs
   uint64_t* empty = bars + Cfg::STAGES;           // both: released by the leader's pair commit
   uint64_t* tfull = bars + 2 * Cfg::STAGES;       // both: accumulator ready
   uint64_t* tempty = tfull + 2;                   // leader: both CTAs' epilogues drained
-  uint64_t* u1full = tempty + 2;                  // local: u1 rows staged
-  uint64_t* u1empty = u1full + 2;                 // local: this CTA's epilogue is done with u1 buffer
-  int32_t* u1hdr = reinterpret_cast<int32_t*>(u1empty + 2);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(u1hdr + 2);
+  uint64_t* uxfull = tempty + 2;                  // leader: both CTAs' u1 operand bytes landed [NUX]
+  uint64_t* uxempty = uxfull + Cfg::NUX;          // both: the u1 MMA of the buffer's last tile completed [NUX]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uxempty + Cfg::NUX);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -111,11 +141,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; s++) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * P_EPI_WARPS); }
-    for (int s = 0; s < 2; s++) { mbar_init(&u1full[s], 1); mbar_init(&u1empty[s], P_EPI_WARPS); }
+    for (int s = 0; s < Cfg::NUX; s++) { mbar_init(&uxfull[s], 1); mbar_init(&uxempty[s], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
     if (ep.out) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmC) : "memory");
+    if (U1) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmOH) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmU1T) : "memory");
+    }
+  }
+  if (U1 && BF16 && warp == 2) {   // bf16: the 4th K chunk of every B_x buffer stays zero
+    for (int b = 0; b < Cfg::NUX; b++)
+      for (int i = lane; i < (BN / 2); i += 32)
+        sts128(smem_u32(sUX + b * Cfg::UX_BUF + Cfg::UXA_BYTES + 3 * (BN / 2) * 16 + i * 16), make_uint4(0, 0, 0, 0));
+    fence_async_smem();
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -138,9 +178,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       int lt = 0;
+      constexpr int TERMS = BF16 ? 3 : 2;
+      // the pair tile's first request rounded down to 8 (16 B-aligned TMA box start), prefetched
+      int r_next = (U1 && pair < items) ? (ep.req_of_ad[ep.a0 + (pair / num_n) * 2 * BM] & ~7) : 0;
       for (int it = pair; it < items; it += npairs, lt++) {
         const int pm = it / num_n, nb = it % num_n;
         const int mrow = pm * 2 * BM + (int)rank * BM;
+        const int r_first = r_next;
+        if (U1 && it + npairs < items) r_next = ep.req_of_ad[ep.a0 + ((it + npairs) / num_n) * 2 * BM] & ~7;
         for (int kb = 0; kb < kb_count; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           if (leader) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
@@ -148,23 +193,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           tma_load_2d_pair(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, nb * BN + (int)rank * (BN / 2), pol_b);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
-        if (U1) {
-          // FC1: stage this CTA's u1 row slice(s) [nb*BN, +BN); <= 2 requests per 128 rows, else global
-          const int acc = lt & 1;
-          mbar_wait(&u1empty[acc], ((lt >> 1) & 1) ^ 1);   // this CTA's epilogue finished tile lt-2
-          const int rlo = mrow, rhi = min(M, rlo + BM) - 1;
-          const int r0 = rlo < M ? ep.req_of_ad[ep.a0 + rlo] : 0;
-          const int r1 = rlo < M ? ep.req_of_ad[ep.a0 + rhi] : 0;
-          float* dst = sU1 + acc * 2 * BN;
-          if (rlo < M && r1 - r0 <= 1) {
-            u1hdr[acc] = (r1 != r0) ? (int)(ep.ad_offsets[r1] - ep.a0 - rlo) : BM;
-            mbar_expect_tx(&u1full[acc], (uint32_t)(BN * 4 * (1 + (r1 != r0))));
-            bulk_load(dst, ep.u1 + (int64_t)r0 * ep.ld_u1 + nb * BN, BN * 4, &u1full[acc]);
-            if (r1 != r0) bulk_load(dst + BN, ep.u1 + (int64_t)r1 * ep.ld_u1 + nb * BN, BN * 4, &u1full[acc]);
-          } else {
-            u1hdr[acc] = -1;
-            mbar_arrive(&u1full[acc]);
-          }
+        if (U1) {   // the tile's u1 operand: A_x one-hot rows (2 boxes) + B_x term columns (TERMS boxes)
+          const int b = lt % Cfg::NUX;
+          mbar_wait(&uxempty[b], ((lt / Cfg::NUX) & 1) ^ 1);
+          uint8_t* ux = sUX + b * Cfg::UX_BUF;
+          if (leader) mbar_expect_tx(&uxfull[b], 2 * (Cfg::UXA_BYTES + TERMS * (BN / 2) * 16));
+          tma_load_2d_pair(ux, &tmOH, &uxfull[b], 0, mrow, pol_a);
+          tma_load_2d_pair(ux + BM * 16, &tmOH, &uxfull[b], 8, mrow, pol_a);
+          const int n0 = nb * BN + (int)rank * (BN / 2);
+#pragma unroll
+          for (int t = 0; t < TERMS; t++)
+            tma_load_2d_pair(ux + Cfg::UXA_BYTES + t * (BN / 2) * 16, &tmU1T, &uxfull[b], r_first, t * N + n0, pol_b);
         }
       }
     }
@@ -193,10 +232,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
           umma_commit_pair(&empty[s]);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
+        if (U1) {   // D += A_x B_x^T: the tile's u1[request(row)] block (K = 16 per term pair)
+          const int b = lt % Cfg::NUX;
+          mbar_wait(&uxfull[b], (lt / Cfg::NUX) & 1);
+          tc_fence_after();
+          const uint32_t ux = smem_u32(sUX + b * Cfg::UX_BUF);
+          const uint64_t ad = sdesc_k16_plain(ux);
+          umma_f16_pair(d, ad, sdesc_k16_plain(ux + Cfg::UXA_BYTES), idesc, 1u);                  // terms 0, 1
+          if (BF16) umma_f16_pair(d, ad, sdesc_k16_plain(ux + Cfg::UXA_BYTES + 2 * (BN / 2) * 16), idesc, 1u);  // 2, 0
+          umma_commit_pair(&uxempty[b]);
+        }
         umma_commit_pair(&tfull[acc]);
       }
     }
-  } else {
+  } else if (warp >= 2 && warp < 2 + P_EPI_WARPS) {
     // ===== epilogue warps 2..9 (both CTAs): TMEM lane quadrant q, column half h =====
     const int ew = warp - 2;
     const int q = warp & 3;
@@ -216,17 +265,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       const int row0 = pm * 2 * BM + (int)rank * BM + q * 32;
       const int row = row0 + lane;
       const bool valid = row < M;
-      uint32_t u1s = 0;                 // staged u1 row in shared memory (column nb*BN)
-      const float* u1row = nullptr;
+      const uint32_t u1s = 0;
+      const float* u1row = nullptr;     // fallback: u1 added here when the tile had too many requests
       if (ep.u1) {
-        int bnd = -1;
-        if (U1) {
-          mbar_wait(&u1full[acc], (lt >> 1) & 1);
-          bnd = u1hdr[acc];
+        bool add_here = !U1;
+        if (U1) {   // same rule as the gather's one-hot rows: more than U1_NSLOT requests in the pair tile
+          const int t0 = pm * 2 * BM;
+          add_here = ep.req_of_ad[ep.a0 + min(t0 + 2 * BM, M) - 1] - (ep.req_of_ad[ep.a0 + t0] & ~7) >= U1_NSLOT;
         }
-        if (bnd >= 0) {
-          u1s = smem_u32(sU1 + acc * 2 * BN + ((q * 32 + lane) < bnd ? 0 : BN));
-        } else {
+        if (add_here) {
           const int req = valid ? ep.req_of_ad[ep.a0 + row] : 0;
           u1row = ep.u1 + (int64_t)req * ep.ld_u1 + nb * BN;
         }
@@ -235,13 +282,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
         const int c_stop = ep.dbg_mode == 1 ? c_begin : c_end;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
         epi_store_wide<BF16>(tbase, c_begin, c_stop, ep.bias, u1s, u1row, ep.relu,
-                             sOut + ew * EPI_WIDE_BOX, &tmC, nb * BN, row0, lane, ep.dbg_mode);
+                             sOut + ew * EPI_WIDE_BOX, &tmC, nb * BN, row0, lane, ep.dbg_mode, ep.instr);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) {
-          mbar_arrive_remote(&tempty[acc], 0);
-          if (U1) mbar_arrive(&u1empty[acc]);
-        }
+        if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
         continue;
       }
       float z0 = 0.0f, z1 = 0.0f;
@@ -317,10 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_remote(&tempty[acc], 0);
-        if (U1) mbar_arrive(&u1empty[acc]);
-      }
+      if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
       if (head && h == 0 && valid) {
         float z;
         if (ep.head_n == 2) z = (z1 + ep.head_b[1]) - (z0 + ep.head_b[0]);
@@ -340,8 +381,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P_THREADS, 1)
 }
 
 template <int BN, bool BF16, bool U1>
-static cudaError_t launch_pair_t(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M,
-                                 int N, int K, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s) {
+static cudaError_t launch_pair_t(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC,
+                                 const CUtensorMap* tmOH, const CUtensorMap* tmU1T, int M, int N, int K,
+                                 const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s) {
   using Cfg = PairCfg<BN, U1>;
   auto kern = gemm_pair_kernel<BN, BF16, U1>;
   static bool attr = false;
@@ -353,7 +395,7 @@ static cudaError_t launch_pair_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   const int pairs = items < num_sms / 2 ? items : num_sms / 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
-  cfg.blockDim = dim3(P_THREADS);
+  cfg.blockDim = dim3(Cfg::THREADS);
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];
@@ -361,19 +403,22 @@ static cudaError_t launch_pair_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, *tmC, M, N, K, ep);
+  // tmOH / tmU1T are only read by the U1 variant; the others get tmA as a placeholder
+  return cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, *tmC, U1 ? *tmOH : *tmA, U1 ? *tmU1T : *tmA, M, N, K, ep);
 }
 
 cudaError_t launch_gemm_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N,
-                             int K, int bn, int bf16, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s) {
+                             int K, int bn, int bf16, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s,
+                             const CUtensorMap* tmOH, const CUtensorMap* tmU1T) {
   if (M <= 0) return cudaSuccess;
-  const bool u1 = ep.u1 != nullptr;
-#define PAIR_CASE(BNV)                                                                                      \
-  if (bn == BNV) {                                                                                          \
-    if (bf16) return u1 ? launch_pair_t<BNV, true, true>(tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s)        \
-                        : launch_pair_t<BNV, true, false>(tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);      \
-    return u1 ? launch_pair_t<BNV, false, true>(tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s)                 \
-              : launch_pair_t<BNV, false, false>(tmA, tmB, tmC, M, N, K, ep, num_sms, pdl, s);               \
+  // U1 variant: u1[request(row)] added on the tensor core (needs the one-hot rows and the u1 terms)
+  const bool u1 = ep.u1 != nullptr && tmOH != nullptr && tmU1T != nullptr;
+#define PAIR_CASE(BNV)                                                                                       \
+  if (bn == BNV) {                                                                                           \
+    if (bf16) return u1 ? launch_pair_t<BNV, true, true>(tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s) \
+                        : launch_pair_t<BNV, true, false>(tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s); \
+    return u1 ? launch_pair_t<BNV, false, true>(tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s)          \
+              : launch_pair_t<BNV, false, false>(tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s);        \
   }
   PAIR_CASE(256)
   PAIR_CASE(128)

@@ -175,10 +175,10 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
         const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + 8 * j));
         const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + 8 * j + 4));
         uint4 w;
-        w.x = Pack<BF16>::two(fmaxf(__uint_as_float(v[o + 0]) + b0.x, 0.0f), fmaxf(__uint_as_float(v[o + 1]) + b0.y, 0.0f));
-        w.y = Pack<BF16>::two(fmaxf(__uint_as_float(v[o + 2]) + b0.z, 0.0f), fmaxf(__uint_as_float(v[o + 3]) + b0.w, 0.0f));
-        w.z = Pack<BF16>::two(fmaxf(__uint_as_float(v[o + 4]) + b1.x, 0.0f), fmaxf(__uint_as_float(v[o + 5]) + b1.y, 0.0f));
-        w.w = Pack<BF16>::two(fmaxf(__uint_as_float(v[o + 6]) + b1.z, 0.0f), fmaxf(__uint_as_float(v[o + 7]) + b1.w, 0.0f));
+        w.x = Pack<BF16>::two_relu(__uint_as_float(v[o + 0]) + b0.x, __uint_as_float(v[o + 1]) + b0.y);
+        w.y = Pack<BF16>::two_relu(__uint_as_float(v[o + 2]) + b0.z, __uint_as_float(v[o + 3]) + b0.w);
+        w.z = Pack<BF16>::two_relu(__uint_as_float(v[o + 4]) + b1.x, __uint_as_float(v[o + 5]) + b1.y);
+        w.w = Pack<BF16>::two_relu(__uint_as_float(v[o + 6]) + b1.z, __uint_as_float(v[o + 7]) + b1.w);
         sts128(smem_u32(atom) + sw128_offset(r, j), w);
       }
       fence_async_smem();      // generic-proxy smem writes -> visible to the tensor core (async proxy)

@@ -161,17 +161,31 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 template <bool BF16> struct Pack;
+// RNE pack of two fp32 into f16x2 / bf16x2 (a -> low half, b -> high half); two_relu fuses ReLU into
+// the conversion (cvt.rn.relu: negative -> +0, NaN stays NaN) so the epilogues spend no FMNMX on it.
 template <> struct Pack<false> {
   static __device__ __forceinline__ uint32_t two(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
+  static __device__ __forceinline__ uint32_t two_relu(float a, float b) {
+    uint32_t d;
+    asm("cvt.rn.relu.f16x2.f32 %0, %2, %1;" : "=r"(d) : "f"(a), "f"(b));
+    return d;
+  }
+  static __device__ __forceinline__ float round_trip(float a) { return __half2float(__float2half_rn(a)); }
 };
 template <> struct Pack<true> {
   static __device__ __forceinline__ uint32_t two(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
   }
+  static __device__ __forceinline__ uint32_t two_relu(float a, float b) {
+    uint32_t d;
+    asm("cvt.rn.relu.bf16x2.f32 %0, %2, %1;" : "=r"(d) : "f"(a), "f"(b));
+    return d;
+  }
+  static __device__ __forceinline__ float round_trip(float a) { return __bfloat162float(__float2bfloat16_rn(a)); }
 };
 
 // Programmatic dependent launch: let the next kernel of the stream start its prologue now, and

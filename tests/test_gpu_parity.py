@@ -135,6 +135,17 @@ def test_kernel_variants_match_oracle(env, monkeypatch):
 
 
 @pytest.mark.parametrize("prec", ["f16", "bf16"])
+def test_many_small_requests(prec):
+    """Tiles spanning many requests: FC1 folds u1[request(row)] into the tensor-core reduction for up
+    to 8 (f16) / 5 (bf16) requests per 128-row tile and adds it in the epilogue beyond that."""
+    sizes = [int(x) for x in np.random.default_rng(5).integers(1, 21, 60)] + [300, 7, 2, 450]
+    sch, params, batch = small_case("paper", R=len(sizes), n_ads=tuple(sizes), precision=prec, cap=20000, seed=61)
+    ctx = make_ctx(sch, params)
+    p, z = _oracle_scores(sch, params, batch)
+    _check_scores(gpu_scores(ctx, batch), p, z, prec, f"small requests {prec}")
+
+
+@pytest.mark.parametrize("prec", ["f16", "bf16"])
 def test_chunking_and_batching_invariance(prec):
     """Scores do not depend on the chunk size nor on the other requests."""
     sch, params, batch = small_case("paper", R=3, n_ads=(300, 1000, 77), precision=prec, cap=20000, seed=41)
@@ -361,3 +372,33 @@ def test_split_request_merge_topk_equals_unsplit(G):
         torch.cuda.synchronize()
         np.testing.assert_array_equal(out_idx.cpu().numpy().reshape(R, K), full_idx)
         np.testing.assert_array_equal(out_key.cpu().numpy().reshape(R, K), full_key)
+
+
+# ---- F4: vector-product based model -----------------------------------------
+
+@pytest.mark.parametrize("prec,d", [("f16", 64), ("bf16", 32), ("f32", 16), ("f16", 256)])
+def test_vps_score_matches_oracle(prec, d):
+    import torch
+    from paper_2007_16122_b200 import vps_score
+    rng = np.random.default_rng(d)
+    card, R = 5000, 5
+    tab32 = coldgen.round_to(rng.uniform(-0.3, 0.3, (card, d)).astype(np.float32), prec)
+    if prec == "f16":
+        stored = tab32.astype(np.float16).view(np.uint16)
+    elif prec == "bf16":
+        stored = coldgen.f32_to_bf16_bits(tab32)
+    else:
+        stored = tab32
+    u = rng.uniform(-0.5, 0.5, (R, d)).astype(np.float32)
+    sizes = [1, 700, 33, 2048, 5]
+    ao = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    ids = rng.integers(0, card, ao[-1]).astype(np.int32)
+    want = oracle.vps_score(stored, prec, u.astype(np.float64), ao, ids)
+    out = torch.empty(int(ao[-1]), dtype=torch.float32, device="cuda")
+    st = np.ascontiguousarray(stored)
+    st = st.view(np.int16) if st.dtype == np.uint16 else st
+    vps_score(torch.from_numpy(st).cuda(), prec, torch.from_numpy(u).cuda(),
+              torch.from_numpy(ids).cuda(), torch.from_numpy(ao).cuda(), ao, out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().astype(np.float64)
+    assert rel_err(got, want).max() <= 1e-5

@@ -358,3 +358,26 @@ def test_ecpm_key():
     bid = np.array([1.0, 10.0, 1.0])
     assert oracle.topk(p, 1)[0][0] == 0
     assert oracle.topk(p * bid, 1)[0][0] == 1
+
+
+# ---- F4: the vector-product based model COLD is compared with -------------
+
+def test_vps_worked_example():
+    gd = load_golden("vps_example.json")
+    p = oracle.vps_score(np.asarray(gd["ad_table"], np.float32), "f32", np.asarray(gd["user_vecs"]),
+                         gd["ad_offsets"], gd["ad_ids"])
+    np.testing.assert_allclose(p, gd["expected_p"], rtol=1e-15)
+
+
+def test_vps_closed_forms():
+    """Orthogonal vectors score sigma(0) = 1/2; v_a = c v_u scores sigma(c |v_u|^2); 16-bit storage of
+    exactly representable values equals fp32 storage; ids out of range raise."""
+    u = np.array([[1.0, -2.0, 0.5, 4.0]])
+    tab = np.array([[2.0, 1.0, 0.0, 0.0], [0.5, -1.0, 0.25, 2.0], [-1, 2, -0.5, -4]], np.float32)
+    p = oracle.vps_score(tab, "f32", u, [0, 3], [0, 1, 2])
+    sq = float((u[0] ** 2).sum())
+    np.testing.assert_allclose(p, [0.5, 1 / (1 + math.exp(-0.5 * sq)), 1 / (1 + math.exp(sq))], rtol=1e-15)
+    p16 = oracle.vps_score(tab.astype(np.float16).view(np.uint16), "f16", u, [0, 3], [0, 1, 2])
+    np.testing.assert_array_equal(p16, p)
+    with pytest.raises(oracle.OracleError):
+        oracle.vps_score(tab, "f32", u, [0, 1], [3])

@@ -1,26 +1,27 @@
 #!/bin/bash
-# Run under gpurun: launch list + one `--set full` capture of each hot kernel (gather, FC1, FC2, tail).
-# Usage: bash tools/ncu_profile.sh <tag> [kernels...]   (default kernels: gather fc1 fc2 tail)
+# Run under gpurun: launch list + one `--set full` capture of each hot kernel.
+# Usage: bash tools/ncu_profile.sh <tag> [kernels...]   (default: gather fc1 fc2 fc3 tail45)
 set -x
 TAG=${1:-r01}
 shift
-KERNELS=${@:-gather fc1 fc2 tail}
+KERNELS=${@:-gather fc1 fc2 fc3 tail45}
 OUT=gpurun_out
-# 32 requests x 9472 ads = 2 full 151552-ad chunks per step
+# 32 requests x 9472 ads = 2 full 151552-ad chunks per step (one gather span)
 ARGS=${NCU_ARGS:-"--requests 32 --ads 9472 --steps 2 --warmup 1 --no-e2e --no-latency --no-cpu"}
 python -m paper_2007_16122_b200.build >/dev/null
 # 1. launch list (cold-cache, serialised: compare shares)
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv \
   --log-file $OUT/launches_$TAG.csv python bench.py $ARGS > $OUT/ncu_launch_bench_$TAG.log 2>&1
 for k in $KERNELS; do
   case $k in
-    gather) RX="regex:gather_kernel";;
-    fc1) RX="regex:^gemm_kernel";;
-    fc2) RX="regex:gemm_pair_kernel";;
-    tail) RX="regex:tail_kernel";;
-    *) RX="regex:$k";;
+    gather) RX="regex:gather_kernel"; S=1;;
+    fc1) RX="regex:gemm_pair_kernel"; S=3;;      # pair launches per chunk: FC1, FC2, FC3
+    fc2) RX="regex:gemm_pair_kernel"; S=4;;
+    fc3) RX="regex:gemm_pair_kernel"; S=5;;
+    tail45) RX="regex:tail45_kernel"; S=1;;
+    *) RX="regex:$k"; S=1;;
   esac
-  timeout 900 ncu --set full --clock-control none --import-source on -k $RX -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k $RX -s $S -c 1 \
     -o $OUT/prof_${k}_$TAG python bench.py $ARGS > $OUT/ncu_${k}_$TAG.log 2>&1
 done
 for f in $OUT/prof_*_$TAG.ncu-rep; do python tools/ncu_summary.py $f; done > $OUT/ncu_summary_$TAG.txt 2>&1
