@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--se-sweep", action="store_true",
                     help="BASELINE configs[3]: SE-selected group subsets of S-full, ads/s vs group count")
     ap.add_argument("--se-sample", type=int, default=10000, help="ads in the SE statistics sample (AMB-16)")
+    ap.add_argument("--vps", action="store_true",
+                    help="F4: the vector-product baseline (P:160-166) on the same request stream, ads/s")
+    ap.add_argument("--vps-dim", type=int, default=64)
     return ap.parse_args()
 
 
@@ -307,10 +310,70 @@ def run_se_sweep(args):
     print(json.dumps(line), flush=True)
 
 
+def run_vps(args):
+    """SURVEY §8(f) F4 / Table tab:sys: the vector-product based model served with
+    precomputed towers (v_a per ad, v_u per request), p = sigma(v_u . v_a) + per-request top-K, on the
+    same request stream shape as the headline run (device-resident inputs, CUDA-event timing)."""
+    import torch
+    from paper_2007_16122_b200 import Context, vps_score
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    R, n, d, K = args.requests, args.ads, args.vps_dim, args.topk
+    card = 10**7                                                    # ad_id cardinality of S-paper
+    g = torch.Generator(device=dev).manual_seed(args.seed)
+    vecs = ((torch.rand(card, d, device=dev, generator=g) - 0.5) * 0.5).to(torch.float16)
+    user = (torch.rand(R, d, device=dev, generator=g) - 0.5) * 0.5
+    ids = torch.randint(0, card, (R * n,), device=dev, generator=g, dtype=torch.int32)
+    ao = np.arange(0, (R + 1) * n, n, dtype=np.int32)
+    d_ao = torch.from_numpy(ao).to(dev)
+    scores = torch.empty(R * n, dtype=torch.float32, device=dev)
+    idx = torch.empty(R * K, dtype=torch.int32, device=dev)
+    key = torch.empty(R * K, dtype=torch.float32, device=dev)
+    sch = coldgen.schema_tiny()           # a ctx only for cold_topk's staging; no parameters needed
+    ctx = Context(sch.groups, sch.k, sch.widths, precision="f32", max_ads=128, max_requests=R)
+
+    def step():
+        vps_score(vecs.view(torch.int16), "f16", user, ids, d_ao, ao, scores)
+        ctx.topk(scores, d_ao, ao, K, idx, key)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    e0.record()
+    for _ in range(args.steps):
+        vps_score(vecs.view(torch.int16), "f16", user, ids, d_ao, ao, scores)
+    e1.record()
+    e1.synchronize()
+    ms_s = e0.elapsed_time(e1) / args.steps
+    bytes_per_ad = d * 2 + 4 + 4
+    peaks, _ = measured_peaks()
+    gbs = R * n * bytes_per_ad / (ms_s / 1e3) / 1e9
+    line = {"metric": METRIC, "value": R * n / (ms / 1e3), "unit": "ads/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "dtype": "f16",
+            "data": "synthetic (random ad / user tower vectors)",
+            "config": {"workload": f"F4 vector-product baseline (P:160-166): {R} requests x {n} ads, d={d}, fp16 "
+                                   f"ad vectors for {card} ads, fp32 user vectors, top-{K}"},
+            "roofline": {"bound": "hbm", "kernel": "vps", "achieved": gbs, "peak": float(peaks["hbm_gbs"]),
+                         "unit": "GB/s", "frac": gbs / float(peaks["hbm_gbs"]),
+                         "algorithmic": f"{bytes_per_ad} B/ad (v_a row + id + score)"},
+            "score_only_ms": ms_s}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.vps:
+        run_vps(args)
         return
     if args.se_sweep:
         run_se_sweep(args)

@@ -101,6 +101,7 @@ struct cold_ctx {
   int cs[COLD_MAX_LAYERS] = {0};     // cluster size (weight-tile multicast) per GEMM layer
   bool resb[COLD_MAX_LAYERS] = {false};  // weight slice resident in shared memory (K x BN <= 128 KB)
   bool pair[COLD_MAX_LAYERS] = {false};  // CTA-pair (cta_group::2) GEMM
+  bool pair_res[COLD_MAX_LAYERS] = {false};  // ... with the pair's weight half resident (one n-tile per pair)
   int tail_mode = 0;                 // 0: every layer a GEMM (head fused into the last); 1: FC(L-3..L-1) +
                                      // head fused (tail_kernel); 2: FC(L-2..L-1) + head fused (tail45_kernel)
   int n_tail = 0;                    // hidden layers inside the fused tail (0, 3 or 2)
@@ -433,8 +434,8 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       if (l < c->L - 2) {
         // epilogue store boxes: 32 rows x 64 columns (SW128) when each epilogue warp's column half is a
         // multiple of 64 (epi.cuh), else 32 x 32 (SW64)
-        s = make_tmap(&c->tmC[l], c->d_H[l], c->precision, c->widths[l], c->chunk, 32,
-                      (c->bn[l] / 2) % 64 == 0 ? 64 : 32);
+        const bool wide = (c->bn[l] / 2) % 64 == 0;   // epi.cuh group boxes: 128 rows x 64 cols (SW128)
+        s = make_tmap(&c->tmC[l], c->d_H[l], c->precision, c->widths[l], c->chunk, wide ? 128 : 32, wide ? 64 : 32);
         if (s) { delete c; return s; }
       } else {
         c->tmC[l] = c->tmA[l];   // unused by the head epilogue
@@ -451,6 +452,8 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       c->pair[l] = !in_tail && l < Lg - 1 && c->bn[l] == 256 &&
                    (pair_mode == 2 || (pair_mode == 1 && !c->resb[l]));
       if (c->pair[l]) { c->resb[l] = false; c->cs[l] = 1; }
+      const char* env_pres = getenv("COLD_PAIR_RES");
+      c->pair_res[l] = c->pair[l] && gemm_pair_resident_ok(c->bn[l], K) && !(env_pres && atoi(env_pres) == 0);
     }
   }
   if (c->tensor && c->pair[0] && c->n_tail < c->L - 1) {
@@ -930,6 +933,10 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     const int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
     ep.instr = instr_on ? g_instr + 8 * l : nullptr;
     {
+      static const char* env_dir = getenv("COLD_EPI_DIRECT");  // bitmask of layers storing with st.global
+      if (env_dir && ((atoi(env_dir) >> l) & 1)) ep.direct = 1;
+    }
+    {
       static const char* env_dbg = getenv("COLD_DBG_GEMM");   // "<layer>:<mode>" timing experiments
       if (env_dbg && atoi(env_dbg) == l && strchr(env_dbg, ':')) ep.dbg_mode = atoi(strchr(env_dbg, ':') + 1);
     }
@@ -937,7 +944,8 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     if (c->pair[l])
       launch_gemm_pair(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
                        c->precision == COLD_BF16 ? 1 : 0, ep, c->num_sms, c->pdl && !c->prof, st,
-                       (l == 0 && c->u1mma) ? &c->tmOH[xslot] : nullptr, (l == 0 && c->u1mma) ? &c->tmU1T : nullptr);
+                       (l == 0 && c->u1mma) ? &c->tmOH[xslot] : nullptr, (l == 0 && c->u1mma) ? &c->tmU1T : nullptr,
+                       c->pair_res[l]);
     else
       launch_gemm(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
                   c->precision == COLD_BF16 ? 1 : 0, c->cs[l], c->resb[l], ep, c->num_sms, c->pdl && !c->prof, st);

@@ -1,25 +1,36 @@
 // epi.cuh — the store-mode epilogue shared by the tcgen05 GEMM kernels (sm_100a).
 //
-// One epilogue warp drains its 32 accumulator rows (TMEM lanes of its quadrant) x 64 columns at a
-// time: two tcgen05.ld 32x32b.x32 in flight, + bias or + u1[request] (fp32), ReLU, RNE pack, one
-// 32-row x 64-col box written in the 128 B-swizzled layout (full 128 B lines per row), one TMA store.
-// Versus 32-column boxes with 64 B rows this halves the TMEM waits, fences, warp syncs and TMA
-// stores per output and gives the TMA unit whole lines (FC1's epilogue was the kernel's bottleneck:
-// 95 us per 151,552-ad chunk with the MMAs disabled vs 65 us for the MMA main loop alone).
+// Each epilogue warp drains its 32 accumulator rows (TMEM lanes of its quadrant q) x 64 columns at a
+// time: two tcgen05.ld 32x32b.x32 in flight, + bias or + u1[request] (fp32), ReLU fused into the RNE
+// pack, and its 32 rows written into a 128-row x 64-column box in the 128 B-swizzled layout (full
+// 128 B lines). The four quadrant warps of a column half form a group (named barrier 1 + h): once all
+// four have written, one elected thread issues ONE 16 KB TMA store for the group. Timing of the FC1
+// epilogue (tools/probes/epi_instr.py) showed the warps waiting ~40% of their time for their own
+// 4 KB stores to drain: the TMA unit, shared with the operand loads, was limited by store count.
 #pragma once
 #include "ptx.cuh"
 
 namespace cold {
 
 constexpr int EPI_WIDE_COLS = 64;
-constexpr int EPI_WIDE_BOX = 32 * EPI_WIDE_COLS * 2;   // 4 KB, single-buffered per warp
+constexpr int EPI_WIDE_BOX = 32 * EPI_WIDE_COLS * 2;   // 4 KB: one warp's rows of the group box
+constexpr int EPI_GROUP_BOX = 4 * EPI_WIDE_BOX;        // 16 KB: 128 rows x 64 columns, single-buffered
 
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// group_buf: the group's 16 KB box (128 rows x 128 B, SW128, 1024 B aligned); q: this warp's quadrant;
+// h: the column half (group id); tile_row0: the tile's first row (the box origin).
 template <bool BF16>
 __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int c_end, const float* __restrict__ bias,
-                                               uint32_t u1s, const float* __restrict__ u1g, int relu, uint8_t* buf,
-                                               const CUtensorMap* tmC, int col_base, int row0, int lane,
-                                               int dbg = 0, unsigned long long* tacc = nullptr) {
-  const uint32_t sbuf = smem_u32(buf);
+                                               uint32_t u1s, const float* __restrict__ u1g, int relu,
+                                               uint8_t* group_buf, const CUtensorMap* tmC, int col_base,
+                                               int tile_row0, int q, int h, int lane, int dbg = 0,
+                                               unsigned long long* tacc = nullptr, void* gout = nullptr,
+                                               int ldo = 0, int M = 0) {
+  const uint32_t sbuf = smem_u32(group_buf) + (uint32_t)q * EPI_WIDE_BOX;
+  const bool elected = (q == 0) && (lane == 0);
   // debug timing (tacc != null, lane 0): cycles in [0] TMEM load+wait, [1] math+pack, [2] wait for the
   // staging buffer, [3] smem writes + fence, [4] store issue
   long long tc0 = 0, tsum[5] = {0, 0, 0, 0, 0};
@@ -78,18 +89,32 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
       continue;
     }
     tick(1);
-    if (lane == 0) bulk_wait_read<0>();   // the previous box of this warp has left shared memory
-    __syncwarp();
+    if (gout) {                           // direct mode: this lane's row, 128 B, four 256-bit stores
+      const int row = tile_row0 + q * 32 + lane;
+      if (row < M) {
+        uint16_t* dst = reinterpret_cast<uint16_t*>(gout) + (int64_t)row * ldo + col0;
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+          asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 16 * j), "r"(pk[8 * j]),
+                       "r"(pk[8 * j + 1]), "r"(pk[8 * j + 2]), "r"(pk[8 * j + 3]), "r"(pk[8 * j + 4]),
+                       "r"(pk[8 * j + 5]), "r"(pk[8 * j + 6]), "r"(pk[8 * j + 7])
+                       : "memory");
+      }
+      tick(4);
+      continue;
+    }
+    if (elected) bulk_wait_read<0>();     // the group's previous box has left shared memory
+    named_bar_sync(1 + h, 128);
     tick(2);
     const uint32_t rowp = sbuf + (uint32_t)lane * 128u;
 #pragma unroll
     for (int j = 0; j < 8; j++)
       sts128(rowp + (uint32_t)((j ^ (lane & 7)) << 4), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
     fence_async_smem();
-    __syncwarp();
+    named_bar_sync(1 + h, 128);           // all 128 rows of the box written
     tick(3);
-    if (lane == 0 && dbg != 4) {
-      tma_store_2d(tmC, buf, col0, row0);
+    if (elected && dbg != 4) {
+      tma_store_2d(tmC, group_buf, col0, tile_row0);
       bulk_commit();
     }
     tick(4);

@@ -104,6 +104,7 @@ struct EpiParams {
   float* scores;                   // chunk-local [M]
   int relu;
   unsigned long long* instr;       // debug: per-role wait-cycle counters [8] (null = off)
+  int direct;                      // epilogue writes rows with st.global (no smem staging / TMA store)
   int dbg_mode;                    // timing experiments only (results invalid): 1 = epilogue only drains
                                    // TMEM (no math / stores), 2 = MMA issuer skips the MMAs, 3 = epilogue
                                    // math without smem / TMA stores, 4 = smem staging but no TMA store
@@ -119,7 +120,10 @@ bool gemm_resident_ok(int bn, int K);
 constexpr int U1_NSLOT = 8;
 cudaError_t launch_gemm_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N,
                              int K, int bn, int bf16, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s,
-                             const CUtensorMap* tmOH = nullptr, const CUtensorMap* tmU1T = nullptr);
+                             const CUtensorMap* tmOH = nullptr, const CUtensorMap* tmU1T = nullptr,
+                             bool res = false);
+// the pair's weight half fits resident (<= 64 KB): the RES variant keeps it in smem for the launch
+bool gemm_pair_resident_ok(int bn, int K);
 
 // fused FC(L-4) .. FC(L-2) + head (paper widths 256, 128, 64 -> 2)
 struct TailParams {

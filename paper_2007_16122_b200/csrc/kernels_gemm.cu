@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int c_stop = ep.dbg_mode == 1 ? c_begin : c_end;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
         epi_store_wide<BF16>(tbase, c_begin, c_stop, ep.bias, u1s, u1row, ep.relu,
-                             sOut + ew * EPI_WIDE_BOX, &tmC, nb * BN, row0, lane, ep.dbg_mode);
+                             sOut + h * EPI_GROUP_BOX, &tmC, nb * BN, row0 - q * 32, q, h, lane, ep.dbg_mode);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);

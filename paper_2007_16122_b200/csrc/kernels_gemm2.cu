@@ -39,21 +39,28 @@ constexpr int P_EPI_COLS = 32;
 constexpr int P_OUT_BOX = 32 * P_EPI_COLS * 2;     // 2 KB staging box (32 rows x 32 cols)
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;        // shared::cluster address of the leader's copy
 
-template <int BN, bool U1> struct PairCfg {
+// RES: the CTA pair owns one n-tile for the whole launch and keeps its weight half (BN/2 x K) resident in
+// shared memory, so only A streams (FC1: K = 256, 64 KB per CTA). The GEMMs here are L2/TMA-bandwidth
+// bound (FC1 moved ~30 B/cycle/SM with or without its epilogue); this halves FC1's operand traffic.
+constexpr int P_RES_BYTES = 64 * 1024;
+
+template <int BN, bool U1, bool RES = false> struct PairCfg {
   static constexpr int A_BYTES = BM * BK * 2;                 // own 128 rows
-  static constexpr int B_BYTES = (BN / 2) * BK * 2;           // own half of the weight tile
+  static constexpr int B_BYTES = RES ? 0 : (BN / 2) * BK * 2; // own half of the weight tile (streamed)
+  static constexpr int B_ATOM = (BN / 2) * BK * 2;            // one resident K block of the weight half
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int RES_BYTES = RES ? P_RES_BYTES : 0;
   static constexpr int OUT_BYTES = P_EPI_WARPS * 2 * P_OUT_BOX;   // = P_EPI_WARPS * EPI_WIDE_BOX
   static constexpr int UXA_BYTES = BM * 32;                   // A_x: 128 rows x 16 halves (2 K chunks)
   static constexpr int UXB_BYTES = (BN / 2) * 16 * 4;         // B_x: own BN/2 columns x 4 K chunks of 8
   static constexpr int UX_BUF = UXA_BYTES + UXB_BYTES;
   static constexpr int NUX = 2;
   static constexpr int UX_BYTES = U1 ? NUX * UX_BUF : 0;
-  static constexpr int STAGES_FIT = (232448 - OUT_BYTES - UX_BYTES - 1024 - 512) / STAGE_BYTES;
+  static constexpr int STAGES_FIT = (232448 - RES_BYTES - OUT_BYTES - UX_BYTES - 1024 - 512) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN;
   static constexpr int THREADS = P_THREADS;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + OUT_BYTES + UX_BYTES + 1024 + 512;
+  static constexpr int SMEM = RES_BYTES + STAGES * STAGE_BYTES + OUT_BYTES + UX_BYTES + 1024 + 512;
 };
 
 // SMEM descriptor, K-major, no swizzle (the u1 operand): core matrices of 8 rows x 16 B; rows are
@@ -109,17 +116,18 @@ __device__ __forceinline__ constexpr uint32_t idesc_pair() {
          ((uint32_t)(256 >> 4) << 24);
 }
 
-template <int BN, bool BF16, bool U1>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THREADS, 1)
+template <int BN, bool BF16, bool U1, bool RES>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>::THREADS, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmOH,
                      const __grid_constant__ CUtensorMap tmU1T, int M, int N, int K, EpiParams ep) {
-  using Cfg = PairCfg<BN, U1>;
+  using Cfg = PairCfg<BN, U1, RES>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
-  uint8_t* sOut = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint8_t* sRes = smem;                                        // RES: [K/64][BN/2 rows x 128 B]
+  uint8_t* sA = smem + Cfg::RES_BYTES;
+  uint8_t* sB = sA + Cfg::STAGES * Cfg::A_BYTES;
+  uint8_t* sOut = sA + Cfg::STAGES * Cfg::STAGE_BYTES;
   uint8_t* sUX = sOut + Cfg::OUT_BYTES;                        // [NUX][A_x | B_x]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sUX + Cfg::UX_BYTES);
   uint64_t* full = bars;                          // leader: A+B bytes of both CTAs
@@ -128,7 +136,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THR
   uint64_t* tempty = tfull + 2;                   // leader: both CTAs' epilogues drained
   uint64_t* uxfull = tempty + 2;                  // leader: both CTAs' u1 operand bytes landed [NUX]
   uint64_t* uxempty = uxfull + Cfg::NUX;          // both: the u1 MMA of the buffer's last tile completed [NUX]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uxempty + Cfg::NUX);
+  uint64_t* bres = uxempty + Cfg::NUX;            // leader: resident weight halves of both CTAs landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -137,11 +146,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THR
   const int num_pm = (M + 2 * BM - 1) / (2 * BM), num_n = N / BN;
   const int items = num_pm * num_n;
   const int kb_count = K / BK;
+  // work list: streaming -> items (pm, nb) strided over all pairs; RES -> this pair's fixed n-tile,
+  // m-tiles strided over the pairs sharing it (pairs beyond groups * num_n get no work)
+  int w_first, w_step, w_count;
+  if (RES) {
+    const int groups = npairs / num_n;
+    w_first = pair / num_n;
+    w_step = groups > 0 ? groups : 1;
+    w_count = (pair < groups * num_n) ? num_pm : 0;
+  } else {
+    w_first = pair;
+    w_step = npairs;
+    w_count = items;
+  }
+  auto tile_of = [&](int it, int& pm, int& nb) {
+    if (RES) { pm = it; nb = pair % num_n; }
+    else { pm = it / num_n; nb = it % num_n; }
+  };
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < Cfg::STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; s++) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * P_EPI_WARPS); }
     for (int s = 0; s < Cfg::NUX; s++) { mbar_init(&uxfull[s], 1); mbar_init(&uxempty[s], 1); }
+    mbar_init(bres, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
@@ -180,17 +207,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THR
       int lt = 0;
       constexpr int TERMS = BF16 ? 3 : 2;
       // the pair tile's first request rounded down to 8 (16 B-aligned TMA box start), prefetched
-      int r_next = (U1 && pair < items) ? (ep.req_of_ad[ep.a0 + (pair / num_n) * 2 * BM] & ~7) : 0;
-      for (int it = pair; it < items; it += npairs, lt++) {
-        const int pm = it / num_n, nb = it % num_n;
+      auto pm_of = [&](int it) { int pm, nb; tile_of(it, pm, nb); return pm; };
+      int r_next = (U1 && w_first < w_count) ? (ep.req_of_ad[ep.a0 + pm_of(w_first) * 2 * BM] & ~7) : 0;
+      if (RES && w_count > 0) {   // this pair's weight half, once
+        if (leader) mbar_expect_tx(bres, 2 * kb_count * Cfg::B_ATOM);
+        for (int kb = 0; kb < kb_count; kb++)
+          tma_load_2d_pair(sRes + kb * Cfg::B_ATOM, &tmB, bres, kb * BK, (pair % num_n) * BN + (int)rank * (BN / 2),
+                           pol_b);
+      }
+      for (int it = w_first; it < w_count; it += w_step, lt++) {
+        int pm, nb;
+        tile_of(it, pm, nb);
         const int mrow = pm * 2 * BM + (int)rank * BM;
         const int r_first = r_next;
-        if (U1 && it + npairs < items) r_next = ep.req_of_ad[ep.a0 + ((it + npairs) / num_n) * 2 * BM] & ~7;
+        if (U1 && it + w_step < w_count) r_next = ep.req_of_ad[ep.a0 + pm_of(it + w_step) * 2 * BM] & ~7;
         for (int kb = 0; kb < kb_count; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           if (leader) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
           tma_load_2d_pair(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK, mrow, pol_a);
-          tma_load_2d_pair(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, nb * BN + (int)rank * (BN / 2), pol_b);
+          if (!RES)
+            tma_load_2d_pair(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, nb * BN + (int)rank * (BN / 2), pol_b);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
         }
         if (U1) {   // the tile's u1 operand: A_x one-hot rows (2 boxes) + B_x term columns (TERMS boxes)
@@ -214,7 +250,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THR
       int s = 0;
       uint32_t ph = 0;
       int lt = 0;
-      for (int it = pair; it < items; it += npairs, lt++) {
+      if (RES && w_count > 0) mbar_wait(bres, 0);
+      for (int it = w_first; it < w_count; it += w_step, lt++) {
         const int acc = lt & 1;
         mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -223,7 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THR
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + s * Cfg::A_BYTES));
-          const uint64_t bd = sdesc_sw128(smem_u32(sB + s * Cfg::B_BYTES));
+          const uint64_t bd = sdesc_sw128(smem_u32(RES ? sRes + kb * Cfg::B_ATOM : sB + s * Cfg::B_BYTES));
           if (ep.dbg_mode != 2) {
 #pragma unroll
             for (int kk = 0; kk < BK / UMMA_K; kk++)
@@ -257,8 +294,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THR
     uint8_t* my_out = sOut + ew * 2 * P_OUT_BOX;
     int ob = 0;
     int lt = 0;
-    for (int it = pair; it < items; it += npairs, lt++) {
-      const int pm = it / num_n, nb = it % num_n;
+    for (int it = w_first; it < w_count; it += w_step, lt++) {
+      int pm, nb;
+      tile_of(it, pm, nb);
       const int acc = lt & 1;
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
@@ -282,7 +320,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THR
         const int c_stop = ep.dbg_mode == 1 ? c_begin : c_end;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
         epi_store_wide<BF16>(tbase, c_begin, c_stop, ep.bias, u1s, u1row, ep.relu,
-                             sOut + ew * EPI_WIDE_BOX, &tmC, nb * BN, row0, lane, ep.dbg_mode, ep.instr);
+                             sOut + h * EPI_GROUP_BOX, &tmC, nb * BN, row0 - q * 32, q, h, lane, ep.dbg_mode,
+                             ep.instr, ep.direct ? ep.out : nullptr, ep.ldo, M);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
@@ -380,19 +419,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1>::THR
   }
 }
 
-template <int BN, bool BF16, bool U1>
+template <int BN, bool BF16, bool U1, bool RES>
 static cudaError_t launch_pair_t(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC,
                                  const CUtensorMap* tmOH, const CUtensorMap* tmU1T, int M, int N, int K,
                                  const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s) {
-  using Cfg = PairCfg<BN, U1>;
-  auto kern = gemm_pair_kernel<BN, BF16, U1>;
+  using Cfg = PairCfg<BN, U1, RES>;
+  auto kern = gemm_pair_kernel<BN, BF16, U1, RES>;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  const int items = ((M + 2 * BM - 1) / (2 * BM)) * (N / BN);
-  const int pairs = items < num_sms / 2 ? items : num_sms / 2;
+  const int num_pm = (M + 2 * BM - 1) / (2 * BM), num_n = N / BN;
+  const int items = num_pm * num_n;
+  int pairs = items < num_sms / 2 ? items : num_sms / 2;
+  if (RES) {   // whole groups of num_n pairs (one per n-tile), no more groups than m-tiles
+    int groups = (num_sms / 2) / num_n;
+    if (groups > num_pm) groups = num_pm;
+    if (groups < 1) groups = 1;
+    pairs = groups * num_n;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(Cfg::THREADS);
@@ -407,23 +453,34 @@ static cudaError_t launch_pair_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
   return cudaLaunchKernelEx(&cfg, kern, *tmA, *tmB, *tmC, U1 ? *tmOH : *tmA, U1 ? *tmU1T : *tmA, M, N, K, ep);
 }
 
+bool gemm_pair_resident_ok(int bn, int K) { return (int64_t)(bn / 2) * K * 2 <= P_RES_BYTES; }
+
 cudaError_t launch_gemm_pair(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N,
                              int K, int bn, int bf16, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s,
-                             const CUtensorMap* tmOH, const CUtensorMap* tmU1T) {
+                             const CUtensorMap* tmOH, const CUtensorMap* tmU1T, bool res) {
   if (M <= 0) return cudaSuccess;
   // U1 variant: u1[request(row)] added on the tensor core (needs the one-hot rows and the u1 terms)
   const bool u1 = ep.u1 != nullptr && tmOH != nullptr && tmU1T != nullptr;
-#define PAIR_CASE(BNV)                                                                                       \
-  if (bn == BNV) {                                                                                           \
-    if (bf16) return u1 ? launch_pair_t<BNV, true, true>(tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s) \
-                        : launch_pair_t<BNV, true, false>(tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s); \
-    return u1 ? launch_pair_t<BNV, false, true>(tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s)          \
-              : launch_pair_t<BNV, false, false>(tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s);        \
+  res = res && gemm_pair_resident_ok(bn, K);
+#define PAIR_ARGS tmA, tmB, tmC, tmOH, tmU1T, M, N, K, ep, num_sms, pdl, s
+#define PAIR_CASE(BNV)                                                                                 \
+  if (bn == BNV) {                                                                                     \
+    if (bf16) {                                                                                        \
+      if (u1) return res ? launch_pair_t<BNV, true, true, true>(PAIR_ARGS)                             \
+                         : launch_pair_t<BNV, true, true, false>(PAIR_ARGS);                           \
+      return res ? launch_pair_t<BNV, true, false, true>(PAIR_ARGS)                                    \
+                 : launch_pair_t<BNV, true, false, false>(PAIR_ARGS);                                  \
+    }                                                                                                  \
+    if (u1) return res ? launch_pair_t<BNV, false, true, true>(PAIR_ARGS)                              \
+                       : launch_pair_t<BNV, false, true, false>(PAIR_ARGS);                            \
+    return res ? launch_pair_t<BNV, false, false, true>(PAIR_ARGS)                                     \
+               : launch_pair_t<BNV, false, false, false>(PAIR_ARGS);                                   \
   }
   PAIR_CASE(256)
   PAIR_CASE(128)
   PAIR_CASE(64)
 #undef PAIR_CASE
+#undef PAIR_ARGS
   return cudaErrorInvalidValue;
 }
 
