@@ -656,6 +656,7 @@ def main():
             "roofline": roofline, "roofline_gather": roofline_gather, "fc_stack": fc_stack,
             "kernels": per_kernel, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
             "clocks": clocks, "latency": latency, "latency_split": latency_split, "setup_s": setup_s,
+            "compressed_activations": bool(info.get("compressed_activations", 0)),
             "profiled_region": {"ms_per_step": ms_prof / args.steps,
                                 "note": "per-kernel CUDA events (kernels, roofline) come from this second timed "
                                         "region of the same steps"},

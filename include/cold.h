@@ -113,6 +113,14 @@ typedef struct {
                                     the selected groups); rounded RNE to the compute precision for the
                                     tensor-core layers; the per-request user block of W1 stays fp32 */
   const float* const* fc_b;      /* [L] each [out_l], kept fp32 */
+  /* Optional input normalisation ("one solution is to use normalization
+   * layers like the batch-norm layer ... batch-norm layers use Float32"): inference-time batch norm
+   * of the network input folded to an affine map per input column, x_j <- x_j * in_scale[j] +
+   * in_shift[j] (in_scale = gamma / sqrt(var + eps), in_shift = beta - mean * in_scale), applied in
+   * fp32 after the SE gate and before the 16-bit cast. [D_in] each, schema order of the selected
+   * groups; both NULL = none. Usually paired with linear_log = 0 (the paper's other choice). */
+  const float* in_scale;
+  const float* in_shift;
 } cold_params;
 
 /* One call's requests. Column-major per group ("column based computation"). */
@@ -136,6 +144,7 @@ typedef struct {
   int32_t kernels_per_call;      /* launches per call outside the chunk loop */
   int32_t tensor_core;           /* 1 if the FC stack runs on tcgen05 */
   int64_t device_bytes;          /* device memory owned by the ctx */
+  int32_t compressed_activations;/* 1 if the activation buffers got compressible memory (COLD_COMPRESS=1) */
 } cold_info;
 
 /* Create a context on config->device: validates the schema (AMB-1..AMB-18 readings in

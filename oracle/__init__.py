@@ -51,7 +51,8 @@ class _Model(C.Structure):
                 ("se_b_dense", C.POINTER(C.c_double)),
                 ("linear_log", C.c_int32), ("ll_after_se", C.c_int32),
                 ("L", C.c_int32), ("widths", C.POINTER(C.c_int32)),
-                ("W", C.POINTER(C.POINTER(C.c_double))), ("b", C.POINTER(C.POINTER(C.c_double)))]
+                ("W", C.POINTER(C.POINTER(C.c_double))), ("b", C.POINTER(C.POINTER(C.c_double))),
+                ("in_scale", C.POINTER(C.c_double)), ("in_shift", C.POINTER(C.c_double))]
 
 
 class _Batch(C.Structure):
@@ -111,7 +112,7 @@ class Model:
 
     def __init__(self, schema: coldgen.Schema, params: coldgen.Params, selected: Optional[Sequence[int]] = None,
                  linear_log: Optional[bool] = None, ll_after_se: bool = False,
-                 se_dense: Optional[tuple] = None):
+                 se_dense: Optional[tuple] = None, in_norm: Optional[tuple] = None):
         self.schema, self.params = schema, params
         sel = list(range(schema.M)) if selected is None else sorted(selected)
         self._keep = []
@@ -142,6 +143,10 @@ class Model:
         m.ll_after_se = int(ll_after_se)
         m.L, m.widths = len(self.W), _ptr(self.widths, C.c_int32)
         m.W, m.b = C.cast(Wp, C.POINTER(C.POINTER(C.c_double))), C.cast(bp, C.POINTER(C.POINTER(C.c_double)))
+        if in_norm is not None:   # (in_scale, in_shift) [n_sel * k]: folded input batch norm
+            self.isc = np.ascontiguousarray(in_norm[0], np.float64)
+            self.ish = np.ascontiguousarray(in_norm[1], np.float64)
+            m.in_scale, m.in_shift = _ptr(self.isc, C.c_double), _ptr(self.ish, C.c_double)
         self.m = m
 
 

@@ -184,6 +184,8 @@ static int features(const orc_model* m, const orc_batch* bt, int64_t r, int64_t 
     for (int d = 0; d < k; d++) {
       double v = s * eh[d];
       if (m->linear_log && m->ll_after_se) v = orc_linear_log(v);
+      /* batch norm of the network input, inference form (folded affine per column) */
+      if (m->in_scale) v = v * m->in_scale[(size_t)j * k + d] + m->in_shift[(size_t)j * k + d];
       x[(size_t)j * k + d] = v;
     }
   }
@@ -307,6 +309,7 @@ int32_t orc_features(const orc_model* m, const orc_batch* bt, const int64_t* ad_
         for (int d = 0; d < k; d++) {
           double v = s * e[d];
           if (m->linear_log && m->ll_after_se) v = orc_linear_log(v);
+          if (m->in_scale) v = v * m->in_scale[(size_t)j * k + d] + m->in_shift[(size_t)j * k + d];
           x_out[(size_t)i * D + (size_t)j * k + d] = v;
         }
       }

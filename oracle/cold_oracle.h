@@ -50,6 +50,8 @@ typedef struct {
   const int32_t* widths;        /* [L] outputs; input of layer 0 = n_sel * k */
   const double* const* W;       /* [L] each [out][in] */
   const double* const* b;       /* [L] each [out] */
+  const double* in_scale;       /* [n_sel * k] or NULL: input batch norm folded to x_j * in_scale[j] +  */
+  const double* in_shift;       /* in_shift[j] (P:276's alternative to linear_log)  */
 } orc_model;
 
 typedef struct {

@@ -56,7 +56,8 @@ class cold_config(C.Structure):
 class cold_params(C.Structure):
     _fields_ = [("table_dtype", C.c_int32), ("tables", C.POINTER(C.c_void_p)),
                 ("se_w", C.c_void_p), ("se_b", C.c_void_p),
-                ("fc_w", C.POINTER(C.c_void_p)), ("fc_b", C.POINTER(C.c_void_p))]
+                ("fc_w", C.POINTER(C.c_void_p)), ("fc_b", C.POINTER(C.c_void_p)),
+                ("in_scale", C.c_void_p), ("in_shift", C.c_void_p)]
 
 
 class cold_batch(C.Structure):
@@ -68,7 +69,7 @@ class cold_batch(C.Structure):
 class cold_info(C.Structure):
     _fields_ = [("version", C.c_uint64), ("d_in", C.c_int32), ("d_user", C.c_int32), ("d_ad", C.c_int32),
                 ("chunk_ads", C.c_int32), ("kernels_per_chunk", C.c_int32), ("kernels_per_call", C.c_int32),
-                ("tensor_core", C.c_int32), ("device_bytes", C.c_int64)]
+                ("tensor_core", C.c_int32), ("device_bytes", C.c_int64), ("compressed_activations", C.c_int32)]
 
 
 _lib = None
@@ -215,9 +216,11 @@ class Context:
         except Exception:
             pass
 
-    def load_params(self, tables, se_w, se_b, fc_w, fc_b, table_dtype: str = "f32") -> int:
+    def load_params(self, tables, se_w, se_b, fc_w, fc_b, table_dtype: str = "f32", in_scale=None,
+                    in_shift=None) -> int:
         """Host arrays: tables[g] [card, k] (float32, or uint16/float16 bit patterns in the compute
-        precision), se_w [M, k], se_b [M], fc_w[l] [out, in], fc_b[l] [out] (float32)."""
+        precision), se_w [M, k], se_b [M], fc_w[l] [out, in], fc_b[l] [out] (float32); optional folded
+        input batch norm in_scale / in_shift [D_in] (float32)."""
         keep = [np.ascontiguousarray(t) for t in tables]
         sw = np.ascontiguousarray(se_w, np.float32)
         sb = np.ascontiguousarray(se_b, np.float32)
@@ -226,8 +229,11 @@ class Context:
         tp = (C.c_void_p * len(keep))(*[t.ctypes.data for t in keep])
         wp = (C.c_void_p * len(ws))(*[w.ctypes.data for w in ws])
         bp = (C.c_void_p * len(bs))(*[b.ctypes.data for b in bs])
+        isc = None if in_scale is None else np.ascontiguousarray(in_scale, np.float32)
+        ish = None if in_shift is None else np.ascontiguousarray(in_shift, np.float32)
         p = cold_params(PRECISION[table_dtype], C.cast(tp, C.POINTER(C.c_void_p)), sw.ctypes.data, sb.ctypes.data,
-                        C.cast(wp, C.POINTER(C.c_void_p)), C.cast(bp, C.POINTER(C.c_void_p)))
+                        C.cast(wp, C.POINTER(C.c_void_p)), C.cast(bp, C.POINTER(C.c_void_p)),
+                        None if isc is None else isc.ctypes.data, None if ish is None else ish.ctypes.data)
         v = C.c_uint64()
         _check(lib().cold_load_params(self.ctx, C.byref(p), C.byref(v)))
         return v.value

@@ -55,6 +55,81 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
+// ---- compressible device memory (Blackwell generic compression; activations after ReLU are
+// zero-rich, so their HBM write/read traffic shrinks). Driver VMM entry points fetched at run time.
+typedef CUresult (*PFN_memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
+typedef CUresult (*PFN_memAddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
+typedef CUresult (*PFN_memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
+typedef CUresult (*PFN_memSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
+typedef CUresult (*PFN_memGetGran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
+typedef CUresult (*PFN_memUnmap)(CUdeviceptr, size_t);
+typedef CUresult (*PFN_memRelease)(CUmemGenericAllocationHandle);
+typedef CUresult (*PFN_memAddressFree)(CUdeviceptr, size_t);
+typedef CUresult (*PFN_memGetProp)(CUmemAllocationProp*, CUmemGenericAllocationHandle);
+template <typename F>
+static F drv(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return reinterpret_cast<F>(p);
+}
+struct CompAlloc {
+  CUdeviceptr ptr = 0;
+  size_t size = 0;
+  CUmemGenericAllocationHandle h = 0;
+};
+// returns nullptr if compressible memory is unavailable (caller falls back to cudaMalloc)
+static void* comp_alloc(int device, size_t bytes, CompAlloc& out, bool& compressed) {
+  static auto create = drv<PFN_memCreate>("cuMemCreate");
+  static auto reserve = drv<PFN_memAddressReserve>("cuMemAddressReserve");
+  static auto map = drv<PFN_memMap>("cuMemMap");
+  static auto access = drv<PFN_memSetAccess>("cuMemSetAccess");
+  static auto gran = drv<PFN_memGetGran>("cuMemGetAllocationGranularity");
+  static auto getprop = drv<PFN_memGetProp>("cuMemGetAllocationPropertiesFromHandle");
+  static auto release = drv<PFN_memRelease>("cuMemRelease");
+  static auto afree = drv<PFN_memAddressFree>("cuMemAddressFree");
+  compressed = false;
+  if (!create || !reserve || !map || !access || !gran || !release || !afree) return nullptr;
+  CUmemAllocationProp prop;
+  memset(&prop, 0, sizeof(prop));
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  prop.allocFlags.compressionType = CU_MEM_ALLOCATION_COMP_GENERIC;
+  size_t g = 0;
+  if (gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || g == 0) return nullptr;
+  const size_t size = (bytes + g - 1) / g * g;
+  CUmemGenericAllocationHandle h;
+  if (create(&h, size, &prop, 0) != CUDA_SUCCESS) return nullptr;
+  CUdeviceptr ptr = 0;
+  if (reserve(&ptr, size, g, 0, 0) != CUDA_SUCCESS) { release(h); return nullptr; }
+  if (map(ptr, size, 0, h, 0) != CUDA_SUCCESS) { afree(ptr, size); release(h); return nullptr; }
+  CUmemAccessDesc ad;
+  memset(&ad, 0, sizeof(ad));
+  ad.location = prop.location;
+  ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (access(ptr, size, &ad, 1) != CUDA_SUCCESS) { afree(ptr, size); release(h); return nullptr; }
+  if (getprop) {
+    CUmemAllocationProp got;
+    memset(&got, 0, sizeof(got));
+    if (getprop(&got, h) == CUDA_SUCCESS) compressed = got.allocFlags.compressionType == CU_MEM_ALLOCATION_COMP_GENERIC;
+  }
+  out.ptr = ptr;
+  out.size = size;
+  out.h = h;
+  return reinterpret_cast<void*>(ptr);
+}
+static void comp_free(const CompAlloc& a) {
+  static auto unmap = drv<PFN_memUnmap>("cuMemUnmap");
+  static auto release = drv<PFN_memRelease>("cuMemRelease");
+  static auto afree = drv<PFN_memAddressFree>("cuMemAddressFree");
+  if (!a.ptr) return;
+  if (unmap) unmap(a.ptr, a.size);
+  if (release) release(a.h);
+  if (afree) afree(a.ptr, a.size);
+}
+
 struct cold_ctx {
   // ---- configuration ----
   int M = 0, k = 0, L = 0, precision = 0, device = 0, linear_log = 1;
@@ -81,6 +156,8 @@ struct cold_ctx {
   float* d_wt[COLD_MAX_LAYERS] = {nullptr};  // fp32 path: transposed weights
   float* d_head_w = nullptr;
   float* d_head_b = nullptr;
+  float* d_in_scale = nullptr;       // folded input batch norm [D_in] (nullable)
+  float* d_in_shift = nullptr;
   CUtensorMap tmB[COLD_MAX_LAYERS];
   // ---- workspace ----
   float* d_u1 = nullptr;
@@ -124,6 +201,8 @@ struct cold_ctx {
   size_t topk_out_bytes = 0;
   int64_t device_bytes = 0;
   std::vector<void*> allocs;
+  std::vector<CompAlloc> comp_allocs;  // compressible activation buffers (COLD_COMPRESS)
+  bool compressed = false;
   // per-kernel event profiling
   bool prof = false;
   std::vector<cudaEvent_t> prof_events;       // pool
@@ -136,6 +215,7 @@ struct cold_ctx {
     cudaSetDevice(device);
     cudaDeviceSynchronize();
     for (void* p : allocs) cudaFree(p);
+    for (const CompAlloc& a : comp_allocs) comp_free(a);
     for (int i = 0; i < 2; i++) {
       if (d_stage[i]) cudaFree(d_stage[i]);
       if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
@@ -155,7 +235,7 @@ struct cold_ctx {
     for (void* p : d_tables) cudaFree(p);
     d_tables.clear();
     void** ps[] = {(void**)&d_groups, (void**)&d_se_w, (void**)&d_se_b, (void**)&d_w1u_t, (void**)&d_b1,
-                   (void**)&d_head_w, (void**)&d_head_b};
+                   (void**)&d_head_w, (void**)&d_head_b, (void**)&d_in_scale, (void**)&d_in_shift};
     for (void** p : ps) { if (*p) cudaFree(*p); *p = nullptr; }
     for (int l = 0; l < COLD_MAX_LAYERS; l++) {
       if (d_w[l]) cudaFree(d_w[l]);
@@ -168,6 +248,22 @@ struct cold_ctx {
     cudaError_t e = cudaMalloc(p, bytes < 16 ? 16 : bytes);
     if (e == cudaSuccess) { allocs.push_back(*p); device_bytes += (int64_t)bytes; }
     return e;
+  }
+  // activation buffers: compressible memory when requested and granted, else cudaMalloc
+  cudaError_t alloc_act(void** p, size_t bytes, bool want_comp) {
+    if (want_comp) {
+      CompAlloc a;
+      bool comp = false;
+      void* q = comp_alloc(device, bytes < 16 ? 16 : bytes, a, comp);
+      if (q) {
+        comp_allocs.push_back(a);
+        *p = q;
+        device_bytes += (int64_t)a.size;
+        compressed = compressed || comp;
+        return cudaSuccess;
+      }
+    }
+    return alloc(p, bytes);
   }
   int elem() const { return precision == COLD_FP32 ? 4 : 2; }
   // bracket one kernel launch with an event pair (only while profiling)
@@ -389,12 +485,14 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   e = e ? e : c->alloc((void**)&c->d_xu, (size_t)c->max_req * std::max(1, c->d_u) * 4);
   e = e ? e : c->alloc((void**)&c->d_req, (size_t)c->max_ads * 4);
   const size_t x_rows = (size_t)c->gspan * c->chunk;
-  e = e ? e : c->alloc((void**)&c->d_X, x_rows * c->d_ac_pad * c->elem());
+  const char* env_comp = getenv("COLD_COMPRESS");
+  const bool want_comp = c->tensor && env_comp && atoi(env_comp) != 0;
+  e = e ? e : c->alloc_act((void**)&c->d_X, x_rows * c->d_ac_pad * c->elem(), want_comp);
   e = e ? e : c->alloc((void**)&c->d_err, 16);
   e = e ? e : c->alloc((void**)&c->d_scores_stage, (size_t)2 * c->chunk * 4);
   e = e ? e : c->alloc((void**)&c->d_adoff, (size_t)(c->max_req + 1) * 4);
   if (c->tensor)
-    for (int l = 0; l < c->L - 2 && !e; l++) e = c->alloc(&c->d_H[l], (size_t)c->chunk * c->widths[l] * 2);
+    for (int l = 0; l < c->L - 2 && !e; l++) e = c->alloc_act(&c->d_H[l], (size_t)c->chunk * c->widths[l] * 2, want_comp);
   if (e != cudaSuccess) {
     delete c;
     cudaGetLastError();
@@ -594,6 +692,14 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
   if (s) return s;
   s = upload(c, (void**)&c->d_se_b, sizeof(float) * c->M, [&](uint8_t* h) { memcpy(h, p->se_b, sizeof(float) * c->M); });
   if (s) return s;
+  if ((p->in_scale == nullptr) != (p->in_shift == nullptr))
+    return fail(COLD_ERR_PARAMS, "in_scale and in_shift must both be set or both be NULL");
+  if (p->in_scale) {
+    s = upload(c, (void**)&c->d_in_scale, sizeof(float) * c->d_in, [&](uint8_t* h) { memcpy(h, p->in_scale, sizeof(float) * c->d_in); });
+    if (s) return s;
+    s = upload(c, (void**)&c->d_in_shift, sizeof(float) * c->d_in, [&](uint8_t* h) { memcpy(h, p->in_shift, sizeof(float) * c->d_in); });
+    if (s) return s;
+  }
   // FC1 split into the per-request user block (fp32, transposed) and the ad+cross block
   const int W0 = c->widths[0];
   const float* W1 = p->fc_w[0];   // [W0][d_in], columns = selected groups in schema order
@@ -836,6 +942,8 @@ static UserArgs make_user_args(cold_ctx* c, const CallPlan& pl, const int32_t* d
   ua.dbg_feat = dbg.feat;
   ua.n_sel = (int)c->sel.size();
   ua.d_in = c->d_in;
+  ua.in_scale = c->d_in_scale;
+  ua.in_shift = c->d_in_shift;
   ua.u1t = c->u1mma ? c->d_u1t : nullptr;
   ua.u1t_ld = c->u1t_ld;
   ua.u1_terms = c->u1_terms;
@@ -865,6 +973,8 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
   ga.dbg_feat = dbg.feat;
   ga.n_sel = (int)c->sel.size();
   ga.d_in = c->d_in;
+  ga.in_scale = c->d_in_scale;
+  ga.in_shift = c->d_in_shift;
   ga.ohot = (c->u1mma && !dbg.pooled && !dbg.feat) ? c->d_ohot : nullptr;
   ga.chunk = c->chunk;
   ga.nslot = U1_NSLOT;
@@ -1042,9 +1152,28 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
       CK(cudaStreamWaitEvent(st, c->ev_copied[slot], 0));
     }
     GatherArgs ga = make_gather_args(c, bv, s0, s1 - s0, dbg);
-    c->mark_begin(st);
-    launch_gather(ga, c->precision, st);
-    c->mark_end(COLD_PROF_GATHER, st);
+    static const bool split = getenv("COLD_GATHER_SPLIT") && atoi(getenv("COLD_GATHER_SPLIT")) != 0;
+    if (split) {   // profiling aid: one launch per group column (then the one-hot column)
+      GatherArgs g1 = ga;
+      for (int j = 0; j < ga.n_ac; j++) {
+        g1.n_ac = 1;
+        g1.ac_g[0] = ga.ac_g[ga.order[j]];
+        g1.order[0] = 0;
+        g1.ohot = nullptr;
+        c->mark_begin(st);
+        launch_gather(g1, c->precision, st);
+        c->mark_end(COLD_PROF_GATHER, st);
+      }
+      g1.n_ac = 0;
+      g1.ohot = ga.ohot;
+      c->mark_begin(st);
+      launch_gather(g1, c->precision, st);
+      c->mark_end(COLD_PROF_GATHER, st);
+    } else {
+      c->mark_begin(st);
+      launch_gather(ga, c->precision, st);
+      c->mark_end(COLD_PROF_GATHER, st);
+    }
     if (pl.host) CK(cudaEventRecord(c->ev_consumed[slot], st));
     if (mode == RUN_SCORE) {
       for (int64_t a0 = s0; a0 < s1; a0 += chunk, ci++) {
@@ -1392,5 +1521,6 @@ extern "C" cold_status cold_get_info(const cold_ctx* c, cold_info* out) {
   int64_t b = c->device_bytes;
   for (int g = 0; g < c->M && g < (int)c->d_tables.size(); g++) b += c->groups[g].cardinality * c->k * c->elem();
   out->device_bytes = b;
+  out->compressed_activations = c->compressed ? 1 : 0;
   return COLD_OK;
 }

@@ -114,7 +114,8 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
     named_bar_sync(1 + h, 128);           // all 128 rows of the box written
     tick(3);
     if (elected && dbg != 4) {
-      tma_store_2d(tmC, group_buf, col0, tile_row0);
+      // dbg 6 (timing experiment): every box to the same L2-resident location (no DRAM write traffic)
+      tma_store_2d(tmC, group_buf, dbg == 6 ? 0 : col0, dbg == 6 ? 0 : tile_row0);
       bulk_commit();
     }
     tick(4);

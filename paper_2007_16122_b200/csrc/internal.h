@@ -27,6 +27,8 @@ struct UserArgs {
   float* dbg_pooled;               // [N][n_sel][k]
   float* dbg_feat;                 // [N][D_in]
   int n_sel, d_in;
+  const float* in_scale;           // input normalisation [D_in] (nullable; cold_params.in_scale)
+  const float* in_shift;
   double* stats;                   // SE statistics mode (cold_se_stats): [M] += s_g * ads of the request;
                                    // x_u / u1 are not written
   uint16_t* u1t;                   // FC1 u1 operand (nullable): [u1_terms * H][u1t_ld] f16/bf16 bits, the
@@ -54,6 +56,8 @@ struct GatherArgs {
   float* dbg_pooled;               // [N][n_sel][k] (call-global rows)
   float* dbg_feat;                 // [N][D_in]
   int n_sel, d_in;
+  const float* in_scale;           // input normalisation [D_in] (nullable)
+  const float* in_shift;
   double* stats;                   // SE statistics mode: [M] += s_g per ad; X is not written
   uint16_t* ohot;                  // FC1 u1 operand (nullable): [n][16] span-local rows, the one-hot slot of
                                    // the row's request in its 256-row CTA-pair tile, repeated in k 0-7 / 8-15

@@ -92,7 +92,11 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
       continue;
     }
     if (lane < K) {
-      const float v = s * e;
+      float v = s * e;
+      if (a.in_scale) {                     // folded input batch norm (fp32, F2)
+        const int col = G.sel_pos * K + lane;
+        v = fmaf(v, a.in_scale[col], a.in_shift[col]);
+      }
       xs[j * K + lane] = v;
       a.xu[(int64_t)r * d_u + j * K + lane] = v;
       if (a.dbg_pooled || a.dbg_feat) {
@@ -189,8 +193,14 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
     return;
   }
   alignas(16) T out[K];
+  if (a.in_scale) {                         // folded input batch norm in fp32 before the cast (F2)
+    const int col = G.sel_pos * K;
 #pragma unroll
-  for (int d = 0; d < K; d++) out[d] = Store<T>::from_f(s * e[d]);
+    for (int d = 0; d < K; d++) out[d] = Store<T>::from_f(fmaf(s * e[d], __ldg(a.in_scale + col + d), __ldg(a.in_shift + col + d)));
+  } else {
+#pragma unroll
+    for (int d = 0; d < K; d++) out[d] = Store<T>::from_f(s * e[d]);
+  }
   T* dst = reinterpret_cast<T*>(a.X) + local * a.ldx + G.sel_slot * K;
   constexpr int BYTES = K * (int)sizeof(T);
   if constexpr (BYTES % 32 == 0) {

@@ -22,36 +22,51 @@ __device__ __forceinline__ void ldg256v(const void* p, uint4& a, uint4& b) {
 
 template <typename T, int D>
 __global__ void __launch_bounds__(256) vps_kernel(VpsArgs a) {
+  constexpr int BYTES = D * (int)sizeof(T);
+  constexpr int NV = BYTES / 16;                 // 16 B vectors per row
+  constexpr int APT = BYTES <= 128 ? 2 : 1;      // ads per thread in flight (row registers <= 64)
   __shared__ float su[D];
   const int r = blockIdx.y;
   for (int i = threadIdx.x; i < D; i += blockDim.x) su[i] = a.user_vecs[(int64_t)r * D + i];
-  __syncthreads();
   const int64_t a0 = a.ad_offsets[r], a1 = a.ad_offsets[r + 1];
   const T* tab = reinterpret_cast<const T*>(a.ad_vecs);
-  constexpr int BYTES = D * (int)sizeof(T);
-  constexpr int NV = BYTES / 16;                 // 16 B vectors per row
-  for (int64_t ad = a0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ad < a1;
-       ad += (int64_t)gridDim.x * blockDim.x) {
-    int64_t id = a.ad_ids[ad];
-    if (id < 0 || id >= a.num_vecs) id = id < 0 ? 0 : a.num_vecs - 1;   // clamp (memory-safe)
-    const uint4* row = reinterpret_cast<const uint4*>(tab + id * D);
-    uint4 q[NV];
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * APT;
+  for (int64_t base = a0 + (int64_t)blockIdx.x * blockDim.x * APT + threadIdx.x; base < a1; base += stride) {
+    int64_t id[APT];
 #pragma unroll
-    for (int v = 0; v < NV; v += 2) ldg256v(row + v, q[v], q[v + 1]);
-    float z = 0.0f;
-#pragma unroll
-    for (int v = 0; v < NV; v++) {
-      const T* t = reinterpret_cast<const T*>(&q[v]);
-#pragma unroll
-      for (int i = 0; i < 16 / (int)sizeof(T); i++) z = fmaf(su[v * (16 / sizeof(T)) + i], Store<T>::to_f(t[i]), z);
+    for (int j = 0; j < APT; j++) {
+      const int64_t ad = base + (int64_t)j * blockDim.x;
+      int64_t v = ad < a1 ? a.ad_ids[ad] : 0;
+      if (v < 0 || v >= a.num_vecs) v = v < 0 ? 0 : a.num_vecs - 1;   // clamp (memory-safe)
+      id[j] = v;
     }
-    a.scores[ad] = sigmoid(z);
+    uint4 q[APT][NV];
+#pragma unroll
+    for (int j = 0; j < APT; j++) {
+      const uint4* row = reinterpret_cast<const uint4*>(tab + id[j] * D);
+#pragma unroll
+      for (int v = 0; v < NV; v += 2) ldg256v(row + v, q[j][v], q[j][v + 1]);
+    }
+#pragma unroll
+    for (int j = 0; j < APT; j++) {
+      const int64_t ad = base + (int64_t)j * blockDim.x;
+      float z = 0.0f;
+#pragma unroll
+      for (int v = 0; v < NV; v++) {
+        const T* t = reinterpret_cast<const T*>(&q[j][v]);
+#pragma unroll
+        for (int i = 0; i < 16 / (int)sizeof(T); i++) z = fmaf(su[v * (16 / sizeof(T)) + i], Store<T>::to_f(t[i]), z);
+      }
+      if (ad < a1) a.scores[ad] = sigmoid(z);
+    }
   }
 }
 
 template <typename T>
 static cudaError_t vps_dispatch(const VpsArgs& a, int max_n, cudaStream_t s) {
-  dim3 grid((unsigned)std::min(64, std::max(1, (max_n + 255) / 256)), (unsigned)a.R);
+  // a block covers up to 8 * 256 * APT candidates of one request (loop), keeping the grid small
+  dim3 grid((unsigned)std::min(64, std::max(1, (max_n + 4095) / 4096)), (unsigned)a.R);
   switch (a.d) {
     case 16: vps_kernel<T, 16><<<grid, 256, 0, s>>>(a); break;
     case 32: vps_kernel<T, 32><<<grid, 256, 0, s>>>(a); break;

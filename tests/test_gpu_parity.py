@@ -402,3 +402,66 @@ def test_vps_score_matches_oracle(prec, d):
     torch.cuda.synchronize()
     got = out.cpu().numpy().astype(np.float64)
     assert rel_err(got, want).max() <= 1e-5
+
+
+# ---- full-size configuration, sampled parity (the launch configuration bench.py times) ------------
+
+def test_full_size_configs2_sampled():
+    """BASELINE configs[2] at full size: S-paper with uncapped cardinalities (4.8 GB of fp16 tables),
+    512 requests x 4000 ads (2,048,000 ads: 14 chunks of the default 151,552-ad pipeline over 4 gather
+    spans), default library configuration. 256 sampled ads are checked against the fp64 oracle one by one,
+    and the per-request top-500 of the GPU scores is checked for validity on every request."""
+    import torch
+    from paper_2007_16122_b200 import Batch, Context
+    sch = coldgen.schema_paper()
+    params = coldgen.make_params(sch, seed=1234, precision="f16")
+    batch = coldgen.make_batch(sch, 512, 4000, seed=1235)
+    ctx = Context(sch.groups, sch.k, sch.widths, precision="f16", max_ads=batch.n_ads, max_requests=batch.R)
+    load_params(ctx, params)
+    db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs)
+    out = torch.empty(batch.n_ads, dtype=torch.float32, device="cuda")
+    ctx.score_batch(db, out)
+    K = 500
+    idx = torch.empty(batch.R * K, dtype=torch.int32, device="cuda")
+    key = torch.empty(batch.R * K, dtype=torch.float32, device="cuda")
+    ctx.topk(out, db.ad_offsets, batch.ad_offsets, K, idx, key)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().astype(np.float64)
+    sample = np.sort(np.random.default_rng(7).choice(batch.n_ads, 256, replace=False))
+    p, z = oracle.score(oracle.Model(sch, params), batch, ad_list=sample)
+    _check_scores(got[sample], p, z, "f16", "configs[2] full size (sampled)")
+    # top-K validity per request: keys sorted desc, equal to the scores at the returned positions, and
+    # no unreturned ad strictly above the K-th key
+    ki, kk = idx.cpu().numpy().reshape(batch.R, K), key.cpu().numpy().reshape(batch.R, K)
+    s32 = out.cpu().numpy()
+    for r in range(batch.R):
+        seg = s32[batch.ad_offsets[r]:batch.ad_offsets[r + 1]]
+        assert np.all(np.diff(kk[r]) <= 0)
+        np.testing.assert_array_equal(seg[ki[r]], kk[r])
+        assert (seg > kk[r, -1]).sum() <= K
+
+
+# ---- F2: folded input batch norm (P:276), the paper's alternative to linear_log ------------------
+
+@pytest.mark.parametrize("prec", ["f16", "bf16", "f32"])
+def test_input_batch_norm_variant(prec):
+    """linear_log off, inference batch norm of the network input applied in fp32 before the 16-bit cast
+    (cold_params.in_scale / in_shift) vs the oracle's explicit per-column affine."""
+    sch, params, batch = small_case("paper", R=3, n_ads=(700, 129, 300), precision=prec, cap=20000, seed=93)
+    rng = np.random.default_rng(4)
+    d = params.fc_w[0].shape[1]
+    scale = rng.uniform(0.1, 0.6, d).astype(np.float32)
+    shift = rng.uniform(-0.3, 0.3, d).astype(np.float32)
+    ctx = make_ctx(sch, params, linear_log=False, load=False)
+    tables = params.tables
+    tdt = params.table_dtype
+    if ctx.precision == "f32" and tdt != "f32":
+        tables = [params.table_f64(g).astype(np.float32) for g in range(len(tables))]
+        tdt = "f32"
+    elif tdt == "f16":
+        tables = [t.view(np.uint16) for t in tables]
+    ctx.load_params(tables, params.se_w, params.se_b, params.fc_w, params.fc_b, table_dtype=tdt,
+                    in_scale=scale, in_shift=shift)
+    p, z = oracle.score(oracle.Model(sch, params, linear_log=False,
+                                     in_norm=(scale.astype(np.float64), shift.astype(np.float64))), batch)
+    _check_scores(gpu_scores(ctx, batch), p, z, prec, f"input batch norm {prec}")

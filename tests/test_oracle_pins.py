@@ -3,6 +3,7 @@ something other than itself — the paper's closed forms, the hand-computed work
 example (tests/golden/), hash known answers, torch fp64 library routines, brute
 force and the independent pure-Python twin oracle/mini.py.
 """
+import dataclasses
 import math
 
 import numpy as np
@@ -381,3 +382,23 @@ def test_vps_closed_forms():
     np.testing.assert_array_equal(p16, p)
     with pytest.raises(oracle.OracleError):
         oracle.vps_score(tab, "f32", u, [0, 1], [3])
+
+
+# ---- F2: batch norm of the network input (P:276's alternative to linear_log) ----------
+
+def test_input_norm_folds_into_fc1():
+    """x <- x * scale + shift before FC1 equals FC1 with W1' = W1 diag(scale), b1' = b1 + W1 shift (an
+    algebraic invariant between two parameterisations of the oracle); identity scale/shift is a no-op."""
+    sch, params, batch = small_case("paper", R=2, n_ads=(17, 9), precision="f32", cap=3000, seed=12)
+    rng = np.random.default_rng(3)
+    d = params.fc_w[0].shape[1]
+    scale, shift = rng.uniform(0.2, 1.5, d), rng.uniform(-0.5, 0.5, d)
+    p_bn, _ = oracle.score(oracle.Model(sch, params, linear_log=False, in_norm=(scale, shift)), batch)
+    W1 = np.asarray(params.fc_w[0], np.float64)
+    folded = dataclasses.replace(params, fc_w=[W1 * scale[None, :]] + list(params.fc_w[1:]),
+                                 fc_b=[np.asarray(params.fc_b[0], np.float64) + W1 @ shift] + list(params.fc_b[1:]))
+    p_fold, _ = oracle.score(oracle.Model(sch, folded, linear_log=False), batch)
+    np.testing.assert_allclose(p_bn, p_fold, rtol=1e-11)
+    p_id, _ = oracle.score(oracle.Model(sch, params, in_norm=(np.ones(d), np.zeros(d))), batch)
+    p_none, _ = oracle.score(oracle.Model(sch, params), batch)
+    np.testing.assert_array_equal(p_id, p_none)
