@@ -168,6 +168,7 @@ struct cold_ctx {
   CUtensorMap tmA[COLD_MAX_LAYERS];
   std::vector<CUtensorMap> tmAX;     // layer-0 A maps, one per chunk slot of the gather span
   bool u1mma = false;                // FC1 adds u1[request(row)] on the tensor core (kernels_gemm2.cu)
+  bool chain = false;                // FC1 -> FC3 in one persistent kernel over 256-row blocks
   int u1_terms = 0, u1t_ld = 0;
   uint16_t* d_u1t = nullptr;         // [u1_terms * H][u1t_ld] 16-bit terms of u1 (written by user_kernel)
   uint16_t* d_ohot = nullptr;        // [gspan * chunk][16] one-hot u1 operand rows (written by gather)
@@ -574,6 +575,11 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       s = make_tmap_plain(&c->tmOH[j], c->d_ohot + (size_t)j * c->chunk * 16, c->precision, 16, c->chunk, 128, 8);
       if (s) { delete c; return s; }
     }
+  }
+  if (c->u1mma && c->tail_mode == 2 && c->L == 6 && c->pair[1] && c->pair[2] &&
+      chain_supported(c->widths[0], c->widths[1], c->widths[2], c->d_ac_pad)) {
+    const char* env_chain = getenv("COLD_CHAIN");
+    c->chain = !(env_chain && atoi(env_chain) == 0);
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
@@ -1011,7 +1017,29 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     c->mark_end(COLD_PROF_FC, st);
     return;
   }
-  const int n_gemm = c->L - 1 - c->n_tail;
+  int n_gemm = c->L - 1 - c->n_tail;
+  if (c->chain) {   // FC1..FC3 in one launch (kernels_chain.cu), then the FC4/FC5/head tail below
+    ChainParams cp;
+    memset(&cp, 0, sizeof(cp));
+    cp.b2 = c->d_b[1];
+    cp.b3 = c->d_b[2];
+    cp.u1 = c->d_u1;
+    cp.ld_u1 = c->widths[0];
+    cp.req_of_ad = c->d_req;
+    cp.a0 = a0;
+    cp.n1 = c->widths[0];
+    cp.n2 = c->widths[1];
+    cp.n3 = c->widths[2];
+    cp.k1 = c->d_ac_pad;
+    cp.h1 = c->d_H[0];
+    cp.h2 = c->d_H[1];
+    const CUtensorMap* tm[9] = {&c->tmAX[xslot], &c->tmB[0], &c->tmB[1], &c->tmB[2], &c->tmC[0], &c->tmC[1],
+                                &c->tmC[2], &c->tmOH[xslot], &c->tmU1T};
+    c->mark_begin(st);
+    launch_chain(tm, (int)n, c->precision == COLD_BF16 ? 1 : 0, cp, c->num_sms, c->pdl && !c->prof, st);
+    c->mark_end(COLD_PROF_FC, st);
+    n_gemm = 0;
+  }
   static bool instr_on = getenv("COLD_INSTR") != nullptr;
   if (instr_on && !g_instr) {
     cudaMalloc(&g_instr, 8 * 8 * COLD_MAX_LAYERS);

@@ -140,6 +140,19 @@ cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const 
                         const CUtensorMap* tmB5, int M, int K3, int bf16, const TailParams& tp, int num_sms, bool pdl,
                         cudaStream_t s);
 
+// FC1 -> FC2 -> FC3 in one persistent CTA-pair kernel over 256-row blocks (kernels_chain.cu)
+struct ChainParams {
+  const float* b2; const float* b3;      // FC2 / FC3 biases (FC1's bias is inside u1)
+  const float* u1; int ld_u1;            // FC1 fallback for blocks spanning > U1_NSLOT requests
+  const int32_t* req_of_ad; int64_t a0;
+  int n1, n2, n3, k1;                    // widths of FC1..FC3 and FC1's K (D_ac_pad)
+  const void* h1; const void* h2;        // H1 / H2 chunk buffers (for the L2 discards)
+};
+bool chain_supported(int n1, int n2, int n3, int k1);
+// tm: X (slot), W1, W2, W3, H1, H2, H3, one-hot (slot), u1 terms
+cudaError_t launch_chain(const CUtensorMap* tm[9], int M, int bf16, const ChainParams& cp, int num_sms, bool pdl,
+                         cudaStream_t s);
+
 // fused FC(L-3) .. FC(L-2) + head after a GEMM FC(L-4) (paper widths 128, 64 -> 2), resident weights
 bool tail45_supported(int n4, int n5, int k4);
 cudaError_t launch_tail45(const CUtensorMap* tmA4, const CUtensorMap* tmB4, const CUtensorMap* tmB5, int M, int bf16,

@@ -1,0 +1,285 @@
+// kernels_chain.cu — FC1 -> FC2 -> FC3 of the COLD stack (§4.1: D_in x 1024 x 512 x 256 ..)
+// in ONE persistent CTA-pair kernel that walks 256-row blocks, so the activations H1 / H2 of a block are
+// consumed while they are still in L2 and are then discarded instead of being written back.
+//
+// Why: the layer-by-layer launches wrote 310 + 155 MB of H1 / H2 per 151,552-ad chunk and read them
+// back, and B200's pure-write bandwidth is 3.9 TB/s (measured): those round trips, not the tensor
+// cores, bounded FC1 (~110 us per chunk, epilogue-bound) and slowed the kernels after it.
+//
+// A pair owns row blocks rb = pair, pair + npairs, ... For its j-th block it runs, in this order,
+//   step j: FC1(j) n-tiles 0..3 | FC3(j-1) | FC2(j) n-tiles 0..1
+// FC2(j) needs all of H1(j) (K = 1024) and FC3(j-1) all of H2(j-1) (K = 512); every row of them was
+// written by this CTA's own epilogue (A is M-split across the pair), so the dependency is local: the
+// epilogue warps arrive on hready[0] / hready[1] once their TMA stores of the block's last tile of
+// FC1 / FC2 have completed, and the producer waits there before loading the block as an A operand.
+// FC3(j-1) sits between FC1(j) and FC2(j) so the tensor pipe has work while H1(j) drains.
+// After FC2(j) (resp. FC3(j-1)) has consumed H1(j) (H2(j-1)), the epilogue issues
+// discard.global.L2 on the CTA's rows of that block: the lines are dead, so L2 drops them without a
+// write-back. H3 is written for the tail kernel (FC4 / FC5 / head).
+//
+// Per tile the machinery is gemm_pair_kernel's: TMA producer (warp 0), leader MMA issuer (warp 1),
+// 8 epilogue warps (2..9) with double-buffered TMEM accumulators and group TMA stores (epi.cuh), and
+// FC1's u1[request(row)] added by one extra K = 16 MMA from the one-hot / u1-term operands (D-4).
+#include <cuda.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+#include "epi.cuh"
+#include "pair.cuh"
+
+namespace cold {
+
+constexpr int C_BN = 256;
+constexpr int C_EPI_WARPS = 8;
+constexpr int C_THREADS = 64 + 32 * C_EPI_WARPS;
+constexpr int C_A_BYTES = BM * BK * 2;                 // 16 KB: own 128 rows x 64 K
+constexpr int C_B_BYTES = (C_BN / 2) * BK * 2;         // 16 KB: own half of the 256-row weight tile
+constexpr int C_STAGE_BYTES = C_A_BYTES + C_B_BYTES;
+constexpr int C_OUT_BYTES = 2 * EPI_GROUP_BOX;          // two 4-warp groups x 16 KB
+constexpr int C_UXA = BM * 32, C_UXB = (C_BN / 2) * 16 * 4, C_UX_BUF = C_UXA + C_UXB, C_NUX = 2;
+constexpr int C_STAGES = (232448 - C_OUT_BYTES - C_NUX * C_UX_BUF - 1024 - 512) / C_STAGE_BYTES;
+constexpr int C_SMEM = C_STAGES * C_STAGE_BYTES + C_OUT_BYTES + C_NUX * C_UX_BUF + 1024 + 512;
+static_assert(C_STAGES >= 4, "chain kernel pipeline depth");
+
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+template <bool BF16>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
+    chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
+                 const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmW3,
+                 const __grid_constant__ CUtensorMap tmH1, const __grid_constant__ CUtensorMap tmH2,
+                 const __grid_constant__ CUtensorMap tmH3, const __grid_constant__ CUtensorMap tmOH,
+                 const __grid_constant__ CUtensorMap tmU1T, int M, ChainParams cp) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = sA + C_STAGES * C_A_BYTES;
+  uint8_t* sOut = smem + C_STAGES * C_STAGE_BYTES;
+  uint8_t* sUX = sOut + C_OUT_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sUX + C_NUX * C_UX_BUF);
+  uint64_t* full = bars;                          // leader: A+B bytes of both CTAs
+  uint64_t* empty = full + C_STAGES;              // both: released by the leader's pair commit
+  uint64_t* tfull = empty + C_STAGES;             // both: accumulator ready [2]
+  uint64_t* tempty = tfull + 2;                   // leader: both CTAs' epilogues drained [2]
+  uint64_t* uxfull = tempty + 2;                  // leader: u1 operand landed [C_NUX]
+  uint64_t* uxempty = uxfull + C_NUX;             // both: u1 MMA of the buffer's last FC1 tile done [C_NUX]
+  uint64_t* hready = uxempty + C_NUX;             // local: [0] H1 block stored, [1] H2 block stored
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hready + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair = (int)cluster_id_x(), npairs = (int)num_clusters_x();
+  const int num_pm = (M + 2 * BM - 1) / (2 * BM);
+  const int nrb = pair < num_pm ? (num_pm - 1 - pair) / npairs + 1 : 0;   // this pair's row blocks
+  const int n_[3] = {cp.n1, cp.n2, cp.n3};
+  const int kbs[3] = {cp.k1 / BK, cp.n1 / BK, cp.n2 / BK};
+  const CUtensorMap* tA[3] = {&tmX, &tmH1, &tmH2};
+  const CUtensorMap* tB[3] = {&tmW1, &tmW2, &tmW3};
+  const CUtensorMap* tC[3] = {&tmH1, &tmH2, &tmH3};
+  const int ntile[3] = {cp.n1 / C_BN, cp.n2 / C_BN, cp.n3 / C_BN};
+
+  // the per-pair task order (all roles walk it identically): step s = 0..nrb:
+  //   FC1(s) n-tiles | FC3(s-1) | FC2(s) n-tiles
+  auto for_tasks = [&](auto&& f) {
+    for (int s = 0; s <= nrb; s++) {
+      if (s < nrb) for (int nb = 0; nb < ntile[0]; nb++) f(0, s, nb);
+      if (s >= 1) for (int nb = 0; nb < ntile[2]; nb++) f(2, s - 1, nb);
+      if (s < nrb) for (int nb = 0; nb < ntile[1]; nb++) f(1, s, nb);
+    }
+  };
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C_STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; s++) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * C_EPI_WARPS); }
+    for (int s = 0; s < C_NUX; s++) { mbar_init(&uxfull[s], 1); mbar_init(&uxempty[s], 1); }
+    mbar_init(&hready[0], C_EPI_WARPS);
+    mbar_init(&hready[1], C_EPI_WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const CUtensorMap* maps[9] = {&tmX, &tmW1, &tmW2, &tmW3, &tmH1, &tmH2, &tmH3, &tmOH, &tmU1T};
+    for (int i = 0; i < 9; i++) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)maps[i]) : "memory");
+  }
+  if (BF16 && warp == 2) {   // bf16: the 4th K chunk of every B_x buffer stays zero
+    for (int b = 0; b < C_NUX; b++)
+      for (int i = lane; i < C_BN / 2; i += 32)
+        sts128(smem_u32(sUX + b * C_UX_BUF + C_UXA + 3 * (C_BN / 2) * 16 + i * 16), make_uint4(0, 0, 0, 0));
+    fence_async_smem();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * C_BN)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer (both CTAs) =====
+      constexpr int TERMS = BF16 ? 3 : 2;
+      const uint64_t pol_x = policy_evict_first();  // X: read once
+      const uint64_t pol_a = policy_evict_last();   // H1 / H2: read while hot, then discarded
+      const uint64_t pol_b = policy_evict_last();   // weights: re-read by every block
+      int s = 0, fc1_t = 0;
+      uint32_t ph = 0;
+      for_tasks([&](int l, int j, int nb) {
+        const int pm = pair + j * npairs;
+        const int mrow = pm * 2 * BM + (int)rank * BM;
+        if (l > 0 && nb == 0) mbar_wait(&hready[l - 1], (uint32_t)(j & 1));   // own rows of the input block
+        for (int kb = 0; kb < kbs[l]; kb++) {
+          mbar_wait(&empty[s], ph ^ 1);
+          if (leader) mbar_expect_tx(&full[s], 2 * C_STAGE_BYTES);
+          tma_load_2d_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb * BK, mrow, l == 0 ? pol_x : pol_a);
+          tma_load_2d_pair(sB + s * C_B_BYTES, tB[l], &full[s], kb * BK, nb * C_BN + (int)rank * (C_BN / 2), pol_b);
+          if (++s == C_STAGES) { s = 0; ph ^= 1; }
+        }
+        if (l == 0) {   // FC1: the tile's u1 operand (one-hot rows + u1-term columns)
+          const int b = fc1_t % C_NUX;
+          mbar_wait(&uxempty[b], ((fc1_t / C_NUX) & 1) ^ 1);
+          const int r_first = cp.req_of_ad[cp.a0 + pm * 2 * BM] & ~7;
+          uint8_t* ux = sUX + b * C_UX_BUF;
+          if (leader) mbar_expect_tx(&uxfull[b], 2 * (C_UXA + TERMS * (C_BN / 2) * 16));
+          tma_load_2d_pair(ux, &tmOH, &uxfull[b], 0, mrow, pol_x);
+          tma_load_2d_pair(ux + BM * 16, &tmOH, &uxfull[b], 8, mrow, pol_x);
+          const int n0 = nb * C_BN + (int)rank * (C_BN / 2);
+#pragma unroll
+          for (int t = 0; t < TERMS; t++)
+            tma_load_2d_pair(ux + C_UXA + t * (C_BN / 2) * 16, &tmU1T, &uxfull[b], r_first, t * cp.n1 + n0, pol_b);
+          fc1_t++;
+        }
+      });
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ===== MMA issuer (leader only) =====
+      constexpr uint32_t idesc = idesc_pair<C_BN, BF16>();
+      int s = 0, lt = 0, fc1_t = 0;
+      uint32_t ph = 0;
+      for_tasks([&](int l, int j, int nb) {
+        const int acc = lt & 1;
+        mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * C_BN;
+        for (int kb = 0; kb < kbs[l]; kb++) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t ad = sdesc_sw128(smem_u32(sA + s * C_A_BYTES));
+          const uint64_t bd = sdesc_sw128(smem_u32(sB + s * C_B_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < BK / UMMA_K; kk++)
+            umma_f16_pair(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+          umma_commit_pair(&empty[s]);
+          if (++s == C_STAGES) { s = 0; ph ^= 1; }
+        }
+        if (l == 0) {   // D += A_x B_x^T = u1[request(row)][n]
+          const int b = fc1_t % C_NUX;
+          mbar_wait(&uxfull[b], (fc1_t / C_NUX) & 1);
+          tc_fence_after();
+          const uint32_t ux = smem_u32(sUX + b * C_UX_BUF);
+          const uint64_t adx = sdesc_k16_plain(ux);
+          umma_f16_pair(d, adx, sdesc_k16_plain(ux + C_UXA), idesc, 1u);
+          if (BF16) umma_f16_pair(d, adx, sdesc_k16_plain(ux + C_UXA + 2 * (C_BN / 2) * 16), idesc, 1u);
+          umma_commit_pair(&uxempty[b]);
+          fc1_t++;
+        }
+        umma_commit_pair(&tfull[acc]);
+        lt++;
+      });
+    }
+  } else {
+    // ===== epilogue warps 2..9 (both CTAs): TMEM lane quadrant q, column half h =====
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int h = ew >> 2;
+    const bool elected = (q == 0) && (lane == 0);
+    int lt = 0;
+    for_tasks([&](int l, int j, int nb) {
+      const int pm = pair + j * npairs;
+      const int acc = lt & 1;
+      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      tc_fence_after();
+      const int trow0 = pm * 2 * BM + (int)rank * BM;   // this CTA's first row of the block
+      const int row = trow0 + q * 32 + lane;
+      const float* u1row = nullptr;   // FC1 fallback: the pair block spans more than U1_NSLOT requests
+      if (l == 0) {
+        const int t0 = pm * 2 * BM;
+        if (cp.req_of_ad[cp.a0 + min(t0 + 2 * BM, M) - 1] - (cp.req_of_ad[cp.a0 + t0] & ~7) >= U1_NSLOT) {
+          const int req = row < M ? cp.req_of_ad[cp.a0 + row] : 0;
+          u1row = cp.u1 + (int64_t)req * cp.ld_u1 + nb * C_BN;
+        }
+      }
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C_BN);
+      epi_store_wide<BF16>(tbase, h * (C_BN / 2), (h + 1) * (C_BN / 2), l == 1 ? cp.b2 : (l == 2 ? cp.b3 : nullptr),
+                           0u, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l], nb * C_BN, trow0, q, h, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
+      lt++;
+      const bool last_of_layer = nb == ntile[l] - 1;
+      if (l < 2 && last_of_layer) {
+        // the block's rows of this layer are stored once this group's bulk stores completed
+        if (elected) {
+          bulk_wait_all();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        named_bar_sync(1 + h, 128);
+        if (lane == 0) mbar_arrive(&hready[l]);
+      }
+      if (l >= 1 && last_of_layer) {
+        // the input of this layer for the block (H1 for FC2, H2 for FC3) has been consumed by the MMAs
+        // (tfull of the last tile): drop this CTA's rows from L2 without write-back
+        const uint8_t* base = reinterpret_cast<const uint8_t*>(l == 1 ? cp.h1 : cp.h2);
+        const int ld = (l == 1 ? cp.n1 : cp.n2) * 2;           // bytes per row
+        const int lines = ld / 128;
+        const int rows = min(BM, M - trow0);
+        for (int i = (ew * 32 + lane); i < rows * lines; i += C_EPI_WARPS * 32)
+          discard_l2(base + (int64_t)(trow0 + i / lines) * ld + (i % lines) * 128);
+      }
+    });
+    if (elected) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * C_BN) : "memory");
+  }
+}
+
+bool chain_supported(int n1, int n2, int n3, int k1) {
+  return n1 % C_BN == 0 && n2 % C_BN == 0 && n3 % C_BN == 0 && k1 % BK == 0 && n1 / BK >= 1;
+}
+
+cudaError_t launch_chain(const CUtensorMap* tm[9], int M, int bf16, const ChainParams& cp, int num_sms, bool pdl,
+                         cudaStream_t s) {
+  if (M <= 0) return cudaSuccess;
+  auto kern = bf16 ? chain_kernel<true> : chain_kernel<false>;
+  static bool attr[2] = {false, false};
+  if (!attr[bf16 ? 1 : 0]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_SMEM);
+    attr[bf16 ? 1 : 0] = true;
+  }
+  const int num_pm = (M + 2 * BM - 1) / (2 * BM);
+  const int pairs = num_pm < num_sms / 2 ? num_pm : num_sms / 2;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(C_THREADS);
+  cfg.dynamicSmemBytes = C_SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, *tm[0], *tm[1], *tm[2], *tm[3], *tm[4], *tm[5], *tm[6], *tm[7], *tm[8], M,
+                            cp);
+}
+
+}  // namespace cold

@@ -30,6 +30,7 @@
 #include "internal.h"
 #include "ptx.cuh"
 #include "epi.cuh"
+#include "pair.cuh"
 
 namespace cold {
 
@@ -37,7 +38,6 @@ constexpr int P_EPI_WARPS = 8;
 constexpr int P_THREADS = 64 + 32 * P_EPI_WARPS;
 constexpr int P_EPI_COLS = 32;
 constexpr int P_OUT_BOX = 32 * P_EPI_COLS * 2;     // 2 KB staging box (32 rows x 32 cols)
-constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;        // shared::cluster address of the leader's copy
 
 // RES: the CTA pair owns one n-tile for the whole launch and keeps its weight half (BN/2 x K) resident in
 // shared memory, so only A streams (FC1: K = 256, 64 KB per CTA). The GEMMs here are L2/TMA-bandwidth
@@ -62,59 +62,6 @@ template <int BN, bool U1, bool RES = false> struct PairCfg {
   static constexpr int THREADS = P_THREADS;
   static constexpr int SMEM = RES_BYTES + STAGES * STAGE_BYTES + OUT_BYTES + UX_BYTES + 1024 + 512;
 };
-
-// SMEM descriptor, K-major, no swizzle (the u1 operand): core matrices of 8 rows x 16 B; rows are
-// 16 B apart (one TMA box of 8 x 128), 8-row groups 128 B apart (SBO), K chunks 2 KB apart (LBO).
-// (probe: tools/probes/umma_k16_probe.cu checks the LBO / SBO roles.)
-__device__ __forceinline__ uint64_t sdesc_k16_plain(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)(2048 >> 4) << 16;
-  d |= (uint64_t)(128 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;                                    // layout type 0 = SWIZZLE_NONE
-}
-
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                                 uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
-      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar) & PEER_MASK), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                              uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// arrive on the same barrier offset in both CTAs of the pair once all prior MMAs completed
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
-}
-// arrive on CTA `rank`'s copy of a barrier
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
-  asm volatile(
-      "{\n\t.reg .b32 ra;\n\t"
-      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
-      "r"(rank)
-      : "memory");
-}
-
-template <int BN, bool BF16>
-__device__ __forceinline__ constexpr uint32_t idesc_pair() {
-  return (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) | ((uint32_t)(BN >> 3) << 17) |
-         ((uint32_t)(256 >> 4) << 24);
-}
 
 template <int BN, bool BF16, bool U1, bool RES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>::THREADS, 1)
