@@ -499,7 +499,7 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as f:
             tj = json.load(f)
-        traffic = tj.get("fc2_dram_bytes_per_launch")
+        traffic = tj.get("dominant_dram_bytes_per_launch", tj.get("fc2_dram_bytes_per_launch"))
         if tj.get("gather_dram_bytes_per_ad") and prof_n[PROF_GATHER]:
             # the capture's gather launch covered a different span: scale per ad to this run's launches
             traffic_g = tj["gather_dram_bytes_per_ad"] * N * args.steps / float(prof_n[PROF_GATHER])

@@ -1033,6 +1033,14 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     cp.k1 = c->d_ac_pad;
     cp.h1 = c->d_H[0];
     cp.h2 = c->d_H[1];
+    {
+      static bool chain_instr = getenv("COLD_INSTR") != nullptr;
+      if (chain_instr && !g_instr) {
+        cudaMalloc(&g_instr, 8 * 8 * COLD_MAX_LAYERS);
+        cudaMemset(g_instr, 0, 8 * 8 * COLD_MAX_LAYERS);
+      }
+      cp.instr = chain_instr ? g_instr + 8 * 4 : nullptr;   // slots 32..39
+    }
     const CUtensorMap* tm[9] = {&c->tmAX[xslot], &c->tmB[0], &c->tmB[1], &c->tmB[2], &c->tmC[0], &c->tmC[1],
                                 &c->tmC[2], &c->tmOH[xslot], &c->tmU1T};
     c->mark_begin(st);

@@ -147,6 +147,8 @@ struct ChainParams {
   const int32_t* req_of_ad; int64_t a0;
   int n1, n2, n3, k1;                    // widths of FC1..FC3 and FC1's K (D_ac_pad)
   const void* h1; const void* h2;        // H1 / H2 chunk buffers (for the L2 discards)
+  unsigned long long* instr;             // debug (nullable): wait cycles [0] producer empty, [1] producer
+                                         // hready, [2] MMA full, [3] MMA tempty, [4] MMA uxfull, [5] epi tfull
 };
 bool chain_supported(int n1, int n2, int n3, int k1);
 // tm: X (slot), W1, W2, W3, H1, H2, H3, one-hot (slot), u1 terms

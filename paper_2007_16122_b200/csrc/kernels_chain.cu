@@ -41,6 +41,14 @@ constexpr int C_STAGES = (232448 - C_OUT_BYTES - C_NUX * C_UX_BUF - 1024 - 512) 
 constexpr int C_SMEM = C_STAGES * C_STAGE_BYTES + C_OUT_BYTES + C_NUX * C_UX_BUF + 1024 + 512;
 static_assert(C_STAGES >= 4, "chain kernel pipeline depth");
 
+// debug: cycles a role spent blocked in a barrier wait (cp.instr != null)
+__device__ __forceinline__ void cwait(uint64_t* bar, uint32_t parity, unsigned long long& acc, bool on) {
+  if (!on) { mbar_wait(bar, parity); return; }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  acc += (unsigned long long)(clock64() - t0);
+}
+
 __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
@@ -83,6 +91,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
 
   // the per-pair task order (all roles walk it identically): step s = 0..nrb:
   //   FC1(s) n-tiles | FC3(s-1) | FC2(s) n-tiles
+  // (measured: interleaving FC1(j) with FC2(j-1) to spread the epilogue load doubles the L2 working set
+  // of live activations and ran 14% slower)
   auto for_tasks = [&](auto&& f) {
     for (int s = 0; s <= nrb; s++) {
       if (s < nrb) for (int nb = 0; nb < ntile[0]; nb++) f(0, s, nb);
@@ -129,12 +139,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       const uint64_t pol_b = policy_evict_last();   // weights: re-read by every block
       int s = 0, fc1_t = 0;
       uint32_t ph = 0;
+      const bool ins = cp.instr != nullptr;
+      unsigned long long w_empty = 0, w_hready = 0;
       for_tasks([&](int l, int j, int nb) {
         const int pm = pair + j * npairs;
         const int mrow = pm * 2 * BM + (int)rank * BM;
-        if (l > 0 && nb == 0) mbar_wait(&hready[l - 1], (uint32_t)(j & 1));   // own rows of the input block
+        if (l > 0 && nb == 0) cwait(&hready[l - 1], (uint32_t)(j & 1), w_hready, ins);   // own rows of the input
         for (int kb = 0; kb < kbs[l]; kb++) {
-          mbar_wait(&empty[s], ph ^ 1);
+          cwait(&empty[s], ph ^ 1, w_empty, ins);
           if (leader) mbar_expect_tx(&full[s], 2 * C_STAGE_BYTES);
           tma_load_2d_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb * BK, mrow, l == 0 ? pol_x : pol_a);
           tma_load_2d_pair(sB + s * C_B_BYTES, tB[l], &full[s], kb * BK, nb * C_BN + (int)rank * (C_BN / 2), pol_b);
@@ -155,6 +167,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           fc1_t++;
         }
       });
+      if (ins) { atomicAdd(cp.instr + 0, w_empty); atomicAdd(cp.instr + 1, w_hready); }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
@@ -162,13 +175,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       constexpr uint32_t idesc = idesc_pair<C_BN, BF16>();
       int s = 0, lt = 0, fc1_t = 0;
       uint32_t ph = 0;
+      const bool ins = cp.instr != nullptr;
+      unsigned long long w_full = 0, w_tempty = 0, w_ux = 0;
       for_tasks([&](int l, int j, int nb) {
         const int acc = lt & 1;
-        mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+        cwait(&tempty[acc], ((lt >> 1) & 1) ^ 1, w_tempty, ins);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * C_BN;
         for (int kb = 0; kb < kbs[l]; kb++) {
-          mbar_wait(&full[s], ph);
+          cwait(&full[s], ph, w_full, ins);
           tc_fence_after();
           const uint64_t ad = sdesc_sw128(smem_u32(sA + s * C_A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + s * C_B_BYTES));
@@ -180,7 +195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         }
         if (l == 0) {   // D += A_x B_x^T = u1[request(row)][n]
           const int b = fc1_t % C_NUX;
-          mbar_wait(&uxfull[b], (fc1_t / C_NUX) & 1);
+          cwait(&uxfull[b], (fc1_t / C_NUX) & 1, w_ux, ins);
           tc_fence_after();
           const uint32_t ux = smem_u32(sUX + b * C_UX_BUF);
           const uint64_t adx = sdesc_k16_plain(ux);
@@ -192,6 +207,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         umma_commit_pair(&tfull[acc]);
         lt++;
       });
+      if (ins) { atomicAdd(cp.instr + 2, w_full); atomicAdd(cp.instr + 3, w_tempty); atomicAdd(cp.instr + 4, w_ux); }
     }
   } else {
     // ===== epilogue warps 2..9 (both CTAs): TMEM lane quadrant q, column half h =====
@@ -199,11 +215,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     const int q = warp & 3;
     const int h = ew >> 2;
     const bool elected = (q == 0) && (lane == 0);
+    const bool ins = cp.instr != nullptr && lane == 0;
+    unsigned long long w_tfull = 0;
     int lt = 0;
     for_tasks([&](int l, int j, int nb) {
       const int pm = pair + j * npairs;
       const int acc = lt & 1;
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      cwait(&tfull[acc], (lt >> 1) & 1, w_tfull, ins);
       tc_fence_after();
       const int trow0 = pm * 2 * BM + (int)rank * BM;   // this CTA's first row of the block
       const int row = trow0 + q * 32 + lane;
@@ -244,6 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       }
     });
     if (elected) bulk_wait_all();
+    if (ins) atomicAdd(cp.instr + 5, w_tfull);
   }
   tc_fence_before();
   cluster_sync();

@@ -1,4 +1,5 @@
 python -m paper_2007_16122_b200.build >/dev/null
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests_s27.log 2>&1
-BENCH_ARGS="--requests 1024 --no-e2e --no-latency --no-cpu --steps 5" timeout 900 bash tools/sweep.sh s27:COLD_TAIL=2 s27nochain:COLD_CHAIN=0
-python tools/show.py gpurun_out/sweep_s27*.log > gpurun_out/sweep_s27.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests_s30.log 2>&1
+COLD_INSTR=1 python tools/probes/chain_instr.py 128 > gpurun_out/chain_instr30.log 2>&1
+BENCH_ARGS="--requests 1024 --no-e2e --no-latency --no-cpu --steps 5" timeout 900 bash tools/sweep.sh s30:COLD_TAIL=2
+python tools/show.py gpurun_out/sweep_s30*.log > gpurun_out/sweep_s30.txt 2>&1

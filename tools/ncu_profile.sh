@@ -4,7 +4,7 @@
 set -x
 TAG=${1:-r01}
 shift
-KERNELS=${@:-gather fc1 fc2 fc3 tail45}
+KERNELS=${@:-gather chain tail45}
 OUT=gpurun_out
 # 32 requests x 9472 ads = 2 full 151552-ad chunks per step (one gather span)
 ARGS=${NCU_ARGS:-"--requests 32 --ads 9472 --steps 2 --warmup 1 --no-e2e --no-latency --no-cpu"}
@@ -15,6 +15,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 for k in $KERNELS; do
   case $k in
     gather) RX="regex:gather_kernel"; S=1;;
+    chain) RX="regex:chain_kernel"; S=1;;
     fc1) RX="regex:gemm_pair_kernel"; S=3;;      # pair launches per chunk: FC1, FC2, FC3
     fc2) RX="regex:gemm_pair_kernel"; S=4;;
     fc3) RX="regex:gemm_pair_kernel"; S=5;;
