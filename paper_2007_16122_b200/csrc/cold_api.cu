@@ -173,6 +173,8 @@ struct cold_ctx {
   uint16_t* d_u1t = nullptr;         // [u1_terms * H][u1t_ld] 16-bit terms of u1 (written by user_kernel)
   uint16_t* d_ohot = nullptr;        // [gspan * chunk][16] one-hot u1 operand rows (written by gather)
   CUtensorMap tmU1T;
+  bool chain_tail = false;           // FC4 -> FC5 -> head inside the chain kernel too
+  CUtensorMap tmW4h, tmW5h;          // W4 / W5 with half-N boxes (CTA-pair tiles)
   std::vector<CUtensorMap> tmOH;     // per chunk slot of the span
   int gspan = 1;                     // chunks per column-wise gather pass (X_ac holds gspan * chunk rows)
   CUtensorMap tmC[COLD_MAX_LAYERS];  // epilogue TMA-store maps (32 x 32 boxes)
@@ -580,6 +582,10 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       chain_supported(c->widths[0], c->widths[1], c->widths[2], c->d_ac_pad)) {
     const char* env_chain = getenv("COLD_CHAIN");
     c->chain = !(env_chain && atoi(env_chain) == 0);
+    // COLD_CHAIN=2 also folds FC4 / FC5 / head into the chain: measured slower than the separate
+    // resident-weight tail kernel (N = 128 / 64 pair tiles, larger live L2 set), so off by default
+    c->chain_tail = c->chain && chain_tail_supported(c->widths[3], c->widths[4], c->widths[2]) &&
+                    c->widths[5] <= 2 && env_chain != nullptr && atoi(env_chain) == 2;
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
@@ -748,6 +754,10 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
       s = make_tmap(&c->tmB[l], c->d_w[l], c->precision, Kp, out,
                     c->pair[l] ? c->bn[l] / 2 : c->bn[l] / c->cs[l]);
       if (s) return s;
+      if (c->chain_tail && (l == 3 || l == 4)) {   // half-N boxes for the chain's pair tiles
+        s = make_tmap(l == 3 ? &c->tmW4h : &c->tmW5h, c->d_w[l], c->precision, Kp, out, out / 2);
+        if (s) return s;
+      }
     }
     const int hl = c->L - 1, hin = c->widths[hl - 1], hout = c->widths[hl];
     s = upload(c, (void**)&c->d_head_w, sizeof(float) * hout * hin, [&](uint8_t* h) { memcpy(h, p->fc_w[hl], sizeof(float) * hout * hin); });
@@ -1041,12 +1051,28 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
       }
       cp.instr = chain_instr ? g_instr + 8 * 4 : nullptr;   // slots 32..39
     }
-    const CUtensorMap* tm[9] = {&c->tmAX[xslot], &c->tmB[0], &c->tmB[1], &c->tmB[2], &c->tmC[0], &c->tmC[1],
-                                &c->tmC[2], &c->tmOH[xslot], &c->tmU1T};
+    if (c->chain_tail) {
+      cp.tail = 1;
+      cp.n4 = c->widths[3];
+      cp.n5 = c->widths[4];
+      cp.b4 = c->d_b[3];
+      cp.b5 = c->d_b[4];
+      cp.head_w = c->d_head_w;
+      cp.head_b = c->d_head_b;
+      cp.head_n = c->widths[5];
+      cp.h3 = c->d_H[2];
+      cp.h4 = c->d_H[3];
+      cp.scores = scores_out;
+    }
+    const CUtensorMap* tm[12] = {&c->tmAX[xslot], &c->tmB[0], &c->tmB[1], &c->tmB[2], &c->tmC[0], &c->tmC[1],
+                                 &c->tmC[2], &c->tmOH[xslot], &c->tmU1T,
+                                 c->chain_tail ? &c->tmW4h : &c->tmB[0], c->chain_tail ? &c->tmW5h : &c->tmB[0],
+                                 c->chain_tail ? &c->tmC[3] : &c->tmB[0]};
     c->mark_begin(st);
     launch_chain(tm, (int)n, c->precision == COLD_BF16 ? 1 : 0, cp, c->num_sms, c->pdl && !c->prof, st);
     c->mark_end(COLD_PROF_FC, st);
     n_gemm = 0;
+    if (c->chain_tail) return;   // FC4 / FC5 / head done inside the chain
   }
   static bool instr_on = getenv("COLD_INSTR") != nullptr;
   if (instr_on && !g_instr) {

@@ -28,7 +28,7 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
                                                uint8_t* group_buf, const CUtensorMap* tmC, int col_base,
                                                int tile_row0, int q, int h, int lane, int dbg = 0,
                                                unsigned long long* tacc = nullptr, void* gout = nullptr,
-                                               int ldo = 0, int M = 0) {
+                                               int ldo = 0, int M = 0, uint64_t store_policy = 0) {
   const uint32_t sbuf = smem_u32(group_buf) + (uint32_t)q * EPI_WIDE_BOX;
   const bool elected = (q == 0) && (lane == 0);
   // debug timing (tacc != null, lane 0): cycles in [0] TMEM load+wait, [1] math+pack, [2] wait for the
@@ -115,7 +115,8 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
     tick(3);
     if (elected && dbg != 4) {
       // dbg 6 (timing experiment): every box to the same L2-resident location (no DRAM write traffic)
-      tma_store_2d(tmC, group_buf, dbg == 6 ? 0 : col0, dbg == 6 ? 0 : tile_row0);
+      if (store_policy) tma_store_2d_hint(tmC, group_buf, col0, tile_row0, store_policy);
+      else tma_store_2d(tmC, group_buf, dbg == 6 ? 0 : col0, dbg == 6 ? 0 : tile_row0);
       bulk_commit();
     }
     tick(4);

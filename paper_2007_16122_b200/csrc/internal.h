@@ -147,12 +147,18 @@ struct ChainParams {
   const int32_t* req_of_ad; int64_t a0;
   int n1, n2, n3, k1;                    // widths of FC1..FC3 and FC1's K (D_ac_pad)
   const void* h1; const void* h2;        // H1 / H2 chunk buffers (for the L2 discards)
+  // TAIL variant: FC4 (n4) -> FC5 (n5) -> head (head_n = 1 or 2) -> sigma -> scores, also in the chain
+  int tail; int n4, n5;
+  const float* b4; const float* b5; const float* head_w; const float* head_b; int head_n;
+  const void* h3; const void* h4;
+  float* scores;                         // chunk-local [M]
   unsigned long long* instr;             // debug (nullable): wait cycles [0] producer empty, [1] producer
                                          // hready, [2] MMA full, [3] MMA tempty, [4] MMA uxfull, [5] epi tfull
 };
 bool chain_supported(int n1, int n2, int n3, int k1);
-// tm: X (slot), W1, W2, W3, H1, H2, H3, one-hot (slot), u1 terms
-cudaError_t launch_chain(const CUtensorMap* tm[9], int M, int bf16, const ChainParams& cp, int num_sms, bool pdl,
+bool chain_tail_supported(int n4, int n5, int n3);
+// tm: X (slot), W1, W2, W3, H1, H2, H3, one-hot (slot), u1 terms, W4 half-box, W5 half-box, H4
+cudaError_t launch_chain(const CUtensorMap* tm[12], int M, int bf16, const ChainParams& cp, int num_sms, bool pdl,
                          cudaStream_t s);
 
 // fused FC(L-3) .. FC(L-2) + head after a GEMM FC(L-4) (paper widths 128, 64 -> 2), resident weights

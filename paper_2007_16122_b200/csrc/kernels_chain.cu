@@ -53,13 +53,15 @@ __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
-template <bool BF16>
+template <bool BF16, bool TAIL>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     chain_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                  const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmW3,
                  const __grid_constant__ CUtensorMap tmH1, const __grid_constant__ CUtensorMap tmH2,
                  const __grid_constant__ CUtensorMap tmH3, const __grid_constant__ CUtensorMap tmOH,
-                 const __grid_constant__ CUtensorMap tmU1T, int M, ChainParams cp) {
+                 const __grid_constant__ CUtensorMap tmU1T, const __grid_constant__ CUtensorMap tmW4,
+                 const __grid_constant__ CUtensorMap tmW5, const __grid_constant__ CUtensorMap tmH4, int M,
+                 ChainParams cp) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -73,8 +75,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   uint64_t* tempty = tfull + 2;                   // leader: both CTAs' epilogues drained [2]
   uint64_t* uxfull = tempty + 2;                  // leader: u1 operand landed [C_NUX]
   uint64_t* uxempty = uxfull + C_NUX;             // both: u1 MMA of the buffer's last FC1 tile done [C_NUX]
-  uint64_t* hready = uxempty + C_NUX;             // local: [0] H1 block stored, [1] H2 block stored
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hready + 2);
+  uint64_t* hready = uxempty + C_NUX;             // local: [l] block of layer l's output stored (H1..H4)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hready + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -82,21 +84,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   const int pair = (int)cluster_id_x(), npairs = (int)num_clusters_x();
   const int num_pm = (M + 2 * BM - 1) / (2 * BM);
   const int nrb = pair < num_pm ? (num_pm - 1 - pair) / npairs + 1 : 0;   // this pair's row blocks
-  const int n_[3] = {cp.n1, cp.n2, cp.n3};
-  const int kbs[3] = {cp.k1 / BK, cp.n1 / BK, cp.n2 / BK};
-  const CUtensorMap* tA[3] = {&tmX, &tmH1, &tmH2};
-  const CUtensorMap* tB[3] = {&tmW1, &tmW2, &tmW3};
-  const CUtensorMap* tC[3] = {&tmH1, &tmH2, &tmH3};
-  const int ntile[3] = {cp.n1 / C_BN, cp.n2 / C_BN, cp.n3 / C_BN};
+  // layers 0..2 = FC1..FC3 (N = 256 per tile), TAIL: 3 = FC4 (N = n4 <= 256), 4 = FC5 (N = n5) + head
+  const int kbs[5] = {cp.k1 / BK, cp.n1 / BK, cp.n2 / BK, cp.n3 / BK, cp.n4 / BK};
+  const CUtensorMap* tA[5] = {&tmX, &tmH1, &tmH2, &tmH3, &tmH4};
+  const CUtensorMap* tB[5] = {&tmW1, &tmW2, &tmW3, &tmW4, &tmW5};
+  const CUtensorMap* tC[4] = {&tmH1, &tmH2, &tmH3, &tmH4};
+  const int ntile[5] = {cp.n1 / C_BN, cp.n2 / C_BN, cp.n3 / C_BN, 1, 1};
+  const int tn[5] = {C_BN, C_BN, C_BN, cp.n4, cp.n5};          // tile N per layer
 
   // the per-pair task order (all roles walk it identically): step s = 0..nrb:
   //   FC1(s) n-tiles | FC3(s-1) | FC2(s) n-tiles
   // (measured: interleaving FC1(j) with FC2(j-1) to spread the epilogue load doubles the L2 working set
   // of live activations and ran 14% slower)
+  // TAIL: step s = FC1(s) | FC5(s-3) | FC4(s-2) | FC3(s-1) | FC2(s). Every consumer sits several tiles
+  // after its producer, and the producer's wait on hready[l](j) always precedes the loads of the task
+  // that would complete the barrier's next phase (no parity aliasing).
   auto for_tasks = [&](auto&& f) {
-    for (int s = 0; s <= nrb; s++) {
+    for (int s = 0; s <= nrb + (TAIL ? 2 : 0); s++) {
       if (s < nrb) for (int nb = 0; nb < ntile[0]; nb++) f(0, s, nb);
-      if (s >= 1) for (int nb = 0; nb < ntile[2]; nb++) f(2, s - 1, nb);
+      if (TAIL && s >= 3) f(4, s - 3, 0);
+      if (TAIL && s >= 2 && s <= nrb + 1) f(3, s - 2, 0);
+      if (s >= 1 && s <= nrb) for (int nb = 0; nb < ntile[2]; nb++) f(2, s - 1, nb);
       if (s < nrb) for (int nb = 0; nb < ntile[1]; nb++) f(1, s, nb);
     }
   };
@@ -105,11 +113,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     for (int s = 0; s < C_STAGES; s++) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; s++) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * C_EPI_WARPS); }
     for (int s = 0; s < C_NUX; s++) { mbar_init(&uxfull[s], 1); mbar_init(&uxempty[s], 1); }
-    mbar_init(&hready[0], C_EPI_WARPS);
-    mbar_init(&hready[1], C_EPI_WARPS);
+    for (int i = 0; i < 4; i++) mbar_init(&hready[i], C_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    const CUtensorMap* maps[9] = {&tmX, &tmW1, &tmW2, &tmW3, &tmH1, &tmH2, &tmH3, &tmOH, &tmU1T};
-    for (int i = 0; i < 9; i++) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)maps[i]) : "memory");
+    const CUtensorMap* maps[12] = {&tmX, &tmW1, &tmW2, &tmW3, &tmH1, &tmH2, &tmH3, &tmOH, &tmU1T, &tmW4, &tmW5, &tmH4};
+    for (int i = 0; i < (TAIL ? 12 : 9); i++) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)maps[i]) : "memory");
   }
   if (BF16 && warp == 2) {   // bf16: the 4th K chunk of every B_x buffer stays zero
     for (int b = 0; b < C_NUX; b++)
@@ -145,11 +152,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         const int pm = pair + j * npairs;
         const int mrow = pm * 2 * BM + (int)rank * BM;
         if (l > 0 && nb == 0) cwait(&hready[l - 1], (uint32_t)(j & 1), w_hready, ins);   // own rows of the input
+        const int bhalf = tn[l] / 2;                  // weight rows this CTA stages (half the tile N)
         for (int kb = 0; kb < kbs[l]; kb++) {
           cwait(&empty[s], ph ^ 1, w_empty, ins);
-          if (leader) mbar_expect_tx(&full[s], 2 * C_STAGE_BYTES);
+          if (leader) mbar_expect_tx(&full[s], 2 * (C_A_BYTES + bhalf * BK * 2));
           tma_load_2d_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb * BK, mrow, l == 0 ? pol_x : pol_a);
-          tma_load_2d_pair(sB + s * C_B_BYTES, tB[l], &full[s], kb * BK, nb * C_BN + (int)rank * (C_BN / 2), pol_b);
+          tma_load_2d_pair(sB + s * C_B_BYTES, tB[l], &full[s], kb * BK, nb * tn[l] + (int)rank * bhalf, pol_b);
           if (++s == C_STAGES) { s = 0; ph ^= 1; }
         }
         if (l == 0) {   // FC1: the tile's u1 operand (one-hot rows + u1-term columns)
@@ -172,12 +180,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   } else if (warp == 1) {
     if (leader && lane == 0) {
       // ===== MMA issuer (leader only) =====
-      constexpr uint32_t idesc = idesc_pair<C_BN, BF16>();
+      constexpr uint32_t id256 = idesc_pair<C_BN, BF16>();
+      const uint32_t id_tail[2] = {cp.n4 == 128 ? idesc_pair<128, BF16>() : idesc_pair<64, BF16>(),
+                                   cp.n5 == 64 ? idesc_pair<64, BF16>() : idesc_pair<32, BF16>()};
       int s = 0, lt = 0, fc1_t = 0;
       uint32_t ph = 0;
       const bool ins = cp.instr != nullptr;
       unsigned long long w_full = 0, w_tempty = 0, w_ux = 0;
       for_tasks([&](int l, int j, int nb) {
+        const uint32_t idesc = l < 3 ? id256 : id_tail[l - 3];
         const int acc = lt & 1;
         cwait(&tempty[acc], ((lt >> 1) & 1) ^ 1, w_tempty, ins);
         tc_fence_after();
@@ -199,8 +210,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           tc_fence_after();
           const uint32_t ux = smem_u32(sUX + b * C_UX_BUF);
           const uint64_t adx = sdesc_k16_plain(ux);
-          umma_f16_pair(d, adx, sdesc_k16_plain(ux + C_UXA), idesc, 1u);
-          if (BF16) umma_f16_pair(d, adx, sdesc_k16_plain(ux + C_UXA + 2 * (C_BN / 2) * 16), idesc, 1u);
+          umma_f16_pair(d, adx, sdesc_k16_plain(ux + C_UXA), id256, 1u);
+          if (BF16) umma_f16_pair(d, adx, sdesc_k16_plain(ux + C_UXA + 2 * (C_BN / 2) * 16), id256, 1u);
           umma_commit_pair(&uxempty[b]);
           fc1_t++;
         }
@@ -215,6 +226,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     const int q = warp & 3;
     const int h = ew >> 2;
     const bool elected = (q == 0) && (lane == 0);
+    const uint64_t pol_h3 = policy_evict_first();
     const bool ins = cp.instr != nullptr && lane == 0;
     unsigned long long w_tfull = 0;
     int lt = 0;
@@ -234,14 +246,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         }
       }
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C_BN);
-      epi_store_wide<BF16>(tbase, h * (C_BN / 2), (h + 1) * (C_BN / 2), l == 1 ? cp.b2 : (l == 2 ? cp.b3 : nullptr),
-                           0u, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l], nb * C_BN, trow0, q, h, lane);
+      if (TAIL && l == 4) {
+        // FC5 + head: h == 0 warps own their quadrant's rows: ReLU(acc + b5) . head_w + head_b -> sigma
+        if (h == 0) {
+          float z0 = 0.0f, z1 = 0.0f;
+          for (int c = 0; c < cp.n5; c += 32) {
+            uint32_t v[32];
+            TMEM_LD32(tbase + c, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+              const float a = fmaxf(__uint_as_float(v[i]) + __ldg(cp.b5 + c + i), 0.0f);
+              z0 = fmaf(__ldg(cp.head_w + c + i), a, z0);
+              if (cp.head_n == 2) z1 = fmaf(__ldg(cp.head_w + cp.n5 + c + i), a, z1);
+            }
+          }
+          if (row < M) {
+            const float z = cp.head_n == 2 ? (z1 + cp.head_b[1]) - (z0 + cp.head_b[0]) : z0 + cp.head_b[0];
+            cp.scores[row] = sigmoid(z);
+          }
+        }
+      } else {
+        // H3 (no TAIL) leaves for the tail kernel: stream it past L2 (evict_first) so it does not push out
+        // live H1 / H2
+        const int half = tn[l] / 2;
+        const float* bias = l == 1 ? cp.b2 : (l == 2 ? cp.b3 : (l == 3 ? cp.b4 : nullptr));
+        epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, 0u, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
+                             nb * tn[l], trow0, q, h, lane, 0, nullptr, nullptr, 0, 0,
+                             (!TAIL && l == 2) ? pol_h3 : 0ull);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
       lt++;
       const bool last_of_layer = nb == ntile[l] - 1;
-      if (l < 2 && last_of_layer) {
+      if ((l < 2 || (TAIL && l < 4)) && last_of_layer) {
         // the block's rows of this layer are stored once this group's bulk stores completed
         if (elected) {
           bulk_wait_all();
@@ -251,10 +290,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         if (lane == 0) mbar_arrive(&hready[l]);
       }
       if (l >= 1 && last_of_layer) {
-        // the input of this layer for the block (H1 for FC2, H2 for FC3) has been consumed by the MMAs
-        // (tfull of the last tile): drop this CTA's rows from L2 without write-back
-        const uint8_t* base = reinterpret_cast<const uint8_t*>(l == 1 ? cp.h1 : cp.h2);
-        const int ld = (l == 1 ? cp.n1 : cp.n2) * 2;           // bytes per row
+        // the input of this layer for the block (H1 for FC2, H2 for FC3, H3 / H4 for FC4 / FC5) has been
+        // consumed by the MMAs (tfull of the last tile): drop this CTA's rows from L2 without write-back
+        const void* in_buf[5] = {nullptr, cp.h1, cp.h2, cp.h3, cp.h4};
+        const int in_w[5] = {0, cp.n1, cp.n2, cp.n3, cp.n4};
+        const uint8_t* base = reinterpret_cast<const uint8_t*>(in_buf[l]);
+        const int ld = in_w[l] * 2;                            // bytes per row
         const int lines = ld / 128;
         const int rows = min(BM, M - trow0);
         for (int i = (ew * 32 + lane); i < rows * lines; i += C_EPI_WARPS * 32)
@@ -275,15 +316,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
 bool chain_supported(int n1, int n2, int n3, int k1) {
   return n1 % C_BN == 0 && n2 % C_BN == 0 && n3 % C_BN == 0 && k1 % BK == 0 && n1 / BK >= 1;
 }
+// FC4 / FC5 as 256-row pair tiles: N in {128, 64} / {64, 32} (the paper: 128 -> 64 -> head)
+bool chain_tail_supported(int n4, int n5, int n3) {
+  return (n4 == 128 || n4 == 64) && (n5 == 64 || n5 == 32) && n3 % BK == 0 && n4 % BK == 0;
+}
 
-cudaError_t launch_chain(const CUtensorMap* tm[9], int M, int bf16, const ChainParams& cp, int num_sms, bool pdl,
+cudaError_t launch_chain(const CUtensorMap* tm[12], int M, int bf16, const ChainParams& cp, int num_sms, bool pdl,
                          cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
-  auto kern = bf16 ? chain_kernel<true> : chain_kernel<false>;
-  static bool attr[2] = {false, false};
-  if (!attr[bf16 ? 1 : 0]) {
+  auto kern = bf16 ? (cp.tail ? chain_kernel<true, true> : chain_kernel<true, false>)
+                   : (cp.tail ? chain_kernel<false, true> : chain_kernel<false, false>);
+  static bool attr[4] = {false, false, false, false};
+  const int ai = (bf16 ? 2 : 0) + (cp.tail ? 1 : 0);
+  if (!attr[ai]) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_SMEM);
-    attr[bf16 ? 1 : 0] = true;
+    attr[ai] = true;
   }
   const int num_pm = (M + 2 * BM - 1) / (2 * BM);
   const int pairs = num_pm < num_sms / 2 ? num_pm : num_sms / 2;
@@ -297,8 +344,8 @@ cudaError_t launch_chain(const CUtensorMap* tm[9], int M, int bf16, const ChainP
   attrs[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, kern, *tm[0], *tm[1], *tm[2], *tm[3], *tm[4], *tm[5], *tm[6], *tm[7], *tm[8], M,
-                            cp);
+  return cudaLaunchKernelEx(&cfg, kern, *tm[0], *tm[1], *tm[2], *tm[3], *tm[4], *tm[5], *tm[6], *tm[7], *tm[8],
+                            *tm[9], *tm[10], *tm[11], M, cp);
 }
 
 }  // namespace cold

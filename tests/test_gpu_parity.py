@@ -122,7 +122,9 @@ def test_paper_stack_tensor_core(prec):
 
 
 @pytest.mark.parametrize("env", [{"COLD_TAIL": "2"}, {"COLD_TAIL": "1"}, {"COLD_TAIL": "0"}, {"COLD_PAIR": "2"},
-                                 {"COLD_PAIR": "0", "COLD_RESB": "0"}, {"COLD_GSPAN": "1"}, {"COLD_GSPAN": "3"}])
+                                 {"COLD_PAIR": "0", "COLD_RESB": "0"}, {"COLD_GSPAN": "1"}, {"COLD_GSPAN": "3"},
+                                 {"COLD_CHAIN": "0"}, {"COLD_CHAIN": "2"}, {"COLD_CHAIN": "0", "COLD_PAIR_RES": "0"},
+                                 {"COLD_CHAIN": "0", "COLD_U1MMA": "0"}])
 def test_kernel_variants_match_oracle(env, monkeypatch):
     """Every kernel variant the library can select (fused tail FC3-5 / FC4-5 / none, CTA-pair or
     single-CTA GEMMs, gather spans of 1 or 3 chunks) on several chunks with a ragged tail."""
