@@ -73,8 +73,10 @@ enum { COLD_RELU = 0 };                                        /* hidden activat
 typedef struct {
   int32_t side;          /* COLD_USER / COLD_AD / COLD_CROSS */
   int32_t pooled;        /* AD groups: 1 = multi-valued bag (CSR offsets), 0 = one id per ad.
-                            USER groups are always CSR (a single-valued group has bags of 1).
-                            CROSS: ignored (rows = user bag x ad bag, x-major). */
+                            USER groups are always CSR; pooled = 0 declares bags of exactly 1 (a
+                            performance hint: crosses of two single groups are gathered in the merged
+                            single-row pass; a request with another bag length still scores correctly
+                            through the general path). CROSS: ignored (rows = user bag x ad bag, x-major). */
   int64_t cardinality;   /* table rows, >= 1 */
   int32_t user_ref;      /* CROSS: schema index of a USER group */
   int32_t ad_ref;        /* CROSS: schema index of an AD group */

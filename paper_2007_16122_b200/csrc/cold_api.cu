@@ -169,6 +169,7 @@ struct cold_ctx {
   std::vector<CUtensorMap> tmAX;     // layer-0 A maps, one per chunk slot of the gather span
   bool u1mma = false;                // FC1 adds u1[request(row)] on the tensor core (kernels_gemm2.cu)
   bool chain = false;                // FC1 -> FC3 in one persistent kernel over 256-row blocks
+  int64_t chain_min = 0;             // chunks smaller than this use the layer-by-layer kernels
   int u1_terms = 0, u1t_ld = 0;
   uint16_t* d_u1t = nullptr;         // [u1_terms * H][u1t_ld] 16-bit terms of u1 (written by user_kernel)
   uint16_t* d_ohot = nullptr;        // [gspan * chunk][16] one-hot u1 operand rows (written by gather)
@@ -582,6 +583,8 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       chain_supported(c->widths[0], c->widths[1], c->widths[2], c->d_ac_pad)) {
     const char* env_chain = getenv("COLD_CHAIN");
     c->chain = !(env_chain && atoi(env_chain) == 0);
+    const char* env_cmin = getenv("COLD_CHAIN_MIN");
+    c->chain_min = env_cmin ? atoll(env_cmin) : (int64_t)c->num_sms * 256;
     // COLD_CHAIN=2 also folds FC4 / FC5 / head into the chain: measured slower than the separate
     // resident-weight tail kernel (N = 128 / 64 pair tiles, larger live L2 set), so off by default
     c->chain_tail = c->chain && chain_tail_supported(c->widths[3], c->widths[4], c->widths[2]) &&
@@ -973,7 +976,23 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
   ga.groups = c->d_groups;
   ga.bv = bv;
   ga.n_ac = (int)c->sel_ac.size();
-  for (int j = 0; j < ga.n_ac; j++) { ga.ac_g[j] = c->sel_ac[j]; ga.order[j] = c->gather_order[j]; }
+  // COLD_GATHER_MERGE=1: single-valued AD groups and single x single crosses go to one merged column
+  // (measured 12% slower than one column per group on the configs[4] stream, so off by default)
+  static const bool merge = getenv("COLD_GATHER_MERGE") && atoi(getenv("COLD_GATHER_MERGE")) != 0;
+  const bool vec_rows = c->k * c->elem() % 16 == 0;
+  auto is_single = [&](int g) {
+    const cold_group& G = c->groups[g];
+    if (G.side == COLD_AD) return !G.pooled;
+    if (G.side == COLD_CROSS) return !c->groups[G.ad_ref].pooled && !c->groups[G.user_ref].pooled;
+    return false;
+  };
+  ga.n_ac = 0;
+  ga.n_single = 0;
+  for (int j = 0; j < (int)c->sel_ac.size(); j++) {
+    const int g = c->sel_ac[c->gather_order[j]];
+    if (merge && vec_rows && is_single(g)) ga.single_g[ga.n_single++] = g;
+    else { ga.ac_g[ga.n_ac] = g; ga.order[ga.n_ac] = ga.n_ac; ga.n_ac++; }
+  }
   ga.k = c->k;
   ga.se_w = c->d_se_w;
   ga.se_b = c->d_se_b;
@@ -1028,7 +1047,9 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     return;
   }
   int n_gemm = c->L - 1 - c->n_tail;
-  if (c->chain) {   // FC1..FC3 in one launch (kernels_chain.cu), then the FC4/FC5/head tail below
+  // the chain walks 256-row blocks per CTA pair: below ~2 blocks per pair (e.g. one 4,000-ad request)
+  // the layer-by-layer kernels expose more parallelism per layer and have lower latency
+  if (c->chain && n >= c->chain_min) {   // FC1..FC3 in one launch (kernels_chain.cu), then the FC4/FC5/head tail below
     ChainParams cp;
     memset(&cp, 0, sizeof(cp));
     cp.b2 = c->d_b[1];
@@ -1221,12 +1242,23 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
         g1.n_ac = 1;
         g1.ac_g[0] = ga.ac_g[ga.order[j]];
         g1.order[0] = 0;
+        g1.n_single = 0;
         g1.ohot = nullptr;
         c->mark_begin(st);
         launch_gather(g1, c->precision, st);
         c->mark_end(COLD_PROF_GATHER, st);
       }
+      if (ga.n_single > 0) {
+        g1 = ga;
+        g1.n_ac = 0;
+        g1.ohot = nullptr;
+        c->mark_begin(st);
+        launch_gather(g1, c->precision, st);
+        c->mark_end(COLD_PROF_GATHER, st);
+      }
+      g1 = ga;
       g1.n_ac = 0;
+      g1.n_single = 0;
       g1.ohot = ga.ohot;
       c->mark_begin(st);
       launch_gather(g1, c->precision, st);
@@ -1359,6 +1391,7 @@ extern "C" cold_status cold_se_stats(cold_ctx* c, const cold_batch* b, double* m
       if (cls == pass) ga.ac_g[ga.n_ac++] = g;
     }
   for (int j = 0; j < ga.n_ac; j++) ga.order[j] = j;
+  ga.n_single = 0;
   ga.X = nullptr;
   ga.ohot = nullptr;
   ga.stats = d_stats;

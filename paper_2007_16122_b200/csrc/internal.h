@@ -58,6 +58,10 @@ struct GatherArgs {
   int n_sel, d_in;
   const float* in_scale;           // input normalisation [D_in] (nullable)
   const float* in_shift;
+  // merged single-row column (grid.y == n_ac): every AD single group and every single x single CROSS
+  // group of an ad in one thread (more loads in flight per thread than one group per thread)
+  int n_single;
+  int single_g[COLD_MAX_GROUPS];   // schema indices, handled by the merged column (excluded from order[])
   double* stats;                   // SE statistics mode: [M] += s_g per ad; X is not written
   uint16_t* ohot;                  // FC1 u1 operand (nullable): [n][16] span-local rows, the one-hot slot of
                                    // the row's request in its 256-row CTA-pair tile, repeated in k 0-7 / 8-15

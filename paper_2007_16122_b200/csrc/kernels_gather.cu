@@ -8,6 +8,7 @@
 //                  AD/CROSS group, threads = consecutive ads. Cross rows are hashed from the user
 //                  bag x the ad bag (AMB-9), rows gathered with 16 B vector loads, pooled in fp32
 //                  in bag order, linear_log -> SE gate -> v -> RNE cast into X_ac (A3-A5).
+#include <algorithm>
 #include <cstdlib>
 
 #include "internal.h"
@@ -61,13 +62,22 @@ __device__ __forceinline__ int64_t checked(int64_t id, int64_t card, int validat
 }
 
 // ---------------------------------------------------------------------------------------------
-// user side: grid = R requests, block = 256 threads
+// user side: grid = (R requests, S output slices), block = 256 threads. Every CTA of a request pools
+// the request's user groups (cheap: ~84 rows); the CTA with blockIdx.y == 0 also writes x_u, the
+// ad -> request map, statistics and debug outputs. The hoisted GEMV u1 = b1 + W1_u x_u is split over
+// the S CTAs (S > 1 when few requests are in flight: the single-request latency path).
+// Bag pooling: the warp loads up to 32 rows of a bag in parallel (one row per lane, 256-bit), stages
+// them in shared memory and lane d sums dimension d sequentially in bag order (the fp32 order the
+// oracle's fp32-ordered mode defines), instead of a dependent id -> row chain per bag element.
 template <typename T, int K>
 __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
-  extern __shared__ float xs[];           // [n_user * K]
+  extern __shared__ float xs[];           // [n_user * K] then per-warp row stage [8][32][K]
+  float* stage = xs + ((a.n_user * K + 3) & ~3);
   const int r = blockIdx.x;
+  const bool main_cta = blockIdx.y == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int d_u = a.n_user * K;
+  float* wst = stage + warp * 32 * K;
   // one warp per selected user group; lane d < K owns dimension d
   for (int j = warp; j < a.n_user; j += blockDim.x / 32) {
     const int g = a.user_g[j];
@@ -77,9 +87,17 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
     const int64_t o1 = (int64_t)B.offs[r + 1 - B.offs_shift] - B.val_shift;
     float e = 0.0f;
     const T* tab = reinterpret_cast<const T*>(G.table);
-    for (int64_t i = o0; i < o1; i++) {
-      int64_t row = checked(B.ids[i], G.card, a.validate, a.err);
-      if (lane < K) e += Store<T>::to_f(tab[row * K + lane]);
+    for (int64_t c0 = o0; c0 < o1; c0 += 32) {
+      const int cnt = (int)min((int64_t)32, o1 - c0);
+      if (lane < cnt) {                      // lane i fetches bag element c0 + i
+        const int64_t row = checked(B.ids[c0 + lane], G.card, a.validate, a.err);
+#pragma unroll
+        for (int d = 0; d < K; d++) wst[lane * K + d] = Store<T>::to_f(tab[row * K + d]);
+      }
+      __syncwarp();
+      if (lane < K)
+        for (int i = 0; i < cnt; i++) e += wst[i * K + lane];
+      __syncwarp();
     }
     float pooled = e;
     if (a.linear_log) e = linear_log(e);
@@ -88,7 +106,8 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
     for (int off = 16; off; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
     const float s = sigmoid(z + a.se_b[g]);
     if (a.stats) {                          // SE statistics: every ad of the request shares s_g
-      if (lane == 0) atomicAdd(a.stats + g, (double)s * (double)(a.ad_offsets[r + 1] - a.ad_offsets[r]));
+      if (lane == 0 && main_cta)
+        atomicAdd(a.stats + g, (double)s * (double)(a.ad_offsets[r + 1] - a.ad_offsets[r]));
       continue;
     }
     if (lane < K) {
@@ -98,19 +117,22 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
         v = fmaf(v, a.in_scale[col], a.in_shift[col]);
       }
       xs[j * K + lane] = v;
-      a.xu[(int64_t)r * d_u + j * K + lane] = v;
-      if (a.dbg_pooled || a.dbg_feat) {
-        const int pos = G.sel_pos;
-        for (int64_t ad = a.ad_offsets[r]; ad < a.ad_offsets[r + 1]; ad++) {
-          if (a.dbg_pooled) a.dbg_pooled[(ad * a.n_sel + pos) * K + lane] = pooled;
-          if (a.dbg_feat) a.dbg_feat[ad * a.d_in + pos * K + lane] = v;
+      if (main_cta) {
+        a.xu[(int64_t)r * d_u + j * K + lane] = v;
+        if (a.dbg_pooled || a.dbg_feat) {
+          const int pos = G.sel_pos;
+          for (int64_t ad = a.ad_offsets[r]; ad < a.ad_offsets[r + 1]; ad++) {
+            if (a.dbg_pooled) a.dbg_pooled[(ad * a.n_sel + pos) * K + lane] = pooled;
+            if (a.dbg_feat) a.dbg_feat[ad * a.d_in + pos * K + lane] = v;
+          }
         }
       }
     }
   }
   __syncthreads();
   // u1[r][o] = b1[o] + sum_i W1u[o][i] x_u[i]   (W1u stored transposed: coalesced over o)
-  for (int o = threadIdx.x; o < a.H && !a.stats; o += blockDim.x) {
+  const int ostep = blockDim.x * gridDim.y;
+  for (int o = blockIdx.y * blockDim.x + threadIdx.x; o < a.H && !a.stats; o += ostep) {
     float acc = a.b1[o];
     for (int i = 0; i < d_u; i++) acc = fmaf(a.w1u_t[(int64_t)i * a.H + o], xs[i], acc);
     a.u1[(int64_t)r * a.H + o] = acc;
@@ -131,8 +153,9 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
       }
     }
   }
-  for (int64_t ad = a.ad_offsets[r] + threadIdx.x; ad < a.ad_offsets[r + 1]; ad += blockDim.x)
-    a.req_of_ad[ad] = r;
+  if (main_cta)
+    for (int64_t ad = a.ad_offsets[r] + threadIdx.x; ad < a.ad_offsets[r + 1]; ad += blockDim.x)
+      a.req_of_ad[ad] = r;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -145,7 +168,7 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
 // cross bags), which keeps the fp32 pooled sums bit-identical to the oracle's fp32-ordered mode.
 // A cross group's user-side half of the hash, hx = fmix64(x ^ salt_g), depends only on the request:
 // a block spanning <= 2 requests hashes their user bags once into shared memory (AMB-9).
-constexpr int GATHER_APT = 4;       // ads per thread
+constexpr int GATHER_APT_BIG = 4;   // ads per thread on large spans
 constexpr int HX_HALF = 256;        // user-bag hashes cached per request slot
 
 template <typename T, int K>
@@ -245,9 +268,112 @@ __device__ __forceinline__ void write_ohot(const GatherArgs& a, int64_t i, uint1
   dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
-template <typename T, int K, bool FAST, int MINB = 4>
+// Merged single-row column: one thread takes an ad through every single-valued AD group and every
+// (single user group) x (single AD group) cross, 4 rows in flight at a time, instead of one group column
+// per pass (each single-row column was one latency-bound wave: id load -> row load -> store).
+// Sums are of one row (0 + v, exact), so results are identical to the per-column path.
+template <typename T, int K, bool FAST, int GATHER_APT>
+__device__ __forceinline__ void singles_column(const GatherArgs& a) {
+  constexpr int NV = K * (int)sizeof(T) / 16;
+  constexpr int RB = NV <= 2 ? 4 : 2;          // rows in flight
+  __shared__ uint64_t s_hx1[COLD_MAX_GROUPS][2];   // per cross: hx of the block's first / last request
+  __shared__ int s_ok[COLD_MAX_GROUPS];            // 1: both requests have a user bag of exactly 1
+  const int64_t base = (int64_t)blockIdx.x * (128 * GATHER_APT);
+  const int64_t last = (base + 128 * GATHER_APT < a.n ? base + 128 * GATHER_APT : a.n) - 1;
+  const int rfirst = a.req_of_ad[a.a0 + base];
+  const int rlast = a.req_of_ad[a.a0 + last];
+  for (int i = threadIdx.x; i < a.n_single; i += blockDim.x) {
+    const int g = a.single_g[i];
+    const DevGroup G = a.groups[g];
+    if (G.side != 2) continue;
+    const DevGroup U = a.groups[G.user_ref];
+    const BatchGroup& BU = a.bv.g[G.user_ref];
+    const uint64_t salt = cross_salt(g);
+    int ok = rlast - rfirst <= 1;
+    for (int q = 0; q < 2; q++) {
+      const int r = q == 0 ? rfirst : rlast;
+      const int64_t o0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
+      const int64_t o1 = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift;
+      if (o1 - o0 != 1) ok = 0;
+      else s_hx1[i][q] = fmix64((uint64_t)checked(BU.ids[o0], U.card, a.validate, a.err) ^ salt);
+    }
+    s_ok[i] = ok;
+  }
+  __syncthreads();
+  for (int i = 0; i < GATHER_APT; i++) {
+    const int64_t li = base + threadIdx.x + i * 128;
+    if (li >= a.n) break;
+    const int64_t ad = a.a0 + li;
+    const int slot = a.req_of_ad[ad] == rfirst ? 0 : 1;
+    for (int i0 = 0; i0 < a.n_single; i0 += RB) {
+      int64_t row[RB];
+      int gi[RB];
+      bool fast[RB];
+      const T* tabs[RB];
+#pragma unroll
+      for (int t = 0; t < RB; t++) {
+        gi[t] = i0 + t < a.n_single ? i0 + t : -1;
+        row[t] = 0;
+        fast[t] = false;
+        if (gi[t] < 0) continue;
+        const int g = a.single_g[gi[t]];
+        const DevGroup G = a.groups[g];
+        tabs[t] = reinterpret_cast<const T*>(G.table);
+        if (G.side == 1) {
+          const BatchGroup& B = a.bv.g[g];
+          row[t] = checked(B.ids[ad - B.id_shift], G.card, a.validate, a.err);
+          fast[t] = true;
+        } else if (s_ok[gi[t]]) {
+          const DevGroup A = a.groups[G.ad_ref];
+          const BatchGroup& BA = a.bv.g[G.ad_ref];
+          const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
+          row[t] = cross_row_from_hx(s_hx1[gi[t]][slot], y, (uint64_t)G.card);
+          fast[t] = true;
+        }
+      }
+      RawRow<T, K> raw[RB];
+#pragma unroll
+      for (int t = 0; t < RB; t++)
+        if (fast[t]) raw[t].load(tabs[t], row[t]);
+#pragma unroll
+      for (int t = 0; t < RB; t++) {
+        if (gi[t] < 0) continue;
+        const int g = a.single_g[gi[t]];
+        const DevGroup G = a.groups[g];
+        float e[K];
+#pragma unroll
+        for (int d = 0; d < K; d++) e[d] = 0.0f;
+        if (fast[t]) {
+          raw[t].add_to(e);
+        } else {   // a request in the block has a user bag != 1: the general x-major cross sum
+          const DevGroup U = a.groups[G.user_ref];
+          const DevGroup A = a.groups[G.ad_ref];
+          const BatchGroup& BU = a.bv.g[G.user_ref];
+          const BatchGroup& BA = a.bv.g[G.ad_ref];
+          const uint64_t salt = cross_salt(g);
+          const int r = a.req_of_ad[ad];
+          const int64_t u0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
+          const int64_t u1 = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift;
+          const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
+          for (int64_t x = u0; x < u1; x++) {
+            const uint64_t hx = fmix64((uint64_t)checked(BU.ids[x], U.card, a.validate, a.err) ^ salt);
+            add_row<T, K>(reinterpret_cast<const T*>(G.table), cross_row_from_hx(hx, y, (uint64_t)G.card), e);
+          }
+        }
+        finish_ad<T, K, FAST>(a, G, g, li, e);
+      }
+    }
+  }
+}
+
+// APT: ads per thread (4 for large spans; 1 for small batches, where per-thread serial work is the latency)
+template <typename T, int K, bool FAST, int MINB = 4, int GATHER_APT = 4>
 __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
-  if ((int)blockIdx.y == a.n_ac) {          // the extra column: FC1's one-hot u1 operand rows
+  if (a.n_single > 0 && (int)blockIdx.y == a.n_ac) {
+    if constexpr ((K * (int)sizeof(T)) % 16 == 0) singles_column<T, K, FAST, GATHER_APT>(a);
+    return;
+  }
+  if ((int)blockIdx.y == a.n_ac + (a.n_single > 0 ? 1 : 0)) {   // FC1's one-hot u1 operand rows
     for (int i = 0; i < GATHER_APT; i++) {
       const int64_t l = (int64_t)blockIdx.x * (128 * GATHER_APT) + threadIdx.x + i * 128;
       if (l < a.n) write_ohot(a, l, a.bf16 ? 0x3F80u : 0x3C00u);
@@ -447,13 +573,24 @@ __global__ void rows_kernel(RowsArgs a) {
 // ---------------------------------------------------------------------------------------------
 template <typename T>
 static void user_dispatch(const UserArgs& a, int R, cudaStream_t s) {
-  size_t smem = (size_t)a.n_user * a.k * sizeof(float) + 16;
+  const size_t smem = ((size_t)a.n_user * a.k + 4) * sizeof(float) + (size_t)8 * 32 * a.k * sizeof(float);
+  // few requests (the latency path): split the u1 GEMV over up to 4 CTAs per request
+  const int slices = R >= 64 ? 1 : std::min(4, std::max(1, (a.H + 255) / 256));
+  const dim3 grid((unsigned)R, (unsigned)slices);
   switch (a.k) {
-    case 2: user_kernel<T, 2><<<R, 256, smem, s>>>(a); break;
-    case 4: user_kernel<T, 4><<<R, 256, smem, s>>>(a); break;
-    case 8: user_kernel<T, 8><<<R, 256, smem, s>>>(a); break;
-    case 16: user_kernel<T, 16><<<R, 256, smem, s>>>(a); break;
-    case 32: user_kernel<T, 32><<<R, 256, smem, s>>>(a); break;
+    case 2: user_kernel<T, 2><<<grid, 256, smem, s>>>(a); break;
+    case 4: user_kernel<T, 4><<<grid, 256, smem, s>>>(a); break;
+    case 8: user_kernel<T, 8><<<grid, 256, smem, s>>>(a); break;
+    case 16: user_kernel<T, 16><<<grid, 256, smem, s>>>(a); break;
+    case 32: {
+      static bool attr = false;
+      if (!attr) {   // 8 warps x 32 rows x 32 floats = 32 KB of staging + x_u
+        cudaFuncSetAttribute(user_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        attr = true;
+      }
+      user_kernel<T, 32><<<grid, 256, smem, s>>>(a);
+      break;
+    }
   }
 }
 
@@ -465,14 +602,17 @@ void launch_user(const UserArgs& a, int R, int precision, cudaStream_t s) {
 
 template <typename T, bool FAST>
 static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
-  dim3 grid((unsigned)((a.n + 128 * GATHER_APT - 1) / (128 * GATHER_APT)), (unsigned)(a.n_ac + (a.ohot ? 1 : 0)));
+  const unsigned gy = (unsigned)(a.n_ac + (a.n_single > 0 ? 1 : 0) + (a.ohot ? 1 : 0));
+  auto grid_for = [&](int apt) { return dim3((unsigned)((a.n + 128 * apt - 1) / (128 * apt)), gy); };
+  const dim3 grid = grid_for(GATHER_APT_BIG);
   switch (a.k) {
     case 2: gather_kernel<T, 2, FAST><<<grid, 128, 0, s>>>(a); break;
     case 4: gather_kernel<T, 4, FAST><<<grid, 128, 0, s>>>(a); break;
     case 8: gather_kernel<T, 8, FAST><<<grid, 128, 0, s>>>(a); break;
     case 16: {
       static const int minb = getenv("COLD_GATHER_MINB") ? atoi(getenv("COLD_GATHER_MINB")) : 8;
-      if (minb >= 8) gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
+      if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
+      else if (minb >= 8) gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
       else gather_kernel<T, 16, FAST><<<grid, 128, 0, s>>>(a);
       break;
     }
@@ -481,7 +621,7 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
 }
 
 void launch_gather(const GatherArgs& a, int precision, cudaStream_t s) {
-  if (a.n <= 0 || (a.n_ac <= 0 && !a.ohot)) return;
+  if (a.n <= 0 || (a.n_ac <= 0 && a.n_single <= 0 && !a.ohot)) return;
   if (precision == 0) gather_dispatch<float, false>(a, s);
   else if (precision == 1) gather_dispatch<__half, true>(a, s);
   else gather_dispatch<__nv_bfloat16, true>(a, s);

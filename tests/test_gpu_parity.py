@@ -123,8 +123,8 @@ def test_paper_stack_tensor_core(prec):
 
 @pytest.mark.parametrize("env", [{"COLD_TAIL": "2"}, {"COLD_TAIL": "1"}, {"COLD_TAIL": "0"}, {"COLD_PAIR": "2"},
                                  {"COLD_PAIR": "0", "COLD_RESB": "0"}, {"COLD_GSPAN": "1"}, {"COLD_GSPAN": "3"},
-                                 {"COLD_CHAIN": "0"}, {"COLD_CHAIN": "2"}, {"COLD_CHAIN": "0", "COLD_PAIR_RES": "0"},
-                                 {"COLD_CHAIN": "0", "COLD_U1MMA": "0"}])
+                                 {"COLD_CHAIN": "0"}, {"COLD_CHAIN_MIN": "0"}, {"COLD_CHAIN": "2", "COLD_CHAIN_MIN": "0"},
+                                 {"COLD_CHAIN": "0", "COLD_PAIR_RES": "0"}, {"COLD_CHAIN": "0", "COLD_U1MMA": "0"}])
 def test_kernel_variants_match_oracle(env, monkeypatch):
     """Every kernel variant the library can select (fused tail FC3-5 / FC4-5 / none, CTA-pair or
     single-CTA GEMMs, gather spans of 1 or 3 chunks) on several chunks with a ragged tail."""
@@ -134,6 +134,19 @@ def test_kernel_variants_match_oracle(env, monkeypatch):
     ctx = make_ctx(sch, params, chunk_ads=512)
     p, z = _oracle_scores(sch, params, batch)
     _check_scores(gpu_scores(ctx, batch), p, z, "f16", f"variant {env}")
+
+
+@pytest.mark.parametrize("prec", ["f16", "bf16"])
+def test_chain_kernel_many_blocks(prec, monkeypatch):
+    """The FC1->FC3 chain kernel (forced for every chunk size) over several chunks of 1280 ads with many
+    256-row blocks per CTA pair, requests crossing block boundaries, a ragged last block."""
+    monkeypatch.setenv("COLD_CHAIN_MIN", "0")
+    sizes = (3000, 17, 1, 2200, 900, 4000, 333)
+    sch, params, batch = small_case("paper", R=len(sizes), n_ads=sizes, precision=prec, cap=30000, seed=63)
+    for chunk in (0, 1280):
+        ctx = make_ctx(sch, params, chunk_ads=chunk)
+        p, z = _oracle_scores(sch, params, batch)
+        _check_scores(gpu_scores(ctx, batch), p, z, prec, f"chain {prec} chunk {chunk}")
 
 
 @pytest.mark.parametrize("prec", ["f16", "bf16"])
