@@ -56,15 +56,32 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
       if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t cum = 0;
-      int b = 255;
-      for (; b > 0; b--) {
-        if (cum + hist[b] >= need) break;
-        cum += hist[b];
+    if (threadIdx.x < 32) {
+      // warp 0 finds the bin b (scanning from 255 down) where the running count reaches `need`: lane L
+      // owns bins 255-8L .. 248-8L; an exclusive warp scan of the lane totals locates the lane, which
+      // then walks its 8 bins (was: one thread walking up to 256 bins)
+      const int L = threadIdx.x;
+      uint32_t cnt[8], tot = 0;
+#pragma unroll
+      for (int i = 0; i < 8; i++) { cnt[i] = hist[255 - 8 * L - i]; tot += cnt[i]; }
+      uint32_t incl = tot;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (L >= off) incl += v;
       }
-      s_prefix = prefix | ((uint32_t)b << shift);
-      s_need = need - cum;
+      const uint32_t excl = incl - tot;
+      const bool mine = excl < need && (incl >= need || L == 31);
+      if (mine) {
+        uint32_t cum = excl;
+        int b = 255 - 8 * L;
+        for (int i = 0; i < 8; i++, b--) {
+          if (cum + cnt[i] >= need || b == 0) break;
+          cum += cnt[i];
+        }
+        s_prefix = prefix | ((uint32_t)b << shift);
+        s_need = need - cum;
+      }
     }
     __syncthreads();
     prefix = s_prefix;
@@ -92,10 +109,18 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
     const uint32_t bal = __ballot_sync(0xffffffffu, eq);
     if (lane == 0) warp_sums[warp] = __popc(bal);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t run = s_eq_base;
-      for (int w = 0; w < TOPK_THREADS / 32; w++) { uint32_t c = warp_sums[w]; warp_sums[w] = run; run += c; }
-      s_eq_base = run;
+    if (threadIdx.x < 32) {   // exclusive scan of the 32 warp counts by warp 0
+      const uint32_t c = warp_sums[threadIdx.x];
+      uint32_t incl = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, off);
+        if ((int)threadIdx.x >= off) incl += v;
+      }
+      const uint32_t base = s_eq_base;
+      __syncwarp();
+      warp_sums[threadIdx.x] = base + incl - c;
+      if (threadIdx.x == 31) s_eq_base = base + incl;
     }
     __syncthreads();
     if (eq) {

@@ -283,8 +283,12 @@ def test_fp16_overflow_without_linear_log():
 
 # ---- host (pinned) batches: the e2e path ------------------------------------------------------
 
-@pytest.mark.parametrize("prec", ["f16", "f32"])
-def test_host_batch_equals_device_batch(prec):
+@pytest.mark.parametrize("prec,chain_min", [("f16", None), ("f32", None), ("f16", "0")])
+def test_host_batch_equals_device_batch(prec, chain_min, monkeypatch):
+    """Pinned-host inputs/outputs (staged per gather span on the copy stream) give the same scores as
+    device-resident ones; with COLD_CHAIN_MIN=0 the chain kernel runs every chunk."""
+    if chain_min is not None:
+        monkeypatch.setenv("COLD_CHAIN_MIN", chain_min)
     sch = bag_schema() if prec == "f32" else coldgen.scaled_schema(coldgen.schema_paper(), 20000)
     params = coldgen.make_params(sch, seed=101, precision=prec)
     batch = coldgen.make_batch(sch, 5, [300, 1, 257, 1000, 40], seed=102)
