@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--vps", action="store_true",
                     help="F4: the vector-product baseline (P:160-166) on the same request stream, ads/s")
     ap.add_argument("--vps-dim", type=int, default=64)
+    ap.add_argument("--latency-sweep", action="store_true",
+                    help="SURVEY §8(d) C2: p50/p95/p99 vs N, multi-stream serving (S contexts sharing one "
+                         "parameter copy), fp32 / fp16 / bf16 ads/s (the analogue of Table tab:qps_cuda)")
     return ap.parse_args()
 
 
@@ -367,10 +370,136 @@ def run_vps(args):
     print(json.dumps(line), flush=True)
 
 
+def run_latency_sweep(args):
+    """SURVEY §8(d) C2 measurements on one B200 (S-paper schema, LL on, K = 500):
+    (1) per-request latency vs N (one stream, requests back to back, device events);
+    (2) S concurrent streams, each with a cold_ctx_clone over the same parameters, closed loop:
+        aggregate ads/s and per-request p99 (the B200 stand-in for the paper's MPS, P:298);
+    (3) ads/s per compute precision at 512 requests x 4000 ads (Table tab:qps_cuda)."""
+    import torch
+    from paper_2007_16122_b200 import Batch, Context
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    sch = schema_for(args)
+    K = args.topk
+    nl = args.latency_requests
+    out = {"metric": METRIC, "unit": "ads/s", "n_gpus": 1, "data": "synthetic (seeded ids, tables, weights)",
+           "config": {"workload": "BASELINE configs[1] family: 1 user x N ads per request, S-paper, top-500"}}
+    params = coldgen.make_params(sch, seed=args.seed, precision="f16")
+    ctx = Context(sch.groups, sch.k, sch.widths, precision="f16", max_ads=10000, max_requests=1)
+    load_ctx_params(ctx, params)
+
+    def requests(n, count, base):
+        lb = coldgen.make_batch(sch, range(base, base + count), n, seed=args.seed + 5)
+        return [Batch.from_numpy(b.ad_offsets, b.ids, b.offs) for b in
+                (coldgen.sub_batch(lb, [i]) for i in range(count))]
+
+    # (1) latency vs N
+    sweep = []
+    for n in (300, 1000, 4000, 10000):
+        reqs = requests(n, nl, 4 * 10**7 + n)
+        sc = torch.empty(n, dtype=torch.float32, device=dev)
+        idx = torch.empty(K if n >= K else n, dtype=torch.int32, device=dev)
+        key = torch.empty(idx.numel(), dtype=torch.float32, device=dev)
+        ao = np.asarray([0, n], np.int32)
+        kk = idx.numel()
+        for r in reqs[:10]:
+            ctx.score_request(r, sc)
+            ctx.topk(sc, r.ad_offsets, ao, kk, idx, key)
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in reqs]
+        for (e0, e1), r in zip(evs, reqs):
+            e0.record()
+            ctx.score_request(r, sc)
+            ctx.topk(sc, r.ad_offsets, ao, kk, idx, key)
+            e1.record()
+        torch.cuda.synchronize()
+        lat = np.array([a.elapsed_time(b) for a, b in evs])
+        sweep.append({"n_ads": n, "top_k": kk, "p50_ms": float(np.percentile(lat, 50)),
+                      "p95_ms": float(np.percentile(lat, 95)), "p99_ms": float(np.percentile(lat, 99)),
+                      "ads_per_s": n / (float(lat.mean()) / 1e3)})
+    out["latency_vs_n"] = sweep
+    # (2) S streams, closed loop, N = 4000
+    n = 4000
+    reqs = requests(n, nl, 5 * 10**7)
+    ao = np.asarray([0, n], np.int32)
+    multi = []
+    for S in (1, 4, 8):
+        ctxs = [ctx] + [ctx.clone() for _ in range(S - 1)]
+        streams = [torch.cuda.Stream() for _ in range(S)]
+        bufs = [(torch.empty(n, dtype=torch.float32, device=dev), torch.empty(K, dtype=torch.int32, device=dev),
+                 torch.empty(K, dtype=torch.float32, device=dev)) for _ in range(S)]
+        per = [reqs[s::S] for s in range(S)]
+        for s in range(S):   # warm-up
+            with torch.cuda.stream(streams[s]):
+                for r in per[s][:3]:
+                    ctxs[s].score_request(r, bufs[s][0], stream=streams[s])
+                    ctxs[s].topk(bufs[s][0], r.ad_offsets, ao, K, bufs[s][1], bufs[s][2], stream=streams[s])
+        torch.cuda.synchronize()
+        evs = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in per[s]]
+               for s in range(S)]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for s in range(S):
+            streams[s].wait_event(t0)
+        for i in range(max(len(p) for p in per)):   # issue round-robin so the streams run concurrently
+            for s in range(S):
+                if i < len(per[s]):
+                    r = per[s][i]
+                    with torch.cuda.stream(streams[s]):
+                        evs[s][i][0].record(streams[s])
+                        ctxs[s].score_request(r, bufs[s][0], stream=streams[s])
+                        ctxs[s].topk(bufs[s][0], r.ad_offsets, ao, K, bufs[s][1], bufs[s][2], stream=streams[s])
+                        evs[s][i][1].record(streams[s])
+        torch.cuda.synchronize()
+        lat = np.array([a.elapsed_time(b) for s in range(S) for a, b in evs[s]])
+        total_ms = max(t0.elapsed_time(evs[s][-1][1]) for s in range(S))
+        multi.append({"streams": S, "requests": len(reqs), "ads_per_s": len(reqs) * n / (total_ms / 1e3),
+                      "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99))})
+        for c in ctxs[1:]:
+            c.close()
+    out["multi_stream_n4000"] = multi
+    ctx.close()
+    # (3) precision table at 512 x 4000
+    R, n = 512, 4000
+    batch = coldgen.make_batch(sch, range(R), n, seed=args.seed + 1)
+    prec_rows = []
+    for prec in ("f32", "f16", "bf16"):
+        pp = coldgen.make_params(sch, seed=args.seed, precision=prec)
+        c = Context(sch.groups, sch.k, sch.widths, precision=prec, max_ads=batch.n_ads, max_requests=R)
+        load_ctx_params(c, pp)
+        db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs)
+        sc = torch.empty(batch.n_ads, dtype=torch.float32, device=dev)
+        idx = torch.empty(R * K, dtype=torch.int32, device=dev)
+        key = torch.empty(R * K, dtype=torch.float32, device=dev)
+        for _ in range(2):
+            c.score_batch(db, sc)
+            c.topk(sc, db.ad_offsets, batch.ad_offsets, K, idx, key)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        steps = 3
+        for _ in range(steps):
+            c.score_batch(db, sc)
+            c.topk(sc, db.ad_offsets, batch.ad_offsets, K, idx, key)
+        e1.record()
+        e1.synchronize()
+        prec_rows.append({"precision": prec, "ads_per_s": steps * batch.n_ads / (e0.elapsed_time(e1) / 1e3),
+                          "fc_path": "fp32 FFMA (SIMT, no TF32)" if prec == "f32" else "tcgen05 fp32-accumulate"})
+        c.close()
+        del pp
+    out["precision"] = prec_rows
+    out["value"] = sweep[2]["ads_per_s"]
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.latency_sweep:
+        run_latency_sweep(args)
         return
     if args.vps:
         run_vps(args)

@@ -154,6 +154,12 @@ typedef struct {
 cold_status cold_create(const cold_config* config, cold_ctx** out);
 void cold_destroy(cold_ctx* ctx);
 
+/* A context for another stream that shares src's device parameters (no second copy of the tables)
+ * and owns its own workspace: the multi-stream serving form of the paper's MPS setup.
+ * src must outlive the clone; cold_load_params on a clone, or on src while clones exist, returns
+ * COLD_ERR_UNSUPPORTED. Clones of clones are refused (COLD_ERR_INVALID_ARG). */
+cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out);
+
 /* Upload parameters (synchronous). Replaces any previous version after all work already
  * queued on the ctx's streams (no call sees a mix of versions). */
 cold_status cold_load_params(cold_ctx* ctx, const cold_params* params, uint64_t* version_out);

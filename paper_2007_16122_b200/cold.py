@@ -27,7 +27,7 @@ STATUS = {0: "COLD_OK", 1: "COLD_ERR_INVALID_ARG", 2: "COLD_ERR_SHAPE", 3: "COLD
 EXPORTS = ["cold_create", "cold_destroy", "cold_load_params", "cold_score_batch", "cold_score_request",
            "cold_topk", "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
            "cold_status_string", "cold_last_error", "cold_profile", "cold_profile_read", "cold_se_stats",
-           "cold_select_groups", "cold_merge_topk", "cold_vps_score"]
+           "cold_select_groups", "cold_merge_topk", "cold_vps_score", "cold_ctx_clone"]
 PROF_KINDS = 3 + 16
 PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC = 0, 1, 2, 3
 
@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
                                       C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
         L.cold_vps_score.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
+        L.cold_ctx_clone.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
         L.cold_profile.argtypes = [C.c_void_p, C.c_int32]
         L.cold_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.cold_status_string.restype = C.c_char_p
@@ -109,7 +110,7 @@ def lib() -> C.CDLL:
         for f in ["cold_create", "cold_load_params", "cold_score_batch", "cold_score_request", "cold_topk",
                   "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
                   "cold_profile", "cold_profile_read", "cold_se_stats", "cold_select_groups",
-                  "cold_merge_topk", "cold_vps_score"]:
+                  "cold_merge_topk", "cold_vps_score", "cold_ctx_clone"]:
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -209,6 +210,16 @@ class Context:
         if self.ctx:
             lib().cold_destroy(self.ctx)
             self.ctx = C.c_void_p()
+
+    def clone(self) -> "Context":
+        """A context sharing this one's device parameters, with its own workspace (cold_ctx_clone):
+        one per concurrent stream. Keep this context alive while the clone is in use."""
+        c = Context.__new__(Context)
+        c.__dict__.update({k: v for k, v in self.__dict__.items() if k != "ctx"})
+        c.ctx = C.c_void_p()
+        c._source = self
+        _check(lib().cold_ctx_clone(self.ctx, C.byref(c.ctx)))
+        return c
 
     def __del__(self):
         try:

@@ -215,9 +215,13 @@ struct cold_ctx {
   double prof_ms[COLD_PROF_KINDS] = {0};
   int64_t prof_n[COLD_PROF_KINDS] = {0};
 
+  bool owns_params = true;           // false for cold_ctx_clone contexts (parameters shared)
+  cold_ctx* clone_of = nullptr;
+  int clones = 0;                    // live clones sharing this context's parameters
   ~cold_ctx() {
     cudaSetDevice(device);
     cudaDeviceSynchronize();
+    if (clone_of) clone_of->clones--;
     for (void* p : allocs) cudaFree(p);
     for (const CompAlloc& a : comp_allocs) comp_free(a);
     for (int i = 0; i < 2; i++) {
@@ -236,6 +240,10 @@ struct cold_ctx {
     cudaGetLastError();
   }
   void freeParams() {
+    if (!owns_params) {   // a clone only drops its references
+      d_tables.clear();
+      return;
+    }
     for (void* p : d_tables) cudaFree(p);
     d_tables.clear();
     void** ps[] = {(void**)&d_groups, (void**)&d_se_w, (void**)&d_se_b, (void**)&d_w1u_t, (void**)&d_b1,
@@ -607,6 +615,60 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
 
 extern "C" void cold_destroy(cold_ctx* c) { delete c; }
 
+// A second context over the same device parameters with its own workspace (one per concurrent
+// stream): the serving form of the paper's "MPS" multi-stream execution without duplicating
+// the 4.8 GB of tables.
+extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
+  if (!src || !out) return fail(COLD_ERR_INVALID_ARG, "null ctx / out");
+  *out = nullptr;
+  if (src->clone_of) return fail(COLD_ERR_INVALID_ARG, "clone the source context, not a clone");
+  cold_config cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.num_groups = src->M;
+  cfg.groups = src->groups.data();
+  cfg.emb_dim = src->k;
+  cfg.num_selected = (int32_t)src->sel.size();
+  cfg.selected = src->sel.data();
+  cfg.num_layers = src->L;
+  cfg.widths = src->widths.data();
+  cfg.activation = COLD_RELU;
+  cfg.linear_log = src->linear_log;
+  cfg.precision = src->precision;
+  cfg.device = src->device;
+  cfg.max_ads_per_call = src->max_ads;
+  cfg.max_requests_per_call = src->max_req;
+  cfg.chunk_ads = src->chunk;
+  cfg.flags = src->flags;
+  cold_ctx* c = nullptr;
+  cold_status s = cold_create(&cfg, &c);
+  if (s) return s;
+  c->owns_params = false;
+  c->clone_of = src;
+  src->clones++;
+  c->loaded = src->loaded;
+  c->version = src->version;
+  c->d_tables = src->d_tables;
+  c->d_groups = src->d_groups;
+  c->d_se_w = src->d_se_w;
+  c->d_se_b = src->d_se_b;
+  c->d_w1u_t = src->d_w1u_t;
+  c->d_b1 = src->d_b1;
+  c->d_head_w = src->d_head_w;
+  c->d_head_b = src->d_head_b;
+  c->d_in_scale = src->d_in_scale;
+  c->d_in_shift = src->d_in_shift;
+  for (int l = 0; l < COLD_MAX_LAYERS; l++) {
+    c->d_w[l] = src->d_w[l];
+    c->d_b[l] = src->d_b[l];
+    c->d_wt[l] = src->d_wt[l];
+    c->tmB[l] = src->tmB[l];
+  }
+  c->tmW4h = src->tmW4h;
+  c->tmW5h = src->tmW5h;
+  *out = c;
+  return COLD_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 // RNE fp32 -> fp16 / bf16 on the host (parameter upload only)
 static uint16_t f32_to_f16_bits(float f) {
@@ -654,6 +716,8 @@ static cold_status upload(cold_ctx* c, void** dst, size_t bytes, F fill) {
 
 extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint64_t* version_out) {
   if (!c || !p) return fail(COLD_ERR_INVALID_ARG, "null ctx/params");
+  if (!c->owns_params) return fail(COLD_ERR_UNSUPPORTED, "load parameters through the source context");
+  if (c->clones > 0) return fail(COLD_ERR_UNSUPPORTED, "destroy the clones before reloading parameters");
   if (!p->tables || !p->se_w || !p->se_b || !p->fc_w || !p->fc_b) return fail(COLD_ERR_PARAMS, "missing arrays");
   if (p->table_dtype != COLD_FP32 && p->table_dtype != c->precision)
     return fail(COLD_ERR_PARAMS, "table_dtype must be FP32 or the compute precision");
@@ -1039,7 +1103,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
       m.width[l] = c->widths[l];
       mw = std::max(mw, c->widths[l]);
     }
-    m.max_w = mw;
+    m.max_w = (mw + 3) / 4 * 4;   // float4 activation reads
     m.scores = scores_out;
     c->mark_begin(st);
     launch_mlp_f32(m, st);

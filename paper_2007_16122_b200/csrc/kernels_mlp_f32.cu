@@ -11,6 +11,10 @@ namespace cold {
 constexpr int MLP_TILE = 16;
 constexpr int MLP_THREADS = 256;
 
+// Register tiling: each thread owns 4 outputs (stride 64, so the 64 threads of a row group read
+// 4 x 64 consecutive weights) x 16 ads; per 4 inputs it loads 16 weights and 16 float4 activations
+// for 256 FFMAs (the naive one-output-per-thread loop was load-bound at 1 FFMA per load).
+// Accumulation order per (ad, output) is the input index order, as before.
 __global__ void __launch_bounds__(MLP_THREADS) mlp_f32_kernel(MlpF32Args a) {
   extern __shared__ float sm[];
   float* buf0 = sm;                                  // [TILE][max_w]
@@ -18,9 +22,9 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_f32_kernel(MlpF32Args a) {
   __shared__ int reqs[MLP_TILE];
   const int64_t t0 = (int64_t)blockIdx.x * MLP_TILE;
   const int nt = (int)(a.n - t0 < MLP_TILE ? a.n - t0 : MLP_TILE);
-  for (int i = threadIdx.x; i < MLP_TILE * a.d_ac; i += blockDim.x) {
-    int t = i / a.d_ac, c = i % a.d_ac;
-    buf0[t * a.max_w + c] = (t < nt) ? a.X[(t0 + t) * a.ldx + c] : 0.0f;
+  for (int i = threadIdx.x; i < MLP_TILE * a.max_w; i += blockDim.x) {
+    const int t = i / a.max_w, c = i % a.max_w;
+    buf0[i] = (t < nt && c < a.d_ac) ? a.X[(t0 + t) * a.ldx + c] : 0.0f;   // zero pad up to max_w
   }
   if (threadIdx.x < MLP_TILE) reqs[threadIdx.x] = (threadIdx.x < nt) ? a.req_of_ad[a.a0 + t0 + threadIdx.x] : 0;
   __syncthreads();
@@ -31,17 +35,57 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_f32_kernel(MlpF32Args a) {
     const int out = a.width[l];
     const float* wt = a.wt[l];
     const bool last = (l == a.L - 1);
-    for (int j = threadIdx.x; j < out; j += blockDim.x) {
-      float acc[MLP_TILE];
+    for (int jb = 0; jb < out; jb += 4 * MLP_THREADS) {      // 1024 outputs per pass
+      const int tx = threadIdx.x;
+      int js[4];
+      bool jv[4];
 #pragma unroll
-      for (int t = 0; t < MLP_TILE; t++) acc[t] = (l == 0) ? a.u1[(int64_t)reqs[t] * a.ld_u1 + j] : a.b[l][j];
-      for (int i = 0; i < in; i++) {
-        const float w = __ldg(wt + (int64_t)i * out + j);
+      for (int q = 0; q < 4; q++) {
+        // thread tx of warp-group g: outputs jb + 256 q + tx  (consecutive across threads: coalesced)
+        js[q] = jb + q * MLP_THREADS + tx;
+        jv[q] = js[q] < out;
+      }
+      if (!(jv[0] || jv[1] || jv[2] || jv[3])) continue;
+      float acc[4][MLP_TILE];
 #pragma unroll
-        for (int t = 0; t < MLP_TILE; t++) acc[t] = fmaf(w, h[t * a.max_w + i], acc[t]);
+      for (int q = 0; q < 4; q++) {
+#pragma unroll
+        for (int t = 0; t < MLP_TILE; t++)
+          acc[q][t] = jv[q] ? ((l == 0) ? a.u1[(int64_t)reqs[t] * a.ld_u1 + js[q]] : a.b[l][js[q]]) : 0.0f;
+      }
+      int i = 0;
+      for (; i + 4 <= in; i += 4) {
+        float w[4][4];
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) w[u][q] = jv[q] ? __ldg(wt + (int64_t)(i + u) * out + js[q]) : 0.0f;
+#pragma unroll
+        for (int t = 0; t < MLP_TILE; t++) {
+          const float4 hv = *reinterpret_cast<const float4*>(h + t * a.max_w + i);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            acc[q][t] = fmaf(w[0][q], hv.x, acc[q][t]);
+            acc[q][t] = fmaf(w[1][q], hv.y, acc[q][t]);
+            acc[q][t] = fmaf(w[2][q], hv.z, acc[q][t]);
+            acc[q][t] = fmaf(w[3][q], hv.w, acc[q][t]);
+          }
+        }
+      }
+      for (; i < in; i++) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const float w = jv[q] ? __ldg(wt + (int64_t)i * out + js[q]) : 0.0f;
+#pragma unroll
+          for (int t = 0; t < MLP_TILE; t++) acc[q][t] = fmaf(w, h[t * a.max_w + i], acc[q][t]);
+        }
       }
 #pragma unroll
-      for (int t = 0; t < MLP_TILE; t++) o[t * a.max_w + j] = last ? acc[t] : fmaxf(acc[t], 0.0f);
+      for (int q = 0; q < 4; q++) {
+        if (!jv[q]) continue;
+#pragma unroll
+        for (int t = 0; t < MLP_TILE; t++) o[t * a.max_w + js[q]] = last ? acc[q][t] : fmaxf(acc[q][t], 0.0f);
+      }
     }
     __syncthreads();
     float* tmp = h; h = o; o = tmp;

@@ -484,3 +484,32 @@ def test_input_batch_norm_variant(prec):
     p, z = oracle.score(oracle.Model(sch, params, linear_log=False,
                                      in_norm=(scale.astype(np.float64), shift.astype(np.float64))), batch)
     _check_scores(gpu_scores(ctx, batch), p, z, prec, f"input batch norm {prec}")
+
+
+# ---- multi-stream serving: contexts sharing one parameter copy ---------------------------------
+
+def test_ctx_clone_shares_params_and_runs_concurrently():
+    """cold_ctx_clone: clones score identically to the source on their own streams at the same time,
+    and parameter reloads are refused while clones exist."""
+    import torch
+    from paper_2007_16122_b200 import ColdError
+    sch, params, batch = small_case("paper", R=3, n_ads=(500, 64, 900), precision="f16", cap=20000, seed=71)
+    src = make_ctx(sch, params)
+    ref = gpu_scores(src, batch)
+    clones = [src.clone() for _ in range(3)]
+    db = device_batch(batch)
+    streams = [torch.cuda.Stream() for _ in clones]
+    outs = [torch.empty(batch.n_ads, dtype=torch.float32, device="cuda") for _ in clones]
+    for c, st, o in zip(clones, streams, outs):
+        with torch.cuda.stream(st):
+            c.score_batch(db, o, stream=st)
+    torch.cuda.synchronize()
+    for o in outs:
+        np.testing.assert_array_equal(o.cpu().numpy().astype(np.float64), ref)
+    with pytest.raises(ColdError):
+        load_params(src, params)
+    with pytest.raises(ColdError):
+        load_params(clones[0], params)
+    for c in clones:
+        c.close()
+    load_params(src, params)   # allowed again
