@@ -611,7 +611,10 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
     case 8: gather_kernel<T, 8, FAST><<<grid, 128, 0, s>>>(a); break;
     case 16: {
       static const int minb = getenv("COLD_GATHER_MINB") ? atoi(getenv("COLD_GATHER_MINB")) : 8;
+      static const int apt = getenv("COLD_GATHER_APT") ? atoi(getenv("COLD_GATHER_APT")) : 4;
       if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
+      else if (apt == 2) gather_kernel<T, 16, FAST, 8, 2><<<grid_for(2), 128, 0, s>>>(a);
+      else if (apt == 1) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);
       else if (minb >= 8) gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
       else gather_kernel<T, 16, FAST><<<grid, 128, 0, s>>>(a);
       break;

@@ -513,3 +513,39 @@ def test_ctx_clone_shares_params_and_runs_concurrently():
     for c in clones:
         c.close()
     load_params(src, params)   # allowed again
+
+
+def test_full_size_configs4_sampled():
+    """The bench.py workload itself: BASELINE configs[4] per GPU, 8192 requests x 10,000 ads (81.92 M ads,
+    541 chain-kernel chunks over 136 gather spans), default configuration, device-resident inputs as
+    bench.py times them. 384 ads sampled across the stream (first / middle / last requests and uniform
+    picks) are checked one by one against the fp64 oracle; the top-500 of 64 sampled requests is
+    checked for validity against the GPU scores."""
+    import torch
+    from paper_2007_16122_b200 import Batch, Context
+    sch = coldgen.schema_paper()
+    params = coldgen.make_params(sch, seed=1234, precision="f16")
+    batch = coldgen.make_batch(sch, range(8192), 10000, seed=1235)
+    ctx = Context(sch.groups, sch.k, sch.widths, precision="f16", max_ads=batch.n_ads, max_requests=batch.R)
+    load_params(ctx, params)
+    db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs)
+    out = torch.empty(batch.n_ads, dtype=torch.float32, device="cuda")
+    ctx.score_batch(db, out)
+    K = 500
+    idx = torch.empty(batch.R * K, dtype=torch.int32, device="cuda")
+    key = torch.empty(batch.R * K, dtype=torch.float32, device="cuda")
+    ctx.topk(out, db.ad_offsets, batch.ad_offsets, K, idx, key)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    rng = np.random.default_rng(11)
+    picks = np.concatenate([np.arange(64), batch.n_ads // 2 + np.arange(64), batch.n_ads - 64 + np.arange(64),
+                            rng.choice(batch.n_ads, 192, replace=False)])
+    sample = np.unique(picks)
+    p, z = oracle.score(oracle.Model(sch, params), batch, ad_list=sample)
+    _check_scores(got[sample].astype(np.float64), p, z, "f16", "configs[4] full size (sampled)")
+    ki, kk = idx.cpu().numpy().reshape(batch.R, K), key.cpu().numpy().reshape(batch.R, K)
+    for r in np.unique(np.concatenate([[0, batch.R - 1], rng.choice(batch.R, 62, replace=False)])):
+        seg = got[batch.ad_offsets[r]:batch.ad_offsets[r + 1]]
+        assert np.all(np.diff(kk[r]) <= 0)
+        np.testing.assert_array_equal(seg[ki[r]], kk[r])
+        assert (seg > kk[r, -1]).sum() <= K
