@@ -1129,6 +1129,10 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     cp.h1 = c->d_H[0];
     cp.h2 = c->d_H[1];
     {
+      static const bool h3ef = getenv("COLD_H3_EF") && atoi(getenv("COLD_H3_EF")) != 0;
+      cp.h3_evict_first = h3ef ? 1 : 0;
+    }
+    {
       static bool chain_instr = getenv("COLD_INSTR") != nullptr;
       if (chain_instr && !g_instr) {
         cudaMalloc(&g_instr, 8 * 8 * COLD_MAX_LAYERS);
@@ -1218,6 +1222,10 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     tp.head_b = c->d_head_b;
     tp.head_n = c->widths[c->L - 1];
     tp.scores = scores_out;
+    {
+      static const bool rev = !(getenv("COLD_TAIL_REV") && atoi(getenv("COLD_TAIL_REV")) == 0);
+      tp.reverse = rev ? 1 : 0;
+    }
     c->mark_begin(st);
     launch_tail45(tmA_of(l4), &c->tmB[l4], &c->tmB[l4 + 1], (int)n, c->precision == COLD_BF16 ? 1 : 0, tp,
                   c->num_sms, c->pdl && !c->prof, st);
@@ -1334,7 +1342,12 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
     }
     if (pl.host) CK(cudaEventRecord(c->ev_consumed[slot], st));
     if (mode == RUN_SCORE) {
-      for (int64_t a0 = s0; a0 < s1; a0 += chunk, ci++) {
+      // COLD_SPAN_REV=1: chunks of the span last-first (the last chunk's X rows are the ones most likely
+      // still in L2); measured neutral, so first-first by default
+      static const bool span_rev = getenv("COLD_SPAN_REV") && atoi(getenv("COLD_SPAN_REV")) != 0;
+      const int64_t nch = (s1 - s0 + chunk - 1) / chunk;
+      for (int64_t k = 0; k < nch; k++, ci++) {
+        const int64_t a0 = s0 + (span_rev ? nch - 1 - k : k) * chunk;
         const int64_t n = std::min(s1, a0 + chunk) - a0;
         const int oslot = (int)(ci & 1);
         float* out = scores_dev ? scores + a0 : c->d_scores_stage + (int64_t)oslot * chunk;

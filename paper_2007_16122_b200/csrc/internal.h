@@ -138,6 +138,8 @@ struct TailParams {
   const float* b3; const float* b4; const float* b5;
   const float* head_w; const float* head_b; int head_n;
   float* scores;                   // chunk-local [M]
+  int reverse;                     // tail45: walk tiles last-first (the most recently written H3 rows are
+                                   // the ones still in L2)
 };
 bool tail_supported(int n3, int n4, int n5, int k3);
 cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const CUtensorMap* tmB4,
@@ -156,6 +158,7 @@ struct ChainParams {
   const float* b4; const float* b5; const float* head_w; const float* head_b; int head_n;
   const void* h3; const void* h4;
   float* scores;                         // chunk-local [M]
+  int h3_evict_first;                    // H3 stores with an evict-first L2 hint (no TAIL)
   unsigned long long* instr;             // debug (nullable): wait cycles [0] producer empty, [1] producer
                                          // hready, [2] MMA full, [3] MMA tempty, [4] MMA uxfull, [5] epi tfull
 };

@@ -273,7 +273,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         const float* bias = l == 1 ? cp.b2 : (l == 2 ? cp.b3 : (l == 3 ? cp.b4 : nullptr));
         epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, 0u, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
                              nb * tn[l], trow0, q, h, lane, 0, nullptr, nullptr, 0, 0,
-                             (!TAIL && l == 2) ? pol_h3 : 0ull);
+                             (!TAIL && l == 2 && cp.h3_evict_first) ? pol_h3 : 0ull);
       }
       tc_fence_before();
       __syncwarp();

@@ -96,10 +96,11 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int tt = tp.reverse ? num_tiles - 1 - t : t;
         for (int kb = 0; kb < Q_K4 / BK; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], Q_A_BYTES);
-          tma_load_2d(sA + s * Q_A_BYTES, &tmA4, &full[s], kb * BK, t * BM, pol_a);
+          tma_load_2d(sA + s * Q_A_BYTES, &tmA4, &full[s], kb * BK, tt * BM, pol_a);
           if (++s == Q_STAGES) { s = 0; ph ^= 1; }
         }
       }
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, lt++) {
       epi4(lt);
       if (lt > 0) epi5(lt - 1, prev_tile);
-      prev_tile = t;
+      prev_tile = tp.reverse ? num_tiles - 1 - t : t;
     }
     if (lt > 0) epi5(lt - 1, prev_tile);
   }
