@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--latency-requests", type=int, default=1000)
+    ap.add_argument("--latency-requests", type=int, default=10000)
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--se-sweep", action="store_true",
                     help="BASELINE configs[3]: SE-selected group subsets of S-full, ads/s vs group count")
@@ -370,6 +370,125 @@ def run_vps(args):
     print(json.dumps(line), flush=True)
 
 
+def usable_rate(service_ms, limit_ms, seed=7):
+    """Highest Poisson arrival rate (requests/s) whose simulated open-loop p99 sojourn time stays
+    <= limit_ms (the paper's "usable QPS": at most 1% of responses over the limit), for one
+    FIFO server whose per-request service times are the measured device times `service_ms`.
+    Lindley recursion W_{i+1} = max(0, W_i + S_i - A_{i+1}); sojourn = W + S. Bisection on the rate."""
+    s = np.asarray(service_ms, np.float64)
+    gaps = np.random.default_rng(seed).exponential(1.0, size=s.size)   # unit-mean inter-arrival gaps
+
+    def p99(rate):
+        a = gaps * (1e3 / rate)   # ms
+        w, out = 0.0, np.empty_like(s)
+        for i in range(s.size):
+            out[i] = w + s[i]
+            if i + 1 < s.size:
+                w = max(0.0, w + s[i] - a[i + 1])
+        return float(np.percentile(out, 99))
+
+    if p99(1.0) > limit_ms:
+        return 0.0
+    lo, hi = 1.0, 1e3 / float(s.mean())   # stability bound: utilisation < 1
+    for _ in range(40):
+        mid = 0.5 * (lo + hi)
+        lo, hi = (mid, hi) if p99(mid) <= limit_ms else (lo, mid)
+    return lo
+
+
+def graph_latency(ctx, sch, n, count, K, seed, dist="uniform", dev=None):
+    """Per-request latency at N = n over `count` requests, each one a CUDA-graph replay of
+    cold_score_request + cold_topk on static device buffers (>= 10^4 sequential
+    requests, graph replay). Request i's ids are packed host-side into one int32 row of a device pool;
+    the timed region of every request is [one D2D copy of its row into the static buffers (ingest),
+    graph replay], bracketed by CUDA events on the replay stream."""
+    import torch
+    from paper_2007_16122_b200 import Batch
+    lb = coldgen.make_batch(sch, range(count), n, seed=seed, dist=dist)
+    # static layout: per USER group [L, ids (cap)], per single AD group [n ids]; bags padded to cap
+    layout, width = [], 0
+    for g, grp in enumerate(sch.groups):
+        if grp.side == coldgen.USER:
+            cap = 1 if not grp.pooled else grp.bag[1]
+            layout.append((g, "user", width, cap))
+            width += 2 + cap
+        elif grp.side == coldgen.AD:
+            if grp.pooled:
+                raise ValueError("graph_latency packs single-valued AD groups only")
+            layout.append((g, "ad", width, n))
+            width += n
+    pool = np.zeros((count, width), np.int32)
+    for g, kind, off, cap in layout:
+        if kind == "user":
+            o, v = lb.offs[g], lb.ids[g]
+            for i in range(count):
+                L = int(o[i + 1] - o[i])
+                pool[i, off] = 0
+                pool[i, off + 1] = L
+                pool[i, off + 2:off + 2 + L] = v[o[i]:o[i + 1]]
+        else:
+            pool[:, off:off + n] = lb.ids[g].reshape(count, n)
+    d_pool = torch.from_numpy(pool).to(dev)
+    static = torch.empty(width, dtype=torch.int32, device=dev)
+    static.copy_(d_pool[0])
+    ids, offs = [None] * sch.M, [None] * sch.M
+    for g, kind, off, cap in layout:
+        if kind == "user":
+            offs[g] = static[off:off + 2]
+            ids[g] = static[off + 2:off + 2 + cap]
+        else:
+            ids[g] = static[off:off + n]
+    ao = np.asarray([0, n], np.int32)
+    d_ao = torch.from_numpy(ao).to(dev)
+    sb = Batch(d_ao, ids, offs, ad_offsets_host=ao,
+               offs_host=[None if o is None else np.asarray([0, 1], np.int32) for o in offs])
+    kk = min(K, n)
+    sc = torch.empty(n, dtype=torch.float32, device=dev)
+    idx = torch.empty(kk, dtype=torch.int32, device=dev)
+    key = torch.empty(kk, dtype=torch.float32, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):   # warm-up outside capture: sizes the library's lazily grown buffers
+            ctx.score_request(sb, sc, stream=s)
+            ctx.topk(sc, d_ao, ao, kk, idx, key, stream=s)
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        ctx.score_request(sb, sc, stream=s)
+        ctx.topk(sc, d_ao, ao, kk, idx, key, stream=s)
+    # parity of the replay against a direct call on request 1
+    with torch.cuda.stream(s):
+        static.copy_(d_pool[1])
+        graph.replay()
+        g_idx = idx.clone()
+        ctx.score_request(sb, sc, stream=s)
+        ctx.topk(sc, d_ao, ao, kk, idx, key, stream=s)
+    s.synchronize()
+    replay_ok = bool(torch.equal(g_idx, idx))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(count)]
+    with torch.cuda.stream(s):
+        for i in range(min(20, count)):
+            static.copy_(d_pool[i])
+            graph.replay()
+        for i in range(count):
+            evs[i][0].record(s)
+            static.copy_(d_pool[i])
+            graph.replay()
+            evs[i][1].record(s)
+    s.synchronize()
+    lat = np.array([a.elapsed_time(b) for a, b in evs])
+    del graph
+    return {"n_ads": n, "top_k": kk, "requests": count, "ids": dist, "p50_ms": float(np.percentile(lat, 50)),
+            "p95_ms": float(np.percentile(lat, 95)), "p99_ms": float(np.percentile(lat, 99)),
+            "mean_ms": float(lat.mean()), "ads_per_s": n / (float(lat.mean()) / 1e3),
+            "usable_rps_p99_le_1ms": usable_rate(lat, 1.0), "usable_rps_p99_le_10ms": usable_rate(lat, 10.0),
+            "replay_matches_direct_call": replay_ok,
+            "timing": "CUDA-graph replay of score_request + top-K per request (ingest = one D2D copy of the "
+                      "request's packed ids, inside the timed region), device events, one stream; usable_rps: "
+                      "Lindley-recursion open-loop Poisson arrivals over these measured service times (P:442 rule)"}
+
+
 def run_latency_sweep(args):
     """SURVEY §8(d) C2 measurements on one B200 (S-paper schema, LL on, K = 500):
     (1) per-request latency vs N (one stream, requests back to back, device events);
@@ -394,34 +513,19 @@ def run_latency_sweep(args):
         return [Batch.from_numpy(b.ad_offsets, b.ids, b.offs) for b in
                 (coldgen.sub_batch(lb, [i]) for i in range(count))]
 
-    # (1) latency vs N
+    # (1) latency vs N: >= 10^4 sequential CUDA-graph replays per N (uniform ids), Zipf(1.05) at 4000
     sweep = []
     for n in (300, 1000, 4000, 10000):
-        reqs = requests(n, nl, 4 * 10**7 + n)
-        sc = torch.empty(n, dtype=torch.float32, device=dev)
-        idx = torch.empty(K if n >= K else n, dtype=torch.int32, device=dev)
-        key = torch.empty(idx.numel(), dtype=torch.float32, device=dev)
-        ao = np.asarray([0, n], np.int32)
-        kk = idx.numel()
-        for r in reqs[:10]:
-            ctx.score_request(r, sc)
-            ctx.topk(sc, r.ad_offsets, ao, kk, idx, key)
-        torch.cuda.synchronize()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in reqs]
-        for (e0, e1), r in zip(evs, reqs):
-            e0.record()
-            ctx.score_request(r, sc)
-            ctx.topk(sc, r.ad_offsets, ao, kk, idx, key)
-            e1.record()
-        torch.cuda.synchronize()
-        lat = np.array([a.elapsed_time(b) for a, b in evs])
-        sweep.append({"n_ads": n, "top_k": kk, "p50_ms": float(np.percentile(lat, 50)),
-                      "p95_ms": float(np.percentile(lat, 95)), "p99_ms": float(np.percentile(lat, 99)),
-                      "ads_per_s": n / (float(lat.mean()) / 1e3)})
+        r = graph_latency(ctx, sch, n, nl, K, seed=args.seed + 5 + n, dist="uniform", dev=dev)
+        r.pop("timing")
+        sweep.append(r)
+    r = graph_latency(ctx, sch, 4000, nl, K, seed=args.seed + 5, dist="zipf", dev=dev)
+    out["latency_timing"] = r.pop("timing")
+    sweep.append(r)
     out["latency_vs_n"] = sweep
     # (2) S streams, closed loop, N = 4000
     n = 4000
-    reqs = requests(n, nl, 5 * 10**7)
+    reqs = requests(n, min(nl, 2000), 5 * 10**7)
     ao = np.asarray([0, n], np.int32)
     multi = []
     for S in (1, 4, 8):
@@ -695,28 +799,38 @@ def main():
     latency = None
     if not args.no_latency and rank == 0:
         nl = args.latency_requests
-        lb = coldgen.make_batch(sch, range(10**7, 10**7 + nl), 4000, seed=args.seed + 1)
+        # >= 10^4 sequential requests, CUDA-graph replay, uniform and Zipf(1.05) ids
+        try:
+            latency = graph_latency(ctx, sch, 4000, nl, K, seed=args.seed + 1, dist="uniform", dev=dev)
+            latency["zipf"] = {k: v for k, v in graph_latency(ctx, sch, 4000, nl, K, seed=args.seed + 1,
+                                                              dist="zipf", dev=dev).items() if k != "timing"}
+        except Exception as exc:   # optional section: report, keep the headline line
+            latency = {"error": f"{type(exc).__name__}: {exc}"}
+        # direct library calls (no graph), requests back to back
+        nd = min(nl, 1000)
+        lb = coldgen.make_batch(sch, range(10**7, 10**7 + nd), 4000, seed=args.seed + 1)
         singles = [Batch.from_numpy(s.ad_offsets, s.ids, s.offs) for s in
-                   (coldgen.sub_batch(lb, [i]) for i in range(nl))]
+                   (coldgen.sub_batch(lb, [i]) for i in range(nd))]
         lscores = torch.empty(4000, dtype=torch.float32, device=dev)
         lidx = torch.empty(K, dtype=torch.int32, device=dev)
         lkey = torch.empty(K, dtype=torch.float32, device=dev)
         ao = np.asarray([0, 4000], np.int32)
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
-        for i in range(min(10, nl)):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nd)]
+        for i in range(min(10, nd)):
             ctx.score_request(singles[i], lscores)
             ctx.topk(lscores, singles[i].ad_offsets, ao, K, lidx, lkey)
         torch.cuda.synchronize()
-        for i in range(nl):
+        for i in range(nd):
             evs[i][0].record(stream)
             ctx.score_request(singles[i], lscores)
             ctx.topk(lscores, singles[i].ad_offsets, ao, K, lidx, lkey)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
         lat = np.array([a.elapsed_time(b) for a, b in evs])
-        latency = {"n_ads": 4000, "requests": nl, "p50_ms": float(np.percentile(lat, 50)),
-                   "p99_ms": float(np.percentile(lat, 99)), "mean_ms": float(lat.mean()),
-                   "timing": "device events per request (score + top-500), requests back to back on one stream"}
+        latency["direct_calls"] = {"requests": nd, "p50_ms": float(np.percentile(lat, 50)),
+                                   "p99_ms": float(np.percentile(lat, 99)), "mean_ms": float(lat.mean()),
+                                   "timing": "device events per request (score + top-500), direct library calls "
+                                             "back to back on one stream"}
 
     # ---- F1: one request's ads split across all ranks (world > 1), per-rank top-K, NCCL all-gather
     # of the candidate lists, cold_merge_topk; p50 / p99 per request at N = args.ads ----
