@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--vps", action="store_true",
                     help="F4: the vector-product baseline (P:160-166) on the same request stream, ads/s")
     ap.add_argument("--vps-dim", type=int, default=64)
+    ap.add_argument("--se-dense", action="store_true",
+                    help="F2: the dense SE reading (AMB-1, P:229-234 Doc B) on the same workload")
     ap.add_argument("--latency-sweep", action="store_true",
                     help="SURVEY §8(d) C2: p50/p95/p99 vs N, multi-stream serving (S contexts sharing one "
                          "parameter copy), fp32 / fp16 / bf16 ads/s (the analogue of Table tab:qps_cuda)")
@@ -160,12 +162,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def load_ctx_params(ctx, params):
+def load_ctx_params(ctx, params, se_dense=None):
     tables = params.tables
     tdt = params.table_dtype
     if tdt == "f16":
         tables = [t.view(np.uint16) for t in tables]
-    ctx.load_params(tables, params.se_w, params.se_b, params.fc_w, params.fc_b, table_dtype=tdt)
+    ctx.load_params(tables, params.se_w, params.se_b, params.fc_w, params.fc_b, table_dtype=tdt, se_dense=se_dense)
+
+
+def dense_se_params(sch, seed):
+    """Dense SE gate (AMB-1 Doc B reading): W [M, M k] ~ U(-0.05, 0.05), b [M] ~ U(-1, 1), seeded."""
+    rng = np.random.default_rng(seed)
+    return (rng.uniform(-0.05, 0.05, (sch.M, sch.M * sch.k)).astype(np.float32),
+            rng.uniform(-1, 1, sch.M).astype(np.float32))
 
 
 # --------------------------------------------------------------------------------------------
@@ -231,7 +240,9 @@ def config_dict(args, sch):
                         + "x".join(map(str, sch.widths)) + f", {args.precision} + linear_log, top-K={args.topk})",
             "requests_per_gpu": args.requests, "ads_per_request": args.ads, "top_k": args.topk,
             "ids": "uniform", "l2": "inputs larger than L2 (ids 2.6 GB + tables 4.8 GB per GPU); no flush",
-            "parallelism": f"request partition x{args.gpus}, replicated params"}
+            "parallelism": f"request partition x{args.gpus}, replicated params",
+            "se": "dense (AMB-1 Doc B reading, user block not hoisted)" if getattr(args, "se_dense", False)
+                  else "per-group (AMB-1)"}
 
 
 # --------------------------------------------------------------------------------------------
@@ -614,7 +625,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2007_16122_b200 import Batch, Context
-    from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER, PROF_TOPK, PROF_USER
+    from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER, PROF_SE_DENSE, PROF_TOPK, PROF_USER
     from paper_2007_16122_b200.dist import gather_topk, request_block
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -631,8 +642,8 @@ def main():
     batch = coldgen.make_batch(sch, request_block(args.requests, rank), args.ads, seed=args.seed + 1)
     N = batch.n_ads
     ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, device=local, max_ads=N,
-                  max_requests=args.requests, chunk_ads=args.chunk)
-    load_ctx_params(ctx, params)
+                  max_requests=args.requests, chunk_ads=args.chunk, se_mode="dense" if args.se_dense else "group")
+    load_ctx_params(ctx, params, dense_se_params(sch, args.seed + 17) if args.se_dense else None)
     db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs)
     K = args.topk
     scores = torch.empty(N, dtype=torch.float32, device=dev)
@@ -702,7 +713,7 @@ def main():
     d_ac = info["d_ad"]
     layer_flops = fc_flops_per_ad(sch, d_ac)
     per_kernel = {}
-    names = {PROF_USER: "user", PROF_GATHER: "gather", PROF_TOPK: "topk"}
+    names = {PROF_USER: "user", PROF_GATHER: "gather", PROF_TOPK: "topk", PROF_SE_DENSE: "se_dense"}
     n_layers = len(sch.widths)
     # a profiled FC kind covers its layer up to the next kind that launched (fused kernels);
     # the last one also covers the head

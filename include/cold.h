@@ -100,7 +100,16 @@ typedef struct {
   int32_t max_requests_per_call; /* capacity: requests in one call */
   int32_t chunk_ads;             /* ads per pipeline chunk (0 = library default) */
   uint32_t flags;                /* COLD_VALIDATE_IDS */
+  int32_t se_mode;               /* COLD_SE_GROUP (0, default): s_g = sigma(w_g . e_g + b_g), one k-vector
+                                    per group (DESIGN.md AMB-1, Doc A). COLD_SE_DENSE (1): the
+                                    other reading of P:229-234 (Doc B), s = sigma(W [e_1 .. e_M] + b) with
+                                    W [n_sel x D_in] over the whole LL'd concat: s_g then depends on the ad,
+                                    so the user block is no longer hoisted into u1 (FC1 runs over all D_in
+                                    columns; cold_params.se_w_dense / se_b_dense are required, se_w / se_b
+                                    are ignored). Not with cold_se_stats (COLD_ERR_UNSUPPORTED). */
 } cold_config;
+
+enum { COLD_SE_GROUP = 0, COLD_SE_DENSE = 1 };
 
 /* Model parameters. All pointers are HOST memory; cold_load_params copies them
  * synchronously, so the caller may free them on return. */
@@ -123,6 +132,11 @@ typedef struct {
    * groups; both NULL = none. Usually paired with linear_log = 0 (the paper's other choice). */
   const float* in_scale;
   const float* in_shift;
+  /* se_mode == COLD_SE_DENSE only (NULL otherwise): row j = output s_j of the j-th selected group
+   * (schema order), columns = the D_in concat of the selected groups' linear_log'ed embeddings in
+   * schema order; fp32, kept fp32 on the device (the gate is computed with fp32 FFMA). */
+  const float* se_w_dense;       /* [n_sel x D_in] */
+  const float* se_b_dense;       /* [n_sel] */
 } cold_params;
 
 /* One call's requests. Column-major per group ("column based computation"). */
@@ -230,7 +244,7 @@ cold_status cold_select_groups(const double* mean_s, int32_t M, int32_t K, int32
 
 /* Kernel classes reported by cold_profile_read. */
 enum { COLD_PROF_USER = 0, COLD_PROF_GATHER = 1, COLD_PROF_TOPK = 2, COLD_PROF_FC = 3 /* + layer */,
-       COLD_PROF_KINDS = 3 + 16 };
+       COLD_PROF_SE_DENSE = 3 + 16 /* the dense SE gate kernel */, COLD_PROF_KINDS = 3 + 16 + 1 };
 
 /* enable = 1: reset counters and record a CUDA event pair around every kernel the library
  * launches (on the launching stream); enable = 0: stop recording. */

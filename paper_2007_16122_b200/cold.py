@@ -28,8 +28,8 @@ EXPORTS = ["cold_create", "cold_destroy", "cold_load_params", "cold_score_batch"
            "cold_topk", "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
            "cold_status_string", "cold_last_error", "cold_profile", "cold_profile_read", "cold_se_stats",
            "cold_select_groups", "cold_merge_topk", "cold_vps_score", "cold_ctx_clone"]
-PROF_KINDS = 3 + 16
-PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC = 0, 1, 2, 3
+PROF_KINDS = 3 + 16 + 1
+PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC, PROF_SE_DENSE = 0, 1, 2, 3, 3 + 16
 
 
 class ColdError(RuntimeError):
@@ -50,14 +50,15 @@ class cold_config(C.Structure):
                 ("num_layers", C.c_int32), ("widths", C.POINTER(C.c_int32)),
                 ("activation", C.c_int32), ("linear_log", C.c_int32), ("precision", C.c_int32),
                 ("device", C.c_int32), ("max_ads_per_call", C.c_int64), ("max_requests_per_call", C.c_int32),
-                ("chunk_ads", C.c_int32), ("flags", C.c_uint32)]
+                ("chunk_ads", C.c_int32), ("flags", C.c_uint32), ("se_mode", C.c_int32)]
 
 
 class cold_params(C.Structure):
     _fields_ = [("table_dtype", C.c_int32), ("tables", C.POINTER(C.c_void_p)),
                 ("se_w", C.c_void_p), ("se_b", C.c_void_p),
                 ("fc_w", C.POINTER(C.c_void_p)), ("fc_b", C.POINTER(C.c_void_p)),
-                ("in_scale", C.c_void_p), ("in_shift", C.c_void_p)]
+                ("in_scale", C.c_void_p), ("in_shift", C.c_void_p),
+                ("se_w_dense", C.c_void_p), ("se_b_dense", C.c_void_p)]
 
 
 class cold_batch(C.Structure):
@@ -183,7 +184,8 @@ class Context:
 
     def __init__(self, groups, emb_dim: int, widths: Sequence[int], precision: str = "f16",
                  selected: Optional[Sequence[int]] = None, linear_log: bool = True, device: int = 0,
-                 max_ads: int = 1 << 20, max_requests: int = 1024, chunk_ads: int = 0, validate_ids: bool = False):
+                 max_ads: int = 1 << 20, max_requests: int = 1024, chunk_ads: int = 0, validate_ids: bool = False,
+                 se_mode: str = "group"):
         L = lib()
         M = len(groups)
         self._groups = (cold_group * M)()
@@ -201,6 +203,7 @@ class Context:
         cfg.precision, cfg.device = PRECISION[precision], device
         cfg.max_ads_per_call, cfg.max_requests_per_call = max_ads, max_requests
         cfg.chunk_ads, cfg.flags = chunk_ads, VALIDATE_IDS if validate_ids else 0
+        cfg.se_mode = {"group": 0, "dense": 1}[se_mode]   # AMB-1 readings (include/cold.h)
         self.precision = precision
         self.device = device
         self.ctx = C.c_void_p()
@@ -228,10 +231,11 @@ class Context:
             pass
 
     def load_params(self, tables, se_w, se_b, fc_w, fc_b, table_dtype: str = "f32", in_scale=None,
-                    in_shift=None) -> int:
+                    in_shift=None, se_dense=None) -> int:
         """Host arrays: tables[g] [card, k] (float32, or uint16/float16 bit patterns in the compute
         precision), se_w [M, k], se_b [M], fc_w[l] [out, in], fc_b[l] [out] (float32); optional folded
-        input batch norm in_scale / in_shift [D_in] (float32)."""
+        input batch norm in_scale / in_shift [D_in] (float32); se_dense = (W [n_sel, D_in], b [n_sel])
+        for a se_mode="dense" context."""
         keep = [np.ascontiguousarray(t) for t in tables]
         sw = np.ascontiguousarray(se_w, np.float32)
         sb = np.ascontiguousarray(se_b, np.float32)
@@ -242,9 +246,14 @@ class Context:
         bp = (C.c_void_p * len(bs))(*[b.ctypes.data for b in bs])
         isc = None if in_scale is None else np.ascontiguousarray(in_scale, np.float32)
         ish = None if in_shift is None else np.ascontiguousarray(in_shift, np.float32)
+        sdw = sdb = None
+        if se_dense is not None:
+            sdw = np.ascontiguousarray(se_dense[0], np.float32)
+            sdb = np.ascontiguousarray(se_dense[1], np.float32)
         p = cold_params(PRECISION[table_dtype], C.cast(tp, C.POINTER(C.c_void_p)), sw.ctypes.data, sb.ctypes.data,
                         C.cast(wp, C.POINTER(C.c_void_p)), C.cast(bp, C.POINTER(C.c_void_p)),
-                        None if isc is None else isc.ctypes.data, None if ish is None else ish.ctypes.data)
+                        None if isc is None else isc.ctypes.data, None if ish is None else ish.ctypes.data,
+                        None if sdw is None else sdw.ctypes.data, None if sdb is None else sdb.ctypes.data)
         v = C.c_uint64()
         _check(lib().cold_load_params(self.ctx, C.byref(p), C.byref(v)))
         return v.value

@@ -138,6 +138,8 @@ struct cold_ctx {
   std::vector<int> sel, widths, sel_user, sel_ac, sel_pos;
   std::vector<int> gather_order;     // sel_ac positions, heaviest (cross over a user bag) first
   int d_u = 0, d_ac = 0, d_ac_pad = 0, d_in = 0;
+  bool dense_se = false;             // COLD_SE_DENSE: X holds all D_in columns (schema order), u1 = b1
+  int d_x = 0;                       // X width before padding: d_ac (per-group SE) or d_in (dense SE)
   int64_t max_ads = 0;
   int max_req = 0, chunk = 0, num_sms = 148;
   bool tensor = false;
@@ -158,10 +160,13 @@ struct cold_ctx {
   float* d_head_b = nullptr;
   float* d_in_scale = nullptr;       // folded input batch norm [D_in] (nullable)
   float* d_in_shift = nullptr;
+  float* d_sewd_t = nullptr;         // dense SE: Wd^T [D_in][n_sel] fp32
+  float* d_sebd = nullptr;           // dense SE: bd [n_sel]
   CUtensorMap tmB[COLD_MAX_LAYERS];
   // ---- workspace ----
   float* d_u1 = nullptr;
   float* d_xu = nullptr;
+  float* d_E = nullptr;              // dense SE: [gspan * chunk][d_in] fp32 pre-SE ê of the span
   int32_t* d_req = nullptr;
   void* d_X = nullptr;
   void* d_H[COLD_MAX_LAYERS] = {nullptr};
@@ -247,7 +252,8 @@ struct cold_ctx {
     for (void* p : d_tables) cudaFree(p);
     d_tables.clear();
     void** ps[] = {(void**)&d_groups, (void**)&d_se_w, (void**)&d_se_b, (void**)&d_w1u_t, (void**)&d_b1,
-                   (void**)&d_head_w, (void**)&d_head_b, (void**)&d_in_scale, (void**)&d_in_shift};
+                   (void**)&d_head_w, (void**)&d_head_b, (void**)&d_in_scale, (void**)&d_in_shift,
+                   (void**)&d_sewd_t, (void**)&d_sebd};
     for (void** p : ps) { if (*p) cudaFree(*p); *p = nullptr; }
     for (int l = 0; l < COLD_MAX_LAYERS; l++) {
       if (d_w[l]) cudaFree(d_w[l]);
@@ -449,6 +455,13 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   c->d_u = (int)c->sel_user.size() * c->k;
   c->d_ac = (int)c->sel_ac.size() * c->k;
   c->d_in = c->d_u + c->d_ac;
+  if (cfg->se_mode != COLD_SE_GROUP && cfg->se_mode != COLD_SE_DENSE) { delete c; return fail(COLD_ERR_INVALID_ARG, "se_mode"); }
+  c->dense_se = cfg->se_mode == COLD_SE_DENSE;
+  c->d_x = c->dense_se ? c->d_in : c->d_ac;
+  if (c->dense_se && se_dense_smem(c->d_in, (int)c->sel.size()) > 227 * 1024 - 1024) {
+    delete c;
+    return fail(COLD_ERR_UNSUPPORTED, "dense SE: Wd^T (D_in x n_sel fp32) must fit in shared memory");
+  }
   c->max_ads = cfg->max_ads_per_call;
   c->max_req = cfg->max_requests_per_call;
 
@@ -471,9 +484,9 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       return fail(COLD_ERR_UNSUPPORTED, "last hidden width must be 64, 128 or 256");
     }
     for (int l = 0; l < c->L - 1; l++) c->bn[l] = (l == c->L - 2) ? pen : pick_bn(c->widths[l]);
-    c->d_ac_pad = std::max(64, (c->d_ac + 63) / 64 * 64);
+    c->d_ac_pad = std::max(64, (c->d_x + 63) / 64 * 64);
   } else {
-    c->d_ac_pad = std::max(1, c->d_ac);
+    c->d_ac_pad = std::max(1, c->d_x);
   }
   int chunk = cfg->chunk_ads > 0 ? cfg->chunk_ads : c->num_sms * 128 * 8;
   if (c->tensor) chunk = (chunk + 127) / 128 * 128;
@@ -500,6 +513,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   const char* env_comp = getenv("COLD_COMPRESS");
   const bool want_comp = c->tensor && env_comp && atoi(env_comp) != 0;
   e = e ? e : c->alloc_act((void**)&c->d_X, x_rows * c->d_ac_pad * c->elem(), want_comp);
+  if (c->dense_se) e = e ? e : c->alloc((void**)&c->d_E, x_rows * c->d_in * 4);
   e = e ? e : c->alloc((void**)&c->d_err, 16);
   e = e ? e : c->alloc((void**)&c->d_scores_stage, (size_t)2 * c->chunk * 4);
   e = e ? e : c->alloc((void**)&c->d_adoff, (size_t)(c->max_req + 1) * 4);
@@ -639,6 +653,7 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
   cfg.max_requests_per_call = src->max_req;
   cfg.chunk_ads = src->chunk;
   cfg.flags = src->flags;
+  cfg.se_mode = src->dense_se ? COLD_SE_DENSE : COLD_SE_GROUP;
   cold_ctx* c = nullptr;
   cold_status s = cold_create(&cfg, &c);
   if (s) return s;
@@ -657,6 +672,8 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
   c->d_head_b = src->d_head_b;
   c->d_in_scale = src->d_in_scale;
   c->d_in_shift = src->d_in_shift;
+  c->d_sewd_t = src->d_sewd_t;
+  c->d_sebd = src->d_sebd;
   for (int l = 0; l < COLD_MAX_LAYERS; l++) {
     c->d_w[l] = src->d_w[l];
     c->d_b[l] = src->d_b[l];
@@ -779,7 +796,20 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
     s = upload(c, (void**)&c->d_in_shift, sizeof(float) * c->d_in, [&](uint8_t* h) { memcpy(h, p->in_shift, sizeof(float) * c->d_in); });
     if (s) return s;
   }
+  if (c->dense_se) {   // Wd^T [D_in][n_sel] and bd, fp32
+    if (!p->se_w_dense || !p->se_b_dense) return fail(COLD_ERR_PARAMS, "se_mode dense needs se_w_dense and se_b_dense");
+    const int ns = (int)c->sel.size();
+    s = upload(c, (void**)&c->d_sewd_t, sizeof(float) * (size_t)c->d_in * ns, [&](uint8_t* h) {
+      float* o = (float*)h;
+      for (int j = 0; j < ns; j++)
+        for (int i = 0; i < c->d_in; i++) o[(size_t)i * ns + j] = p->se_w_dense[(size_t)j * c->d_in + i];
+    });
+    if (s) return s;
+    s = upload(c, (void**)&c->d_sebd, sizeof(float) * ns, [&](uint8_t* h) { memcpy(h, p->se_b_dense, sizeof(float) * ns); });
+    if (s) return s;
+  }
   // FC1 split into the per-request user block (fp32, transposed) and the ad+cross block
+  // (dense SE: no split; the whole W1 multiplies the per-ad X, schema order)
   const int W0 = c->widths[0];
   const float* W1 = p->fc_w[0];   // [W0][d_in], columns = selected groups in schema order
   const int d_in = c->d_in;
@@ -806,7 +836,8 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
             float v = 0.0f;
             if (l == 0) {
               int j = kk / k, d = kk % k;
-              if (j < (int)c->sel_ac.size()) v = W[(size_t)n * d_in + col_of(c->sel_ac[j], d)];
+              if (c->dense_se) { if (kk < d_in) v = W[(size_t)n * d_in + kk]; }
+              else if (j < (int)c->sel_ac.size()) v = W[(size_t)n * d_in + col_of(c->sel_ac[j], d)];
             } else {
               v = W[(size_t)n * Kp + kk];
             }
@@ -834,14 +865,14 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
   } else {
     for (int l = 0; l < c->L; l++) {
       const int out = c->widths[l];
-      const int in = (l == 0) ? c->d_ac : layer_in(l);
+      const int in = (l == 0) ? c->d_x : layer_in(l);
       const float* W = p->fc_w[l];
       s = upload(c, (void**)&c->d_wt[l], sizeof(float) * (size_t)std::max(1, in) * out, [&](uint8_t* h) {
         float* o = (float*)h;
         for (int i = 0; i < in; i++)
           for (int n = 0; n < out; n++) {
             float v;
-            if (l == 0) v = W[(size_t)n * d_in + col_of(c->sel_ac[i / k], i % k)];
+            if (l == 0) v = c->dense_se ? W[(size_t)n * d_in + i] : W[(size_t)n * d_in + col_of(c->sel_ac[i / k], i % k)];
             else v = W[(size_t)n * in + i];
             o[(size_t)i * out + n] = v;
           }
@@ -1031,6 +1062,7 @@ static UserArgs make_user_args(cold_ctx* c, const CallPlan& pl, const int32_t* d
   ua.u1t_ld = c->u1t_ld;
   ua.u1_terms = c->u1_terms;
   ua.bf16 = c->precision == COLD_BF16 ? 1 : 0;
+  ua.dense = c->dense_se ? 1 : 0;
   return ua;
 }
 
@@ -1078,6 +1110,10 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
   ga.chunk = c->chunk;
   ga.nslot = U1_NSLOT;
   ga.bf16 = c->precision == COLD_BF16 ? 1 : 0;
+  if (c->dense_se) {
+    ga.E = c->d_E;
+    ga.lde = c->d_in;
+  }
   return ga;
 }
 
@@ -1089,14 +1125,14 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     memset(&m, 0, sizeof(m));
     m.X = (const float*)c->d_X + (size_t)xslot * c->chunk * c->d_ac_pad;
     m.ldx = c->d_ac_pad;
-    m.d_ac = c->d_ac;
+    m.d_ac = c->d_x;
     m.u1 = c->d_u1;
     m.ld_u1 = c->widths[0];
     m.req_of_ad = c->d_req;
     m.a0 = a0;
     m.n = n;
     m.L = c->L;
-    int mw = std::max(1, c->d_ac);
+    int mw = std::max(1, c->d_x);
     for (int l = 0; l < c->L; l++) {
       m.wt[l] = c->d_wt[l];
       m.b[l] = c->d_b[l];
@@ -1340,6 +1376,32 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
       launch_gather(ga, c->precision, st);
       c->mark_end(COLD_PROF_GATHER, st);
     }
+    if (c->dense_se) {   // dense SE gate over the span (the Doc B reading of P:229-234, AMB-1)
+      SeDenseArgs sa;
+      memset(&sa, 0, sizeof(sa));
+      sa.E = c->d_E;
+      sa.lde = c->d_in;
+      sa.xu = c->d_xu;
+      sa.ldu = c->d_u;
+      sa.n_user = (int)c->sel_user.size();
+      for (int j = 0; j < sa.n_user; j++) sa.user_pos[j] = c->sel_pos[c->sel_user[j]];
+      sa.req_of_ad = c->d_req;
+      sa.a0 = s0;
+      sa.n = s1 - s0;
+      sa.wdt = c->d_sewd_t;
+      sa.bd = c->d_sebd;
+      sa.n_sel = (int)c->sel.size();
+      sa.k = c->k;
+      sa.d_in = c->d_in;
+      sa.in_scale = c->d_in_scale;
+      sa.in_shift = c->d_in_shift;
+      sa.X = c->d_X;
+      sa.ldx = c->d_ac_pad;
+      sa.dbg_feat = dbg.feat;
+      c->mark_begin(st);
+      launch_se_dense(sa, c->precision, st);
+      c->mark_end(COLD_PROF_SE_DENSE, st);
+    }
     if (pl.host) CK(cudaEventRecord(c->ev_consumed[slot], st));
     if (mode == RUN_SCORE) {
       // COLD_SPAN_REV=1: chunks of the span last-first (the last chunk's X rows are the ones most likely
@@ -1434,6 +1496,7 @@ extern "C" cold_status cold_debug_rows(cold_ctx* c, const cold_batch* b, int32_t
 // ---------------------------------------------------------------------------------------------
 // feature-group selection statistics
 extern "C" cold_status cold_se_stats(cold_ctx* c, const cold_batch* b, double* mean_s_out, void* stream) {
+  if (c && c->dense_se) return fail(COLD_ERR_UNSUPPORTED, "cold_se_stats: per-group SE only (se_mode dense)");
   if (!c || !mean_s_out) return fail(COLD_ERR_INVALID_ARG, "null ctx / output");
   if (!c->loaded) return fail(COLD_ERR_NOT_LOADED, "cold_load_params has not been called");
   CallPlan pl;
@@ -1684,8 +1747,8 @@ extern "C" cold_status cold_get_info(const cold_ctx* c, cold_info* out) {
   if (!c || !out) return fail(COLD_ERR_INVALID_ARG, "null");
   out->version = c->version;
   out->d_in = c->d_in;
-  out->d_user = c->d_u;
-  out->d_ad = c->d_ac;
+  out->d_user = c->dense_se ? 0 : c->d_u;   // hoisted user part (none under dense SE)
+  out->d_ad = c->d_x;
   out->chunk_ads = c->chunk;
   out->kernels_per_chunk = 1 + (c->tensor ? (c->L - 1 - c->n_tail + (c->n_tail ? 1 : 0)) : 1);
   out->kernels_per_call = 1;

@@ -34,6 +34,7 @@ struct UserArgs {
   uint16_t* u1t;                   // FC1 u1 operand (nullable): [u1_terms * H][u1t_ld] f16/bf16 bits, the
                                    // 2 (f16) or 3 (bf16) RNE terms of u1[r][o] at [t * H + o][r]
   int u1t_ld, u1_terms, bf16;
+  int dense;                       // dense SE (COLD_SE_DENSE): xu gets the pre-SE linear_log'ed ê_u, u1 = b1
 };
 
 struct GatherArgs {
@@ -68,7 +69,27 @@ struct GatherArgs {
   int chunk;                       // rows per FC chunk (pair tiles are 256-row aligned inside a chunk)
   int nslot;                       // max requests per pair tile folded into the MMA (else all-zero rows)
   int bf16;
+  float* E;                        // dense SE (nullable): [n][lde] fp32 pre-SE ê (after linear_log) at
+  int lde;                         //   column sel_pos * k; the gate runs in se_dense_kernel
 };
+
+// dense SE gate (COLD_SE_DENSE, the Doc B reading of P:229-234): per ad, ê = [ê_g] over the selected
+// groups in schema order (user columns from xu[request], the rest from E), s = sigma(Wd ê + bd),
+// X[ad][sel_pos * k + d] = cast(s_g ê_g[d]) (input normalisation in fp32 before the cast).
+struct SeDenseArgs {
+  const float* E; int lde;         // span-local [n][lde] (ad + cross columns)
+  const float* xu; int ldu;        // [R][ldu] per-request user ê, user group j at column j * k
+  int n_user; int user_pos[COLD_MAX_GROUPS];   // selected position of user group j
+  const int32_t* req_of_ad; int64_t a0; int64_t n;
+  const float* wdt;                // [D_in][n_sel] (Wd transposed)
+  const float* bd;                 // [n_sel]
+  int n_sel, k, d_in;
+  const float* in_scale; const float* in_shift;
+  void* X; int ldx;                // span-local [n][ldx] storage dtype
+  float* dbg_feat;                 // [N][D_in] (call-global rows, nullable)
+};
+void launch_se_dense(const SeDenseArgs& a, int precision, cudaStream_t s);
+size_t se_dense_smem(int d_in, int n_sel);   // dynamic shared memory of the dense-SE kernel (<= 227 KB)
 
 struct RowsArgs {
   const DevGroup* groups;

@@ -101,6 +101,18 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
     }
     float pooled = e;
     if (a.linear_log) e = linear_log(e);
+    if (a.dense) {                          // dense SE: the gate needs the ad's columns (se_dense_kernel)
+      if (lane < K) {
+        xs[j * K + lane] = e;
+        if (main_cta) {
+          a.xu[(int64_t)r * d_u + j * K + lane] = e;
+          if (a.dbg_pooled)
+            for (int64_t ad = a.ad_offsets[r]; ad < a.ad_offsets[r + 1]; ad++)
+              a.dbg_pooled[(ad * a.n_sel + G.sel_pos) * K + lane] = pooled;
+        }
+      }
+      continue;
+    }
     float z = (lane < K) ? a.se_w[g * K + lane] * e : 0.0f;
 #pragma unroll
     for (int off = 16; off; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
@@ -134,7 +146,8 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
   const int ostep = blockDim.x * gridDim.y;
   for (int o = blockIdx.y * blockDim.x + threadIdx.x; o < a.H && !a.stats; o += ostep) {
     float acc = a.b1[o];
-    for (int i = 0; i < d_u; i++) acc = fmaf(a.w1u_t[(int64_t)i * a.H + o], xs[i], acc);
+    if (!a.dense)   // dense SE: W1's user columns run inside FC1 with the gated per-ad x (u1 = b1)
+      for (int i = 0; i < d_u; i++) acc = fmaf(a.w1u_t[(int64_t)i * a.H + o], xs[i], acc);
     a.u1[(int64_t)r * a.H + o] = acc;
     if (a.u1t) {   // u1 = term_0 + term_1 (+ term_2), each RNE in 16 bits: the FC1 tensor-core operand
       float u = acc;
@@ -206,6 +219,17 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
   if (a.linear_log) {
 #pragma unroll
     for (int d = 0; d < K; d++) e[d] = linear_log_t<FAST>(e[d]);
+  }
+  if (a.E) {                                // dense SE: store ê (fp32); the gate runs in se_dense_kernel
+    float* dst = a.E + local * a.lde + G.sel_pos * K;
+    if constexpr (K % 4 == 0) {
+#pragma unroll
+      for (int d = 0; d < K; d += 4) *reinterpret_cast<float4*>(dst + d) = make_float4(e[d], e[d + 1], e[d + 2], e[d + 3]);
+    } else {
+#pragma unroll
+      for (int d = 0; d < K; d++) dst[d] = e[d];
+    }
+    return;
   }
   float z = 0.0f;
 #pragma unroll

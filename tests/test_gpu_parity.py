@@ -486,6 +486,73 @@ def test_input_batch_norm_variant(prec):
     _check_scores(gpu_scores(ctx, batch), p, z, prec, f"input batch norm {prec}")
 
 
+# ---- F2: dense SE gate (AMB-1, the Doc B reading of P:229-234) ----------------------------------
+
+def _dense_se_params(sch, params, scale=0.05, seed=5):
+    rng = np.random.default_rng(seed)
+    n_sel, d_in = sch.M, sch.M * sch.k
+    return (rng.uniform(-scale, scale, (n_sel, d_in)).astype(np.float32),
+            rng.uniform(-1, 1, n_sel).astype(np.float32))
+
+
+def _load_dense(ctx, params, W, b):
+    tables = params.tables
+    tdt = params.table_dtype
+    if ctx.precision == "f32" and tdt != "f32":
+        tables = [params.table_f64(g).astype(np.float32) for g in range(len(tables))]
+        tdt = "f32"
+    elif tdt == "f16":
+        tables = [t.view(np.uint16) for t in tables]
+    ctx.load_params(tables, params.se_w, params.se_b, params.fc_w, params.fc_b, table_dtype=tdt, se_dense=(W, b))
+
+
+@pytest.mark.parametrize("prec", ["f16", "bf16", "f32"])
+def test_dense_se_variant(prec):
+    """se_mode dense: s = sigma(Wd [ê_1 .. ê_M] + bd) per ad (user block not hoisted, FC1 over all D_in
+    columns) vs the oracle's dense-SE mode; features element by element, scores within tolerance; ragged
+    requests over several FC chunks."""
+    import torch
+    from paper_2007_16122_b200 import Context
+    sch, params, batch = small_case("paper", R=4, n_ads=(1300, 1, 257, 700), precision=prec, cap=20000, seed=95)
+    W, b = _dense_se_params(sch, params)
+    ctx = Context(sch.groups, sch.k, sch.widths, precision=prec, max_ads=4096, max_requests=8, chunk_ads=1024,
+                  se_mode="dense")
+    _load_dense(ctx, params, W, b)
+    assert ctx.info()["d_user"] == 0 and ctx.info()["d_ad"] == sch.M * sch.k
+    model = oracle.Model(sch, params, se_dense=(W.astype(np.float64), b.astype(np.float64)))
+    feat = torch.empty((batch.n_ads, sch.M * sch.k), dtype=torch.float32, device="cuda")
+    ctx.debug_features(device_batch(batch), feat)
+    torch.cuda.synchronize()
+    x = oracle.features(model, batch)
+    tol = {"f32": 1e-5, "f16": 2e-3, "bf16": 1e-2}[prec]
+    np.testing.assert_allclose(feat.cpu().numpy(), x, rtol=tol, atol=tol * 1e-2)
+    p, z = oracle.score(model, batch)
+    _check_scores(gpu_scores(ctx, batch), p, z, prec, f"dense SE {prec}")
+    c2 = ctx.clone()   # clones share the dense gate weights
+    np.testing.assert_array_equal(gpu_scores(c2, batch), gpu_scores(ctx, batch))
+    c2.close()
+    ctx.close()
+
+
+def test_dense_se_block_diagonal_equals_group_path():
+    """A block-diagonal dense W is the per-group gate (AMB-1): both GPU modes score alike."""
+    sch, params, batch = small_case("paper", R=2, n_ads=(900, 333), precision="f16", cap=20000, seed=96)
+    M, k = sch.M, sch.k
+    W = np.zeros((M, M * k), np.float32)
+    for g in range(M):
+        W[g, g * k:(g + 1) * k] = params.se_w[g]
+    from paper_2007_16122_b200 import Context
+    dense = Context(sch.groups, k, sch.widths, precision="f16", max_ads=4096, max_requests=8, se_mode="dense")
+    _load_dense(dense, params, W, params.se_b.astype(np.float32))
+    group = make_ctx(sch, params)
+    a, b = gpu_scores(dense, batch), gpu_scores(group, batch)
+    assert rel_err(a, b).max() <= 2e-2
+    with pytest.raises(Exception):
+        dense.se_stats(device_batch(batch))
+    dense.close()
+    group.close()
+
+
 # ---- multi-stream serving: contexts sharing one parameter copy ---------------------------------
 
 def test_ctx_clone_shares_params_and_runs_concurrently():

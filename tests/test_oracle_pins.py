@@ -303,6 +303,28 @@ def test_dense_se_block_diagonal_equals_per_group():
     np.testing.assert_allclose(p1, p2, rtol=1e-15)
 
 
+def test_dense_se_cross_group_gate_closed_form():
+    """AMB-1, Doc B: under the dense reading the gate of group j may read another group's
+    embedding. With one nonzero per row, W[j, (j+1 mod M) k + d_j] = c_j, the gate is the closed form
+    s_j = sigma(c_j * ê_{j+1}[d_j] + b_j); check x = s ê against the identity-gate features (x = ê) of the
+    same batch. A transposed W, a wrong column order or a dropped bias fails this."""
+    sch, params, batch = small_case("tiny", R=2, n_ads=(6, 3))
+    M, k = sch.M, sch.k
+    rng = np.random.default_rng(11)
+    W = np.zeros((M, M * k))
+    c = rng.uniform(-1.5, 1.5, M)
+    dj = rng.integers(0, k, M)
+    for j in range(M):
+        W[j, ((j + 1) % M) * k + dj[j]] = c[j]
+    b = rng.uniform(-1, 1, M)
+    x = oracle.features(oracle.Model(sch, params, se_dense=(W, b)), batch)
+    e = oracle.features(oracle.Model(sch, coldgen.make_params(sch, seed=7, precision="f32", se="identity")), batch)
+    for j in range(M):
+        src = e[:, ((j + 1) % M) * k + dj[j]]
+        s = 1.0 / (1.0 + np.exp(-(c[j] * src + b[j])))
+        np.testing.assert_allclose(x[:, j * k:(j + 1) * k], s[:, None] * e[:, j * k:(j + 1) * k], rtol=1e-12, atol=1e-15)
+
+
 def test_ll_order_variants_agree_when_gate_is_one():
     sch, params, batch = small_case("tiny", R=1, n_ads=(9,), se="identity")
     a = oracle.features(oracle.Model(sch, params), batch)

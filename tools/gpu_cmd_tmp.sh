@@ -1,4 +1,3 @@
 python -m paper_2007_16122_b200.build >/dev/null
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "not full_size" > gpurun_out/gpu_tests_s41.log 2>&1
-BENCH_ARGS="--requests 1024 --no-e2e --no-latency --no-cpu --steps 5" timeout 1200 bash tools/sweep.sh s41:COLD_TAIL=2 s41old:"COLD_TAIL_REV=0 COLD_SPAN_REV=0 COLD_H3_EF=1" s41ef:COLD_H3_EF=1 s41norev:COLD_SPAN_REV=0
-python tools/show.py gpurun_out/sweep_s41*.log > gpurun_out/sweep_s41.txt 2>&1
+timeout 600 python -m pytest tests -m gpu -q -k "dense" > gpurun_out/gpu_tests_s6.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_s6.log
+timeout 600 python bench.py --requests 2048 --no-e2e --no-cpu --no-latency --steps 5 --se-dense > gpurun_out/bench_dense_s6.jsonl 2>&1
