@@ -63,17 +63,31 @@ __device__ __forceinline__ int64_t cross_row_from_hx(uint64_t hx, uint64_t y, ui
 
 // ---- storage types -------------------------------------------------------------------------
 template <typename T> struct Store;
+// add(acc, v) = acc + (float)v rounded to nearest: the widening is exact, so this is the fp32 sum the
+// oracle's fp32-ordered mode defines; for 16-bit v it is one sm_100 mixed-precision add (FHADD),
+// instead of a convert + FADD pair.
 template <> struct Store<float> {
   static __device__ __forceinline__ float to_f(float v) { return v; }
   static __device__ __forceinline__ float from_f(float v) { return v; }
+  static __device__ __forceinline__ float add(float acc, float v) { return acc + v; }
 };
 template <> struct Store<__half> {
   static __device__ __forceinline__ float to_f(__half v) { return __half2float(v); }
   static __device__ __forceinline__ __half from_f(float v) { return __float2half_rn(v); }  // RNE, non-saturating
+  static __device__ __forceinline__ float add(float acc, __half v) {
+    float r;
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(r) : "h"(__half_as_ushort(v)), "f"(acc));
+    return r;
+  }
 };
 template <> struct Store<__nv_bfloat16> {
   static __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
   static __device__ __forceinline__ __nv_bfloat16 from_f(float v) { return __float2bfloat16_rn(v); }
+  static __device__ __forceinline__ float add(float acc, __nv_bfloat16 v) {
+    float r;
+    asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(r) : "h"(__bfloat16_as_ushort(v)), "f"(acc));
+    return r;
+  }
 };
 
 // ---- per-ctx static group description (device resident) ------------------------------------

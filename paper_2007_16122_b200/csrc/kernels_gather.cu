@@ -45,11 +45,11 @@ __device__ __forceinline__ void add_row(const T* __restrict__ table, int64_t row
     for (int v = 0; v < BYTES / 16; v++) {
       const T* t = reinterpret_cast<const T*>(&qv[v]);
 #pragma unroll
-      for (int i = 0; i < 16 / (int)sizeof(T); i++) e[v * (16 / sizeof(T)) + i] += Store<T>::to_f(t[i]);
+      for (int i = 0; i < 16 / (int)sizeof(T); i++) e[v * (16 / sizeof(T)) + i] = Store<T>::add(e[v * (16 / sizeof(T)) + i], t[i]);
     }
   } else {                                   // tiny rows (k = 2, 4)
 #pragma unroll
-    for (int d = 0; d < K; d++) e[d] += Store<T>::to_f(table[row * K + d]);
+    for (int d = 0; d < K; d++) e[d] = Store<T>::add(e[d], table[row * K + d]);
   }
 }
 
@@ -203,7 +203,7 @@ struct RawRow {
     for (int v = 0; v < NV; v++) {
       const T* t = reinterpret_cast<const T*>(&q[v]);
 #pragma unroll
-      for (int i = 0; i < 16 / (int)sizeof(T); i++) e[v * (16 / sizeof(T)) + i] += Store<T>::to_f(t[i]);
+      for (int i = 0; i < 16 / (int)sizeof(T); i++) e[v * (16 / sizeof(T)) + i] = Store<T>::add(e[v * (16 / sizeof(T)) + i], t[i]);
     }
   }
 };

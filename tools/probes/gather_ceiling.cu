@@ -99,6 +99,8 @@ int main() {
   run<4, 64>("hbm_rand64", tab, big, out, blocks);
   run<8, 64>("hbm_rand64", tab, big, out, sms * 4);
   run<4, 128>("hbm_rand128", tab, big, out, sms * 4);
+  for (uint64_t mb : {128ull, 256ull, 512ull, 1024ull, 2048ull})   // TLB reach vs table span
+    run<8, 32>("span_rand32", tab, mb << 20, out, blocks);
   run<4, 32>("l2_rand32", tab, small, out, blocks);
   run<8, 32>("l2_rand32", tab, small, out, blocks);
   run<16, 32>("l2_rand32", tab, small, out, sms * 4);
