@@ -497,7 +497,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     // group column is gathered for every ad of the span before the next group starts, so each
     // table's hot rows are fetched from HBM once per span and then served by L2.
     const char* env_span = getenv("COLD_GSPAN");
-    int span = env_span ? atoi(env_span) : 4;
+    int span = env_span ? atoi(env_span) : 16;   // measured: 4 -> 16 is +4% gather GB/s, +1% ads/s
     if (span < 1) span = 1;
     const int64_t need = (c->max_ads + c->chunk - 1) / c->chunk;
     c->gspan = (int)std::min<int64_t>(span, std::max<int64_t>(need, 1));

@@ -209,8 +209,10 @@ struct RawRow {
 };
 
 // pooled e -> [debug] -> linear_log -> SE gate -> v = s ê -> RNE cast -> X_ac[local][slot]
+// sew / seb: the group's SE weights (staged in shared memory by the one-group-per-CTA columns)
 template <typename T, int K, bool FAST>
-__device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G, int g, int64_t local, float* e) {
+__device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G, int g, int64_t local, float* e,
+                                          const float* sew, float seb) {
   const int64_t ad = a.a0 + local;
   if (a.dbg_pooled) {
 #pragma unroll
@@ -233,8 +235,8 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
   }
   float z = 0.0f;
 #pragma unroll
-  for (int d = 0; d < K; d++) z = fmaf(__ldg(a.se_w + g * K + d), e[d], z);
-  const float s = sigmoid_t<FAST>(z + __ldg(a.se_b + g));
+  for (int d = 0; d < K; d++) z = fmaf(sew[d], e[d], z);
+  const float s = sigmoid_t<FAST>(z + seb);
   if (a.stats) {                            // SE statistics mode (cold_se_stats)
     atomicAdd(a.stats + g, (double)s);
     return;
@@ -384,7 +386,7 @@ __device__ __forceinline__ void singles_column(const GatherArgs& a) {
             add_row<T, K>(reinterpret_cast<const T*>(G.table), cross_row_from_hx(hx, y, (uint64_t)G.card), e);
           }
         }
-        finish_ad<T, K, FAST>(a, G, g, li, e);
+        finish_ad<T, K, FAST>(a, G, g, li, e, a.se_w + g * K, __ldg(a.se_b + g));
       }
     }
   }
@@ -408,10 +410,13 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
   constexpr int NV = K * (int)sizeof(T) / 16;
   // bag rows in flight per thread (<= 16 vectors of raw registers; halved when the register budget
   // is halved for twice the resident warps)
-  constexpr int GATHER_RB = (NV <= 2 ? 8 : (NV == 4 ? 4 : 2)) / (MINB >= 8 ? 2 : 1);
+  constexpr int GATHER_RB = (NV <= 2 ? 8 : (NV == 4 ? 4 : 2)) / (MINB >= 12 ? 4 : (MINB >= 8 ? 2 : 1));
   __shared__ uint64_t s_hx[2][HX_HALF];
+  __shared__ float s_w[K + 1];              // the group's SE weights and bias (read by every ad)
   const int j = a.order[blockIdx.y];
   const int g = a.ac_g[j];
+  if (threadIdx.x <= K) s_w[threadIdx.x] = threadIdx.x < K ? a.se_w[g * K + threadIdx.x] : a.se_b[g];
+  __syncthreads();
   const DevGroup G = a.groups[g];
   const T* tab = reinterpret_cast<const T*>(G.table);
   const int64_t base = (int64_t)blockIdx.x * (128 * GATHER_APT);
@@ -439,7 +444,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
 #pragma unroll
         for (int d = 0; d < K; d++) e[d] = 0.0f;
         raw[i].add_to(e);
-        if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e);
+        if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, s_w, s_w[K]);
       }
     } else {
       for (int i = 0; i < GATHER_APT; i++) {
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
           const int64_t o1 = (int64_t)B.offs[ad + 1 - B.offs_shift] - B.val_shift;
           for (int64_t q = o0; q < o1; q++) add_row<T, K>(tab, checked(B.ids[q], G.card, a.validate, a.err), e);
         }
-        finish_ad<T, K, FAST>(a, G, g, li, e);
+        finish_ad<T, K, FAST>(a, G, g, li, e, s_w, s_w[K]);
       }
     }
     return;
@@ -505,7 +510,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
 #pragma unroll
       for (int d = 0; d < K; d++) e[d] = 0.0f;
       raw[i].add_to(e);
-      if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e);
+      if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, s_w, s_w[K]);
     }
     return;
   }
@@ -555,7 +560,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
         }
       }
     }
-    finish_ad<T, K, FAST>(a, G, g, li, e);
+    finish_ad<T, K, FAST>(a, G, g, li, e, s_w, s_w[K]);
   }
 }
 
@@ -639,6 +644,8 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
       if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
       else if (apt == 2) gather_kernel<T, 16, FAST, 8, 2><<<grid_for(2), 128, 0, s>>>(a);
       else if (apt == 1) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);
+      else if (minb >= 16) gather_kernel<T, 16, FAST, 16><<<grid, 128, 0, s>>>(a);
+      else if (minb >= 12) gather_kernel<T, 16, FAST, 12><<<grid, 128, 0, s>>>(a);
       else if (minb >= 8) gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
       else gather_kernel<T, 16, FAST><<<grid, 128, 0, s>>>(a);
       break;

@@ -101,6 +101,14 @@ int main() {
   run<4, 128>("hbm_rand128", tab, big, out, sms * 4);
   for (uint64_t mb : {128ull, 256ull, 512ull, 1024ull, 2048ull})   // TLB reach vs table span
     run<8, 32>("span_rand32", tab, mb << 20, out, blocks);
+  for (int gran : {32, 64, 128}) {   // cudaLimitMaxL2FetchGranularity: DRAM fetch size behind a miss
+    cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, gran);
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitMaxL2FetchGranularity);
+    printf("{\"l2_fetch_granularity\": %zu}\n", got);
+    run<8, 32>("hbm_rand32_gran", tab, big, out, blocks);
+    run<8, 32>("span_rand32_gran", tab, 256ull << 20, out, blocks);
+  }
   run<4, 32>("l2_rand32", tab, small, out, blocks);
   run<8, 32>("l2_rand32", tab, small, out, blocks);
   run<16, 32>("l2_rand32", tab, small, out, sms * 4);
