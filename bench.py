@@ -98,6 +98,48 @@ def gather_bytes_per_ad(sch, elem):
     return rows * k * elem + id_bytes + 4 + n_ac * k * elem, rows
 
 
+# Random-row ceilings measured on this pool's B200s by tools/probes/gather_ceiling.cu
+# (profiles/r01/gather_ceiling.jsonl): 32 B rows at uniformly random positions of a table larger than
+# L2 come back at 46 G rows/s (1.47 TB/s useful) whatever the number in flight, and ncu counts 125 DRAM
+# bytes per such row (the DRAM side moves 128 B per random 32 B sector miss); rows of a 32 MB table
+# (L2-resident) come back at 287 G rows/s.
+RAND_DRAM_BYTES_PER_ROW = 125.0
+RAND_L2_ROWS_PER_S = 287e9
+L2_BYTES = 126 * 2**20
+
+
+def gather_access_model(sch, span_ads, elem, hbm_gbs):
+    """Ceiling of the ad + cross gather from the measured random-access rates: each group's rows are
+    L2-served when its table fits comfortably in L2 and every row is touched >= 2x per column-wise span,
+    else they are random DRAM rows (125 B of DRAM traffic each); L2-class tables still cost one random
+    DRAM fetch per row per span. Sequential bytes: ad ids, request index, X_ac write."""
+    k = sch.k
+    dram_rows = l2_rows = 0.0
+    first_touch = 0.0
+    for g in sch.groups:
+        if g.side == coldgen.USER:
+            continue
+        if g.side == coldgen.AD:
+            rows = 1 if not g.pooled else (g.bag[0] + g.bag[1]) / 2
+        else:
+            u, a = sch.groups[g.user_ref], sch.groups[g.ad_ref]
+            rows = (1 if not u.pooled else (u.bag[0] + u.bag[1]) / 2) * (1 if not a.pooled else (a.bag[0] + a.bag[1]) / 2)
+        tbytes = g.card * k * elem
+        if tbytes <= L2_BYTES // 3 and span_ads * rows / g.card >= 2:
+            l2_rows += rows
+            first_touch += min(g.card, span_ads * rows) * RAND_DRAM_BYTES_PER_ROW / span_ads
+        else:
+            dram_rows += rows
+    n_ac = len([g for g in sch.groups if g.side != coldgen.USER])
+    seq = 4 * len([g for g in sch.groups if g.side == coldgen.AD]) + 4 + n_ac * k * elem
+    dram_b = dram_rows * RAND_DRAM_BYTES_PER_ROW + first_touch + seq
+    t_dram = dram_b / (hbm_gbs * 1e9)
+    t_l2 = l2_rows / RAND_L2_ROWS_PER_S
+    return {"dram_random_rows_per_ad": dram_rows, "l2_rows_per_ad": l2_rows,
+            "dram_bytes_per_ad": dram_b, "ceiling_ads_per_s_overlapped": 1.0 / max(t_dram, t_l2),
+            "ceiling_ads_per_s_serial": 1.0 / (t_dram + t_l2)}
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -763,6 +805,17 @@ def main():
                                            "the column-wise gather",
                            "algorithmic": f"{gb_per_ad:.0f} B/ad ({rows_per_ad:.0f} rows x {sch.k} x 2 B + ids "
                                           f"+ X_ac write)"}
+        span_ads = min(N, info["chunk_ads"] * int(os.environ.get("COLD_GSPAN", "16")))
+        model = gather_access_model(sch, span_ads, 2 if args.precision != "f32" else 4, hb)
+        g_ads = N * args.steps / (prof_ms[PROF_GATHER] / 1e3)
+        model.update({"achieved_ads_per_s": g_ads,
+                      "frac_overlapped": g_ads / model["ceiling_ads_per_s_overlapped"],
+                      "frac_serial": g_ads / model["ceiling_ads_per_s_serial"],
+                      "note": "random 32 B rows cost 125 DRAM B each and cap at 46 G rows/s on this B200 "
+                              "(tools/probes/gather_ceiling.cu, profiles/r01/gather_ceiling.jsonl); ceilings "
+                              "from the per-group L2 / DRAM split of the column-wise span, DRAM and L2 time "
+                              "overlapped (max) or serial (sum)"})
+        roofline_gather["random_access_model"] = model
     fc_total_ms = sum(prof_ms[PROF_FC + l] for l in covers)
     fc_flops_all = N * args.steps * sum(layer_flops)
     fc_stack = {"tflops": fc_flops_all / (fc_total_ms / 1e3) / 1e12,

@@ -10,7 +10,7 @@ OUT=gpurun_out
 ARGS=${NCU_ARGS:-"--requests 32 --ads 9472 --steps 2 --warmup 1 --no-e2e --no-latency --no-cpu"}
 python -m paper_2007_16122_b200.build >/dev/null
 # 1. launch list (cold-cache, serialised: compare shares)
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv \
+timeout 400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv \
   --log-file $OUT/launches_$TAG.csv python bench.py $ARGS > $OUT/ncu_launch_bench_$TAG.log 2>&1
 for k in $KERNELS; do
   case $k in
@@ -22,7 +22,7 @@ for k in $KERNELS; do
     tail45) RX="regex:tail45_kernel"; S=1;;
     *) RX="regex:$k"; S=1;;
   esac
-  timeout 900 ncu --set full --clock-control none --import-source on -k $RX -s $S -c 1 \
+  timeout 400 ncu --set full --clock-control none --import-source on -k $RX -s $S -c 1 \
     -o $OUT/prof_${k}_$TAG python bench.py $ARGS > $OUT/ncu_${k}_$TAG.log 2>&1
 done
 for f in $OUT/prof_*_$TAG.ncu-rep; do python tools/ncu_summary.py $f; done > $OUT/ncu_summary_$TAG.txt 2>&1
