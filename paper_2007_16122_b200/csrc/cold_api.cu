@@ -1194,6 +1194,8 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
                                  c->chain_tail ? &c->tmW4h : &c->tmB[0], c->chain_tail ? &c->tmW5h : &c->tmB[0],
                                  c->chain_tail ? &c->tmC[3] : &c->tmB[0]};
     c->mark_begin(st);
+    static const bool gbias = getenv("COLD_CHAIN_GBIAS") && atoi(getenv("COLD_CHAIN_GBIAS")) != 0;
+    cp.gbias = gbias ? 1 : 0;
     launch_chain(tm, (int)n, c->precision == COLD_BF16 ? 1 : 0, cp, c->num_sms, c->pdl && !c->prof, st);
     c->mark_end(COLD_PROF_FC, st);
     n_gemm = 0;

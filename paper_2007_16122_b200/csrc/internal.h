@@ -180,6 +180,7 @@ struct ChainParams {
   const void* h3; const void* h4;
   float* scores;                         // chunk-local [M]
   int h3_evict_first;                    // H3 stores with an evict-first L2 hint (no TAIL)
+  int gbias;                             // 1: epilogue reads FC2 / FC3 biases from global (A/B switch)
   unsigned long long* instr;             // debug (nullable): wait cycles [0] producer empty, [1] producer
                                          // hready, [2] MMA full, [3] MMA tempty, [4] MMA uxfull, [5] epi tfull
 };
