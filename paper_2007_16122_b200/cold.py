@@ -13,7 +13,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcold.so")
+# COLD_LIB_AB: load an A/B variant build instead (tools/ab_build.sh; measurement tooling only)
+LIB_PATH = os.environ.get("COLD_LIB_AB") or os.path.join(HERE, "libcold.so")
 
 USER, AD, CROSS = 0, 1, 2
 FP32, FP16, BF16 = 0, 1, 2
