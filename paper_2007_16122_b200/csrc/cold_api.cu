@@ -149,6 +149,7 @@ struct cold_ctx {
   uint64_t version = 0;
   std::vector<void*> d_tables;
   DevGroup* d_groups = nullptr;
+  std::vector<DevGroup> h_groups;    // host copy (gather kernel parameters)
   float* d_se_w = nullptr;
   float* d_se_b = nullptr;
   float* d_w1u_t = nullptr;
@@ -664,6 +665,7 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
   c->version = src->version;
   c->d_tables = src->d_tables;
   c->d_groups = src->d_groups;
+  c->h_groups = src->h_groups;
   c->d_se_w = src->d_se_w;
   c->d_se_b = src->d_se_b;
   c->d_w1u_t = src->d_w1u_t;
@@ -767,7 +769,8 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
     }
   }
   // group descriptors
-  std::vector<DevGroup> dg(c->M);
+  std::vector<DevGroup>& dg = c->h_groups;
+  dg.assign(c->M, DevGroup());
   std::vector<int> slot(c->M, -1);
   for (size_t j = 0; j < c->sel_user.size(); j++) slot[c->sel_user[j]] = (int)j;
   for (size_t j = 0; j < c->sel_ac.size(); j++) slot[c->sel_ac[j]] = (int)j;
@@ -1070,6 +1073,7 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
   GatherArgs ga;
   memset(&ga, 0, sizeof(ga));
   ga.groups = c->d_groups;
+  for (int g = 0; g < c->M; g++) ga.gp[g] = c->h_groups[g];
   ga.bv = bv;
   ga.n_ac = (int)c->sel_ac.size();
   // COLD_GATHER_MERGE=1: single-valued AD groups and single x single crosses go to one merged column

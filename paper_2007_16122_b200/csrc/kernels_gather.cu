@@ -208,6 +208,14 @@ struct RawRow {
   }
 };
 
+// group descriptors of the gather: from the kernel parameters (constant bank, no dependent global
+// load at CTA start) unless the A/B build asks for the device array
+#ifdef COLD_GATHER_GLOBAL_GROUPS
+#define GGROUP(a, g) ((a).groups[g])
+#else
+#define GGROUP(a, g) ((a).gp[g])
+#endif
+
 // pooled e -> [debug] -> linear_log -> SE gate -> v = s ê -> RNE cast -> X_ac[local][slot]
 // sew / seb: the group's SE weights (staged in shared memory by the one-group-per-CTA columns)
 template <typename T, int K, bool FAST>
@@ -235,7 +243,11 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
   }
   float z = 0.0f;
 #pragma unroll
+#ifdef COLD_GATHER_SW_SMEM
   for (int d = 0; d < K; d++) z = fmaf(sew[d], e[d], z);
+#else
+  for (int d = 0; d < K; d++) z = fmaf(__ldg(sew + d), e[d], z);
+#endif
   const float s = sigmoid_t<FAST>(z + seb);
   if (a.stats) {                            // SE statistics mode (cold_se_stats)
     atomicAdd(a.stats + g, (double)s);
@@ -310,9 +322,9 @@ __device__ __forceinline__ void singles_column(const GatherArgs& a) {
   const int rlast = a.req_of_ad[a.a0 + last];
   for (int i = threadIdx.x; i < a.n_single; i += blockDim.x) {
     const int g = a.single_g[i];
-    const DevGroup G = a.groups[g];
+    const DevGroup G = GGROUP(a, g);
     if (G.side != 2) continue;
-    const DevGroup U = a.groups[G.user_ref];
+    const DevGroup U = GGROUP(a, G.user_ref);
     const BatchGroup& BU = a.bv.g[G.user_ref];
     const uint64_t salt = cross_salt(g);
     int ok = rlast - rfirst <= 1;
@@ -343,14 +355,14 @@ __device__ __forceinline__ void singles_column(const GatherArgs& a) {
         fast[t] = false;
         if (gi[t] < 0) continue;
         const int g = a.single_g[gi[t]];
-        const DevGroup G = a.groups[g];
+        const DevGroup G = GGROUP(a, g);
         tabs[t] = reinterpret_cast<const T*>(G.table);
         if (G.side == 1) {
           const BatchGroup& B = a.bv.g[g];
           row[t] = checked(B.ids[ad - B.id_shift], G.card, a.validate, a.err);
           fast[t] = true;
         } else if (s_ok[gi[t]]) {
-          const DevGroup A = a.groups[G.ad_ref];
+          const DevGroup A = GGROUP(a, G.ad_ref);
           const BatchGroup& BA = a.bv.g[G.ad_ref];
           const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
           row[t] = cross_row_from_hx(s_hx1[gi[t]][slot], y, (uint64_t)G.card);
@@ -365,15 +377,15 @@ __device__ __forceinline__ void singles_column(const GatherArgs& a) {
       for (int t = 0; t < RB; t++) {
         if (gi[t] < 0) continue;
         const int g = a.single_g[gi[t]];
-        const DevGroup G = a.groups[g];
+        const DevGroup G = GGROUP(a, g);
         float e[K];
 #pragma unroll
         for (int d = 0; d < K; d++) e[d] = 0.0f;
         if (fast[t]) {
           raw[t].add_to(e);
         } else {   // a request in the block has a user bag != 1: the general x-major cross sum
-          const DevGroup U = a.groups[G.user_ref];
-          const DevGroup A = a.groups[G.ad_ref];
+          const DevGroup U = GGROUP(a, G.user_ref);
+          const DevGroup A = GGROUP(a, G.ad_ref);
           const BatchGroup& BU = a.bv.g[G.user_ref];
           const BatchGroup& BA = a.bv.g[G.ad_ref];
           const uint64_t salt = cross_salt(g);
@@ -412,12 +424,19 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
   // is halved for twice the resident warps)
   constexpr int GATHER_RB = (NV <= 2 ? 8 : (NV == 4 ? 4 : 2)) / (MINB >= 12 ? 4 : (MINB >= 8 ? 2 : 1));
   __shared__ uint64_t s_hx[2][HX_HALF];
-  __shared__ float s_w[K + 1];              // the group's SE weights and bias (read by every ad)
   const int j = a.order[blockIdx.y];
   const int g = a.ac_g[j];
+#ifdef COLD_GATHER_SW_SMEM   // A/B build: the group's SE weights staged in shared memory (a barrier at CTA start)
+  __shared__ float s_w[K + 1];
   if (threadIdx.x <= K) s_w[threadIdx.x] = threadIdx.x < K ? a.se_w[g * K + threadIdx.x] : a.se_b[g];
   __syncthreads();
-  const DevGroup G = a.groups[g];
+  const float* sew = s_w;
+  const float seb = s_w[K];
+#else
+  const float* sew = a.se_w + g * K;
+  const float seb = __ldg(a.se_b + g);
+#endif
+  const DevGroup G = GGROUP(a, g);
   const T* tab = reinterpret_cast<const T*>(G.table);
   const int64_t base = (int64_t)blockIdx.x * (128 * GATHER_APT);
   int64_t loc[GATHER_APT];
@@ -444,7 +463,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
 #pragma unroll
         for (int d = 0; d < K; d++) e[d] = 0.0f;
         raw[i].add_to(e);
-        if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, s_w, s_w[K]);
+        if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb);
       }
     } else {
       for (int i = 0; i < GATHER_APT; i++) {
@@ -461,15 +480,15 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
           const int64_t o1 = (int64_t)B.offs[ad + 1 - B.offs_shift] - B.val_shift;
           for (int64_t q = o0; q < o1; q++) add_row<T, K>(tab, checked(B.ids[q], G.card, a.validate, a.err), e);
         }
-        finish_ad<T, K, FAST>(a, G, g, li, e, s_w, s_w[K]);
+        finish_ad<T, K, FAST>(a, G, g, li, e, sew, seb);
       }
     }
     return;
   }
 
   // ---------------- CROSS group: rows = hash(user bag x ad bag), x-major ----------------
-  const DevGroup U = a.groups[G.user_ref];
-  const DevGroup A = a.groups[G.ad_ref];
+  const DevGroup U = GGROUP(a, G.user_ref);
+  const DevGroup A = GGROUP(a, G.ad_ref);
   const BatchGroup& BU = a.bv.g[G.user_ref];
   const BatchGroup& BA = a.bv.g[G.ad_ref];
   const uint64_t salt = cross_salt(g);
@@ -510,7 +529,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
 #pragma unroll
       for (int d = 0; d < K; d++) e[d] = 0.0f;
       raw[i].add_to(e);
-      if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, s_w, s_w[K]);
+      if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb);
     }
     return;
   }
@@ -560,7 +579,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
         }
       }
     }
-    finish_ad<T, K, FAST>(a, G, g, li, e, s_w, s_w[K]);
+    finish_ad<T, K, FAST>(a, G, g, li, e, sew, seb);
   }
 }
 

@@ -1,4 +1,5 @@
 python -m paper_2007_16122_b200.build >/dev/null
-AB=COLD_LIB_AB=$PWD/paper_2007_16122_b200/_ab/llbranchy.so
-BENCH_ARGS="--requests 2048 --no-e2e --no-latency --no-cpu --steps 5" timeout 1500 bash tools/sweep.sh s13new1: s13old1:$AB s13new2: s13old2:$AB
-python tools/show.py gpurun_out/sweep_s13*.log > gpurun_out/sweep_s13.txt 2>&1
+A=COLD_LIB_AB=$PWD/paper_2007_16122_b200/_ab/oldgroups.so
+B=COLD_LIB_AB=$PWD/paper_2007_16122_b200/_ab/swsmem.so
+BENCH_ARGS="--requests 2048 --no-e2e --no-latency --no-cpu --steps 5" timeout 1500 bash tools/sweep.sh s15new1: s15old1:$A s15sw1:$B s15new2: s15old2:$A s15sw2:$B
+python tools/show.py gpurun_out/sweep_s15*.log > gpurun_out/sweep_s15.txt 2>&1
