@@ -199,6 +199,8 @@ struct cold_ctx {
   const int32_t* cur_adoff = nullptr;  // device ad offsets of the call in flight
   // host-batch staging
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t side_stream = nullptr;   // few-request calls: the user kernel runs here, beside the gather
+  cudaEvent_t ev_fork = nullptr, ev_user = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
   cudaEvent_t ev_scored[2] = {nullptr, nullptr}, ev_drained[2] = {nullptr, nullptr};
   void* d_stage[2] = {nullptr, nullptr};
@@ -241,6 +243,9 @@ struct cold_ctx {
     if (d_topk_in) cudaFree(d_topk_in);
     if (d_topk_out) cudaFree(d_topk_out);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (side_stream) cudaStreamDestroy(side_stream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_user) cudaEventDestroy(ev_user);
     for (cudaEvent_t e : prof_events) cudaEventDestroy(e);
     freeParams();
     cudaGetLastError();
@@ -613,10 +618,17 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     c->chain_tail = c->chain && chain_tail_supported(c->widths[3], c->widths[4], c->widths[2]) &&
                     c->widths[5] <= 2 && env_chain != nullptr && atoi(env_chain) == 2;
   }
-  if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      [&] {   // the user kernel is on the latency path's critical chain: highest stream priority
+        int lo = 0, hi = 0;
+        cudaDeviceGetStreamPriorityRange(&lo, &hi);
+        return cudaStreamCreateWithPriority(&c->side_stream, cudaStreamNonBlocking, hi);
+      }() != cudaSuccess) {
     delete c;
     return fail(COLD_ERR_CUDA, "stream create failed");
   }
+  cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming);
   for (int i = 0; i < 2; i++) {
     cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_consumed[i], cudaEventDisableTiming);
@@ -1310,10 +1322,25 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
   const bool scores_dev = mode == RUN_SCORE && is_device_ptr(scores);
   c->cur_adoff = d_adoff;
   UserArgs ua = make_user_args(c, pl, d_adoff, dbg);
-  c->mark_begin(st);
-  launch_user(ua, pl.R, c->precision, st);
-  c->mark_end(COLD_PROF_USER, st);
+  // Latency path (a few requests, scoring): the user side (pooling, u1 GEMV, ad -> request map) does not
+  // feed the gather, which finds an ad's request by searching ad_offsets, so the two run concurrently
+  // (fork onto the side stream, join before the FC stack). COLD_USER_FORK=0 serialises them.
+  static const bool fork_env = !(getenv("COLD_USER_FORK") && atoi(getenv("COLD_USER_FORK")) == 0);
+  const bool fork = fork_env && mode == RUN_SCORE && pl.R <= 4;
+  if (fork) {
+    CK(cudaEventRecord(c->ev_fork, st));
+    CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+    c->mark_begin(c->side_stream);
+    launch_user(ua, pl.R, c->precision, c->side_stream);
+    c->mark_end(COLD_PROF_USER, c->side_stream);
+    CK(cudaEventRecord(c->ev_user, c->side_stream));
+  } else {
+    c->mark_begin(st);
+    launch_user(ua, pl.R, c->precision, st);
+    c->mark_end(COLD_PROF_USER, st);
+  }
   CK(cudaGetLastError());
+  bool joined = !fork;
   const int64_t chunk = c->chunk;
   const int64_t span = chunk * c->gspan;            // ads per column-wise gather pass
   const int64_t nspans = (pl.N + span - 1) / span;
@@ -1349,6 +1376,11 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
       CK(cudaStreamWaitEvent(st, c->ev_copied[slot], 0));
     }
     GatherArgs ga = make_gather_args(c, bv, s0, s1 - s0, dbg);
+    if (fork) {
+      ga.search_req = 1;
+      ga.adoff = d_adoff;
+      ga.R = pl.R;
+    }
     static const bool split = getenv("COLD_GATHER_SPLIT") && atoi(getenv("COLD_GATHER_SPLIT")) != 0;
     if (split) {   // profiling aid: one launch per group column (then the one-hot column)
       GatherArgs g1 = ga;
@@ -1381,6 +1413,10 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
       c->mark_begin(st);
       launch_gather(ga, c->precision, st);
       c->mark_end(COLD_PROF_GATHER, st);
+    }
+    if (!joined) {   // dense SE and the FC stack read x_u / u1 and req_of_ad
+      CK(cudaStreamWaitEvent(st, c->ev_user, 0));
+      joined = true;
     }
     if (c->dense_se) {   // dense SE gate over the span (the Doc B reading of P:229-234, AMB-1)
       SeDenseArgs sa;

@@ -283,6 +283,19 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
   }
 }
 
+// request of a call-global ad: the map written by user_kernel, or (search_req: the few-request latency
+// path, where the user kernel runs concurrently on the ctx's side stream) a binary search of ad_offsets
+__device__ __forceinline__ int req_at(const GatherArgs& a, int64_t ad) {
+  if (!a.search_req) return a.req_of_ad[ad];
+  int lo = 0, hi = a.R;   // ad_offsets[lo] <= ad < ad_offsets[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(a.adoff + mid) <= ad) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
 // FC1 u1 operand rows: for span-local row i, slot = request(i) - base, base = the first request of its
 // 256-row CTA-pair tile rounded down to a multiple of 8 (tiles are 256-aligned inside each FC chunk);
 // 1.0 at k = slot and k = 8 + slot; all zero when the tile's requests do not fit in [base, base + 8)
@@ -292,9 +305,9 @@ __device__ __forceinline__ void write_ohot(const GatherArgs& a, int64_t i, uint1
   const int64_t c_end = min((j + 1) * (int64_t)a.chunk, a.n);
   const int64_t t0 = j * a.chunk + (q & ~(int64_t)255);
   const int64_t t1 = min(t0 + 256, c_end) - 1;
-  const int r0 = a.req_of_ad[a.a0 + t0] & ~7;   // 8-aligned: the u1-term TMA box starts 16 B aligned
-  const int slot = a.req_of_ad[a.a0 + i] - r0;
-  const bool ok = a.req_of_ad[a.a0 + t1] - r0 < a.nslot;
+  const int r0 = req_at(a, a.a0 + t0) & ~7;   // 8-aligned: the u1-term TMA box starts 16 B aligned
+  const int slot = req_at(a, a.a0 + i) - r0;
+  const bool ok = req_at(a, a.a0 + t1) - r0 < a.nslot;
   uint32_t w[8];
 #pragma unroll
   for (int c = 0; c < 8; c++) {
@@ -318,8 +331,8 @@ __device__ __forceinline__ void singles_column(const GatherArgs& a) {
   __shared__ int s_ok[COLD_MAX_GROUPS];            // 1: both requests have a user bag of exactly 1
   const int64_t base = (int64_t)blockIdx.x * (128 * GATHER_APT);
   const int64_t last = (base + 128 * GATHER_APT < a.n ? base + 128 * GATHER_APT : a.n) - 1;
-  const int rfirst = a.req_of_ad[a.a0 + base];
-  const int rlast = a.req_of_ad[a.a0 + last];
+  const int rfirst = req_at(a, a.a0 + base);
+  const int rlast = req_at(a, a.a0 + last);
   for (int i = threadIdx.x; i < a.n_single; i += blockDim.x) {
     const int g = a.single_g[i];
     const DevGroup G = GGROUP(a, g);
@@ -342,7 +355,7 @@ __device__ __forceinline__ void singles_column(const GatherArgs& a) {
     const int64_t li = base + threadIdx.x + i * 128;
     if (li >= a.n) break;
     const int64_t ad = a.a0 + li;
-    const int slot = a.req_of_ad[ad] == rfirst ? 0 : 1;
+    const int slot = req_at(a, ad) == rfirst ? 0 : 1;
     for (int i0 = 0; i0 < a.n_single; i0 += RB) {
       int64_t row[RB];
       int gi[RB];
@@ -389,7 +402,7 @@ __device__ __forceinline__ void singles_column(const GatherArgs& a) {
           const BatchGroup& BU = a.bv.g[G.user_ref];
           const BatchGroup& BA = a.bv.g[G.ad_ref];
           const uint64_t salt = cross_salt(g);
-          const int r = a.req_of_ad[ad];
+          const int r = req_at(a, ad);
           const int64_t u0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
           const int64_t u1 = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift;
           const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
@@ -495,8 +508,8 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
   const uint64_t card = (uint64_t)G.card;
   // requests of the block's first and last ad; <= 2 requests -> user-bag hashes in shared memory
   const int64_t last = (base + 128 * GATHER_APT < a.n ? base + 128 * GATHER_APT : a.n) - 1;
-  const int rfirst = a.req_of_ad[a.a0 + base];
-  const int rlast = a.req_of_ad[a.a0 + last];
+  const int rfirst = req_at(a, a.a0 + base);
+  const int rlast = req_at(a, a.a0 + last);
   int64_t ub[2], ul[2];
 #pragma unroll
   for (int q = 0; q < 2; q++) {
@@ -517,7 +530,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
 #pragma unroll
     for (int i = 0; i < GATHER_APT; i++) {
       const uint64_t y = (uint64_t)checked(BA.ids[a.a0 + loc[i] - BA.id_shift], A.card, a.validate, a.err);
-      const int sl = (a.req_of_ad[a.a0 + loc[i]] == rfirst) ? 0 : 1;
+      const int sl = (req_at(a, a.a0 + loc[i]) == rfirst) ? 0 : 1;
       row[i] = cross_row_from_hx(s_hx[sl][0], y, card);
     }
     RawRow<T, K> raw[GATHER_APT];
@@ -538,13 +551,13 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
     const int64_t li = base + threadIdx.x + i * 128;
     if (li >= a.n) break;
     const int64_t ad = a.a0 + li;
-    const int sl = (a.req_of_ad[ad] == rfirst) ? 0 : 1;
+    const int sl = (req_at(a, ad) == rfirst) ? 0 : 1;
     int64_t u0, L;
     if (shared_hx) {
       u0 = sl ? ub[1] : ub[0];
       L = sl ? ul[1] : ul[0];
     } else {
-      const int r = a.req_of_ad[ad];
+      const int r = req_at(a, ad);
       u0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
       L = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift - u0;
     }
