@@ -1664,6 +1664,8 @@ extern "C" cold_status cold_topk(cold_ctx* c, const float* scores, const int32_t
   ta.G = 0;
   ta.Kl = 0;
   ta.cand_idx = nullptr;
+  ta.max_n = 0;
+  for (int r = 0; r < R; r++) ta.max_n = std::max(ta.max_n, ad_offsets_host[r + 1] - ad_offsets_host[r]);
   ta.idx = out_dev ? idx_out : (int32_t*)c->d_topk_out;
   ta.key = out_dev ? key_out : (float*)((uint8_t*)c->d_topk_out + (size_t)R * K * 4);
   c->mark_begin(st);
@@ -1710,6 +1712,7 @@ extern "C" cold_status cold_merge_topk(cold_ctx* c, const float* cand_key, const
   ta.R = R;
   ta.K = K;
   ta.G = G;
+  ta.max_n = G * Kl;
   ta.Kl = Kl;
   ta.cand_idx = cand_idx;
   ta.idx = idx_out;

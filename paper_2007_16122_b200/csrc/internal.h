@@ -219,6 +219,8 @@ struct TopkArgs {
   // (g, j) in rank order; the output position is cand_idx + the slice start floor(g * n_r / G)
   int G, Kl;
   const int32_t* cand_idx;
+  int max_n;                       // longest segment (host-known): keys are staged in smem when small
+  int stage;                       // set by launch_topk: smem key capacity (0 = read keys from global)
 };
 void launch_topk(const TopkArgs& a, cudaStream_t s);
 

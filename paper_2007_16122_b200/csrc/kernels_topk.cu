@@ -13,6 +13,7 @@ namespace cold {
 
 constexpr int TOPK_THREADS = 1024;
 constexpr int TOPK_MAX_K = 4096;
+constexpr int TOPK_STAGE = 12288;   // keys of a segment staged in shared memory when n <= this (48 KB)
 
 __device__ __forceinline__ uint32_t orderable(float f) {
   uint32_t u = __float_as_uint(f);
@@ -46,13 +47,24 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
     return orderable(v);
   };
 
+  // keys read once from global into shared memory (the radix passes and the collect re-read them)
+  int P = 1;
+  while (P < K) P <<= 1;
+  uint32_t* skey = reinterpret_cast<uint32_t*>(cand + P);
+  const bool staged = n <= a.stage;
+  if (staged) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) skey[i] = key_at(i);
+    __syncthreads();
+  }
+  auto key = [&](int i) -> uint32_t { return staged ? skey[i] : key_at(i); };
+
   // ---- radix select: the K-th largest orderable key ----
   uint32_t prefix = 0, mask = 0, need = (uint32_t)K;
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint32_t u = key_at(i);
+      const uint32_t u = key(i);
       if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
     }
     __syncthreads();
@@ -100,7 +112,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
     const int i = i0 + threadIdx.x;
     uint32_t u = 0;
     bool gt = false, eq = false;
-    if (i < n) { u = key_at(i); gt = u > T; eq = u == T; }
+    if (i < n) { u = key(i); gt = u > T; eq = u == T; }
     if (gt) {
       const uint32_t slot = atomicAdd(&s_gt_count, 1u);
       cand[slot] = ((unsigned long long)u << 32) | (0xffffffffu - (uint32_t)i);
@@ -129,8 +141,6 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
     }
     __syncthreads();
   }
-  int P = 1;
-  while (P < K) P <<= 1;
   for (int i = K + threadIdx.x; i < P; i += blockDim.x) cand[i] = 0ull;
   __syncthreads();
   // ---- bitonic sort, descending ----
@@ -161,14 +171,16 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
   }
 }
 
-void launch_topk(const TopkArgs& a, cudaStream_t s) {
+void launch_topk(const TopkArgs& a0, cudaStream_t s) {
+  TopkArgs a = a0;
   int P = 1;
   while (P < a.K) P <<= 1;
-  const size_t smem = (size_t)P * sizeof(unsigned long long);
+  a.stage = (a.max_n > 0 && a.max_n <= TOPK_STAGE) ? a.max_n : 0;
+  const size_t smem = (size_t)P * sizeof(unsigned long long) + (size_t)a.stage * sizeof(uint32_t);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TOPK_MAX_K * (int)sizeof(unsigned long long));
+                         TOPK_MAX_K * (int)sizeof(unsigned long long) + TOPK_STAGE * (int)sizeof(uint32_t));
     attr = true;
   }
   topk_kernel<<<a.R, TOPK_THREADS, smem, s>>>(a);
