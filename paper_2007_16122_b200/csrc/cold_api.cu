@@ -1325,11 +1325,18 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
   // Latency path (a few requests, scoring): the user side (pooling, u1 GEMV, ad -> request map) does not
   // feed the gather, which finds an ad's request by searching ad_offsets, so the two run concurrently
   // (fork onto the side stream, join before the FC stack). COLD_USER_FORK=0 serialises them.
-  static const bool fork_env = !(getenv("COLD_USER_FORK") && atoi(getenv("COLD_USER_FORK")) == 0);
-  const bool fork = fork_env && mode == RUN_SCORE && pl.R <= 4;
+  // COLD_USER_FORK=2: the user kernel stays on the caller's stream (launched first, so dispatched first)
+  // and the single gather span goes to the side stream instead.
+  static const int fork_env = getenv("COLD_USER_FORK") ? atoi(getenv("COLD_USER_FORK")) : 1;
+  const bool fork = fork_env != 0 && mode == RUN_SCORE && pl.R <= 4;
+  const bool one_span = pl.N <= (int64_t)c->chunk * c->gspan;
+  const bool gather_side = fork && fork_env == 2 && one_span && !pl.host;
+  cudaStream_t gst = st;   // stream of the gather launches
   if (fork) {
     CK(cudaEventRecord(c->ev_fork, st));
     CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
+  }
+  if (fork && !gather_side) {
     c->mark_begin(c->side_stream);
     launch_user(ua, pl.R, c->precision, c->side_stream);
     c->mark_end(COLD_PROF_USER, c->side_stream);
@@ -1338,6 +1345,7 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
     c->mark_begin(st);
     launch_user(ua, pl.R, c->precision, st);
     c->mark_end(COLD_PROF_USER, st);
+    if (gather_side) gst = c->side_stream;
   }
   CK(cudaGetLastError());
   bool joined = !fork;
@@ -1410,11 +1418,12 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
       launch_gather(g1, c->precision, st);
       c->mark_end(COLD_PROF_GATHER, st);
     } else {
-      c->mark_begin(st);
-      launch_gather(ga, c->precision, st);
-      c->mark_end(COLD_PROF_GATHER, st);
+      c->mark_begin(gst);
+      launch_gather(ga, c->precision, gst);
+      c->mark_end(COLD_PROF_GATHER, gst);
     }
-    if (!joined) {   // dense SE and the FC stack read x_u / u1 and req_of_ad
+    if (!joined) {   // dense SE and the FC stack read x_u / u1 and req_of_ad (or the side-stream gather's X)
+      if (gather_side) CK(cudaEventRecord(c->ev_user, c->side_stream));
       CK(cudaStreamWaitEvent(st, c->ev_user, 0));
       joined = true;
     }
