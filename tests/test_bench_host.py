@@ -42,3 +42,11 @@ def test_gather_access_model_tiny_tables_all_l2():
     m = bench.gather_access_model(sch, 10**6, 4, 6500.0)
     assert m["dram_random_rows_per_ad"] == 0
     assert m["l2_rows_per_ad"] > 0
+
+
+def test_usable_rate_more_servers_more_rate():
+    """S servers with the same service times sustain more load, at most S times the one-server bound."""
+    s = np.full(3000, 0.1)
+    r1 = bench.usable_rate(s, 1.0)
+    r4 = bench.usable_rate(s, 1.0, servers=4)
+    assert r1 < r4 < 4 * 1e4
