@@ -166,9 +166,10 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
       }
     }
   }
-  if (main_cta)
-    for (int64_t ad = a.ad_offsets[r] + threadIdx.x; ad < a.ad_offsets[r + 1]; ad += blockDim.x)
-      a.req_of_ad[ad] = r;
+  if (main_cta) {   // bounds in registers: the stores may alias ad_offsets, which would reload it per step
+    const int64_t e0 = a.ad_offsets[r], e1 = a.ad_offsets[r + 1];
+    for (int64_t ad = e0 + threadIdx.x; ad < e1; ad += blockDim.x) a.req_of_ad[ad] = r;
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
