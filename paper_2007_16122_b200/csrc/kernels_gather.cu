@@ -146,8 +146,19 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
   const int ostep = blockDim.x * gridDim.y;
   for (int o = blockIdx.y * blockDim.x + threadIdx.x; o < a.H && !a.stats; o += ostep) {
     float acc = a.b1[o];
-    if (!a.dense)   // dense SE: W1's user columns run inside FC1 with the gated per-ad x (u1 = b1)
-      for (int i = 0; i < d_u; i++) acc = fmaf(a.w1u_t[(int64_t)i * a.H + o], xs[i], acc);
+    if (!a.dense) {   // dense SE: W1's user columns run inside FC1 with the gated per-ad x (u1 = b1)
+      // 16 independent weight loads in flight per step (the loop was latency-bound: one L2 round trip
+      // per few FMAs); the accumulation order is unchanged
+      int i = 0;
+      for (; i + 16 <= d_u; i += 16) {
+        float w[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) w[j] = __ldg(a.w1u_t + (int64_t)(i + j) * a.H + o);
+#pragma unroll
+        for (int j = 0; j < 16; j++) acc = fmaf(w[j], xs[i + j], acc);
+      }
+      for (; i < d_u; i++) acc = fmaf(a.w1u_t[(int64_t)i * a.H + o], xs[i], acc);
+    }
     a.u1[(int64_t)r * a.H + o] = acc;
     if (a.u1t) {   // u1 = term_0 + term_1 (+ term_2), each RNE in 16 bits: the FC1 tensor-core operand
       float u = acc;
