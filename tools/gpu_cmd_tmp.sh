@@ -1,5 +1,3 @@
 python -m paper_2007_16122_b200.build >/dev/null
-timeout 900 python -m pytest tests -m gpu -x -q -k "not full_size" > gpurun_out/gpu_tests_s21.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_s21.log
-COLD_USER_FORK=0 timeout 300 python tools/probes/latency_profile.py > gpurun_out/latprof_s21_serial.txt 2>&1
-timeout 300 python tools/probes/latency_profile.py > gpurun_out/latprof_s21.txt 2>&1
-timeout 900 python bench.py --latency-sweep --latency-requests 3000 > gpurun_out/lat_s21.jsonl 2>&1
+BENCH_ARGS="--requests 2048 --no-e2e --no-latency --no-cpu --steps 5" timeout 1500 bash tools/sweep.sh s22a4: s22a2:COLD_GATHER_APT=2 s22g32:COLD_GSPAN=32 s22a4b: s22a2b:COLD_GATHER_APT=2 s22g32b:COLD_GSPAN=32
+python tools/show.py gpurun_out/sweep_s22*.log > gpurun_out/sweep_s22.txt 2>&1
