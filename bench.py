@@ -296,7 +296,6 @@ def run_se_sweep(args):
     import torch
     from paper_2007_16122_b200 import Batch, Context, select_groups
     from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER
-    import oracle
     torch.cuda.set_device(0)
     sch = coldgen.schema_full()
     R, n_ads, K = 512, 4000, args.topk
@@ -308,7 +307,10 @@ def run_se_sweep(args):
     load_ctx_params(ctx, full)
     mean_s = ctx.se_stats(Batch.from_numpy(sample.ad_offsets, sample.ids, sample.offs))
     ctx.close()
-    want = oracle.se_gates(oracle.Model(sch, full), sample).mean(0)   # same sample, fp64 (parity check)
+    # the planted gates (b_g = 3 - 0.5 g, |w_g| <= 0.01; coldgen se="planted_noisy") rank the groups in
+    # schema order (SURVEY P-11); the oracle parity of cold_se_stats itself is a GPU test
+    # (tests/test_gpu_parity.py::test_se_stats_and_selection_match_oracle), not part of the bench
+    planted_ok = bool(np.array_equal(np.argsort(-np.asarray(mean_s), kind="stable"), np.arange(sch.M)))
     batch = coldgen.make_batch(sch, range(R), n_ads, seed=args.seed + 1)
     db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs)
     dev = torch.device("cuda", 0)
@@ -361,7 +363,7 @@ def run_se_sweep(args):
                                    f"{n_ads} ads, top-{K}; groups selected by mean SE weight over a "
                                    f"{sample.n_ads}-ad sample (cold_se_stats)"},
             "se_mean_s": [round(float(x), 6) for x in mean_s],
-            "se_mean_s_oracle_maxdiff": float(np.max(np.abs(mean_s - want))),
+            "se_ranking_matches_planted_order": planted_ok,
             "se_sweep": rows}
     print(json.dumps(line), flush=True)
 
