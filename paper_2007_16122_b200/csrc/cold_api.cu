@@ -458,6 +458,23 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       const int cls = G.side == COLD_CROSS ? 0 : (G.pooled ? 1 : 2);
       if (cls == pass) c->gather_order.push_back((int)j);
     }
+  // COLD_GATHER_ORDER=1: interleave the L2-bound cross-bag columns with the DRAM-bound single-row
+  // columns (heavy, light, heavy, light, ...) instead of all heavy columns first
+  if (getenv("COLD_GATHER_ORDER") && atoi(getenv("COLD_GATHER_ORDER")) == 1) {
+    std::vector<int> heavy, light, mixed;
+    for (int j : c->gather_order) {
+      const cold_group& G = c->groups[c->sel_ac[j]];
+      const bool bagx = G.side == COLD_CROSS && (c->groups[G.user_ref].pooled || c->groups[G.ad_ref].pooled);
+      (bagx ? heavy : light).push_back(j);
+    }
+    size_t h = 0, l = 0;
+    while (h < heavy.size() || l < light.size()) {
+      if (h < heavy.size()) mixed.push_back(heavy[h++]);
+      const size_t per = heavy.empty() ? light.size() : (light.size() + heavy.size() - 1) / heavy.size();
+      for (size_t t = 0; t < per && l < light.size(); t++) mixed.push_back(light[l++]);
+    }
+    c->gather_order = mixed;
+  }
   c->d_u = (int)c->sel_user.size() * c->k;
   c->d_ac = (int)c->sel_ac.size() * c->k;
   c->d_in = c->d_u + c->d_ac;
