@@ -616,3 +616,50 @@ def test_full_size_configs4_sampled():
         assert np.all(np.diff(kk[r]) <= 0)
         np.testing.assert_array_equal(seg[ki[r]], kk[r])
         assert (seg > kk[r, -1]).sum() <= K
+
+
+# ---- serving: CUDA-graph capture of one request (the latency bench's replay path) ---------------
+
+def test_graph_replay_matches_direct_call():
+    """cold_score_request + cold_topk captured in a CUDA graph (including the latency path's side-stream
+    fork/join) and replayed on new ids copied into the static buffers give exactly what direct calls give,
+    and the replay matches the oracle within tolerance."""
+    import torch
+    sch, params, batch = small_case("paper", R=3, n_ads=(700, 700, 700), precision="f16", cap=20000, seed=97)
+    ctx = make_ctx(sch, params, max_ads=4096, max_requests=4)
+    from paper_2007_16122_b200 import Batch
+    singles = [coldgen.sub_batch(batch, [i]) for i in range(3)]
+    dev = [device_batch(b) for b in singles]
+    static = device_batch(singles[0])
+    n, K = 700, 50
+    ao = np.asarray([0, n], np.int32)
+    sc = torch.empty(n, device="cuda")
+    idx = torch.empty(K, dtype=torch.int32, device="cuda")
+    key = torch.empty(K, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx.score_request(static, sc, stream=s)
+        ctx.topk(sc, static.ad_offsets, ao, K, idx, key, stream=s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ctx.score_request(static, sc, stream=s)
+        ctx.topk(sc, static.ad_offsets, ao, K, idx, key, stream=s)
+    for i in (1, 2):
+        with torch.cuda.stream(s):
+            for dst, src in zip(static.ids + static.offs, dev[i].ids + dev[i].offs):
+                if dst is not None:
+                    dst.copy_(src)
+            g.replay()
+        s.synchronize()
+        got_sc, got_idx = sc.clone(), idx.clone()
+        ref_sc = torch.empty(n, device="cuda")
+        ctx.score_request(dev[i], ref_sc)
+        ref_idx = torch.empty(K, dtype=torch.int32, device="cuda")
+        ref_key = torch.empty(K, dtype=torch.float32, device="cuda")
+        ctx.topk(ref_sc, dev[i].ad_offsets, ao, K, ref_idx, ref_key)
+        torch.cuda.synchronize()
+        assert torch.equal(got_sc, ref_sc) and torch.equal(got_idx, ref_idx)
+        p, z = oracle.score(oracle.Model(sch, params), singles[i])
+        _check_scores(got_sc.cpu().numpy().astype(np.float64), p, z, "f16", f"graph replay request {i}")
+    ctx.close()
