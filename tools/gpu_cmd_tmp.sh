@@ -1,2 +1,3 @@
-python -m paper_2007_16122_b200.build >/dev/null
-timeout 600 python -m pytest tests -m gpu -x -q -k "host_batch" > gpurun_out/gpu_tests_s26.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_s26.log
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_r01k.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/gpu_tests_r01k.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests_r01k.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r01k.log 2>&1; echo "rc=$?" >> gpurun_out/smoke_r01k.log
