@@ -43,7 +43,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="f16", choices=["f16", "bf16", "f32"])
-    ap.add_argument("--requests", type=int, default=8192, help="requests per GPU per step")
+    ap.add_argument("--requests", type=int, default=8192,
+                    help="requests per step: the whole stream, partitioned over the GPUs (strong scaling), or "
+                         "per GPU with --scaling weak")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--ads", type=int, default=10000, help="ads per request")
     ap.add_argument("--topk", type=int, default=500)
     ap.add_argument("--chunk", type=int, default=0)
@@ -268,7 +271,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": config_dict(args, sch),
+        "config": config_dict(args, sch, args.gpus),
         "cpu_baseline": {"value": v, "unit": "ads/s", "cores": cores, "kind": "oracle",
                          "sample": f"each step = {n} ads of request 0 of the workload stream"},
         "e2e": {"value": v, "unit": "ads/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -276,13 +279,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(args, sch):
-    return {"workload": f"BASELINE configs[4] per GPU: {args.requests} requests x {args.ads} ads "
+def config_dict(args, sch, world=1):
+    per = "per GPU" if args.scaling == "weak" else f"partitioned over {world} GPU(s)"
+    return {"workload": f"BASELINE configs[4]: {args.requests} requests x {args.ads} ads {per} "
                         f"(S-paper schema {sch.name}, M={sch.M}, k={sch.k}, FC {sch.M * sch.k}x"
                         + "x".join(map(str, sch.widths)) + f", {args.precision} + linear_log, top-K={args.topk})",
-            "requests_per_gpu": args.requests, "ads_per_request": args.ads, "top_k": args.topk,
+            "requests": args.requests, "requests_per_gpu": args.requests if args.scaling == "weak"
+            else -(-args.requests // world), "ads_per_request": args.ads, "top_k": args.topk,
             "ids": "uniform", "l2": "inputs larger than L2 (ids 2.6 GB + tables 4.8 GB per GPU); no flush",
-            "parallelism": f"request partition x{args.gpus}, replicated params",
+            "parallelism": f"request partition x{world} ({args.scaling} scaling), replicated params, NCCL top-K "
+                           f"all-gather",
             "se": "dense (AMB-1 Doc B reading, user block not hoisted)" if getattr(args, "se_dense", False)
                   else "per-group (AMB-1)"}
 
@@ -295,7 +301,7 @@ def run_se_sweep(args):
     lighter model (its own FC1 over D_in = 16 K_g) is timed on 512 requests x 4000 ads + top-500."""
     import torch
     from paper_2007_16122_b200 import Batch, Context, select_groups
-    from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER
+    from paper_2007_16122_b200.cold import PROF_GATHER
     torch.cuda.set_device(0)
     sch = coldgen.schema_full()
     R, n_ads, K = 512, 4000, args.topk
@@ -344,16 +350,17 @@ def run_se_sweep(args):
         c.profile(True)
         for _ in range(args.steps):
             step()
-        pm, pn = c.profile_read()
+        pm, pn, pf = c.profile_read(with_flop=True)
         c.profile(False)
         info = c.info()
-        flops = fc_flops_per_ad(sch, info["d_ad"])
-        fc_ms = sum(pm[PROF_FC + l] for l in range(len(sch.widths)))
+        cls = kernel_classes(sch, pm, pn, pf)
+        fc_ms = sum(v["total_ms"] for v in cls.values() if v.get("fc"))
+        fc_flop = sum(v.get("flop_per_launch", 0.0) * v["launches"] for v in cls.values() if v.get("fc"))
         n_user = sum(1 for g in sel if sch.groups[g].side == coldgen.USER)
         rows.append({"k_g": kg, "selected_user_ad_cross": [n_user, sum(1 for g in sel if sch.groups[g].side == coldgen.AD),
                                                             sum(1 for g in sel if sch.groups[g].side == coldgen.CROSS)],
                      "d_in": info["d_in"], "d_ad_cross": info["d_ad"], "ads_per_s": batch.n_ads / (ms / 1e3),
-                     "ms_per_step": ms, "fc_tflops": batch.n_ads * args.steps * sum(flops) / (fc_ms / 1e3) / 1e12,
+                     "ms_per_step": ms, "fc_tflops": fc_flop / (fc_ms / 1e3) / 1e12,
                      "gather_ms": float(pm[PROF_GATHER] / args.steps), "fc_ms": float(fc_ms / args.steps)})
         c.close()
     line = {"metric": METRIC, "value": rows[-1]["ads_per_s"], "unit": "ads/s", "n_gpus": 1, "steps": args.steps,
@@ -668,6 +675,165 @@ def run_latency_sweep(args):
     print(json.dumps(out), flush=True)
 
 
+class RankStep:
+    """One bench step on this rank: cold_score_batch over the rank's requests,
+    cold_topk into device buffers, and at N > 1 the per-request top-K all-gather (dist.gather_topk:
+    NCCL in bench, gloo in the one-GPU multi-process test). The result of a step is
+    `result()`: this rank's [r_pad * K] idx / key at N = 1, the rank-major [world * r_pad * K]
+    gathered blocks at N > 1 (unpad with dist.unpad_gathered)."""
+
+    def __init__(self, ctx, batch, K, world, r_pad, dev):
+        import torch
+        from paper_2007_16122_b200 import Batch
+        self.ctx, self.batch, self.K, self.world, self.r_pad = ctx, batch, K, world, r_pad
+        self.db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs, device=dev)
+        self.scores = torch.empty(batch.n_ads, dtype=torch.float32, device=dev)
+        self.idx = torch.zeros(r_pad * K, dtype=torch.int32, device=dev)
+        self.key = torch.zeros(r_pad * K, dtype=torch.float32, device=dev)
+        self.g_idx = self.g_key = None
+        if world > 1:
+            self.g_idx = torch.empty(world * r_pad * K, dtype=torch.int32, device=dev)
+            self.g_key = torch.empty(world * r_pad * K, dtype=torch.float32, device=dev)
+        self.gather_events = None     # a list: (start, end) CUDA events around every top-K gather
+
+    def result(self):
+        return (self.g_idx, self.g_key) if self.world > 1 else (self.idx, self.key)
+
+    def __call__(self, b=None):
+        import torch
+        from paper_2007_16122_b200.dist import gather_topk
+        self.ctx.score_batch(b if b is not None else self.db, self.scores)
+        self.ctx.topk(self.scores, self.db.ad_offsets, self.batch.ad_offsets, self.K, self.idx, self.key)
+        if self.world > 1:
+            ev = None
+            if self.gather_events is not None:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
+            gather_topk(self.idx, self.key, self.g_idx, self.g_key)
+            if ev is not None:
+                ev[1].record()
+                self.gather_events.append(ev)
+
+
+class SplitRequest:
+    """F1 (P:248-250 / P:496-498 split one query's ads into parallel inference calls
+    and merge the results): this rank scores its slice [floor(g n/G), floor((g+1) n/G)) of one
+    request (cold_score_request), keeps its top-K (cold_topk), the G candidate lists are
+    all-gathered rank-major, and cold_merge_topk picks the request's top-K over request positions."""
+
+    def __init__(self, ctx, n_full, n_mine, K, world, dev):
+        import torch
+        self.ctx, self.K, self.world = ctx, K, world
+        self.kl = min(K, n_mine)
+        self.sscores = torch.empty(max(1, n_mine), dtype=torch.float32, device=dev)
+        self.lidx = torch.empty(self.kl, dtype=torch.int32, device=dev)
+        self.lkey = torch.empty(self.kl, dtype=torch.float32, device=dev)
+        self.cidx = torch.empty(world * self.kl, dtype=torch.int32, device=dev)
+        self.ckey = torch.empty(world * self.kl, dtype=torch.float32, device=dev)
+        self.midx = torch.empty(K, dtype=torch.int32, device=dev)
+        self.mkey = torch.empty(K, dtype=torch.float32, device=dev)
+        self.ao_full = np.asarray([0, n_full], np.int32)
+        self.d_ao_full = torch.from_numpy(self.ao_full).to(dev)
+        self.ao_loc = np.asarray([0, n_mine], np.int32)
+
+    def __call__(self, b):
+        from paper_2007_16122_b200.dist import gather_topk
+        self.ctx.score_request(b, self.sscores)
+        self.ctx.topk(self.sscores, b.ad_offsets, self.ao_loc, self.kl, self.lidx, self.lkey)
+        gather_topk(self.lidx, self.lkey, self.cidx, self.ckey)
+        self.ctx.merge_topk(self.ckey, self.cidx, self.world, self.kl, self.d_ao_full, self.ao_full, self.K,
+                            self.midx, self.mkey)
+        return self.midx, self.mkey
+
+
+def rank_requests(args, world, rank):
+    """The rank's share of the configs[4] request stream: strong scaling (default) partitions the
+    one stream of args.requests requests into near-equal contiguous blocks; weak
+    scaling gives every rank its own block of args.requests."""
+    from paper_2007_16122_b200.dist import request_block, split_even
+    if args.scaling == "weak":
+        return request_block(args.requests, rank), args.requests
+    return split_even(args.requests, world, rank), -(-args.requests // world)
+
+
+def kernel_classes(sch, prof_ms, prof_n, prof_fl, names_extra=None):
+    """Per kernel class of the profiled region: launches, average device time, share of the summed
+    kernel time, and for the FC classes the algorithmic TFLOP/s (the library counts each launch's
+    FLOPs from the rows it covered, so mixed chain / layer-by-layer steps attribute correctly)."""
+    from paper_2007_16122_b200.cold import (PROF_CHAIN, PROF_FC, PROF_GATHER, PROF_MLP_F32, PROF_SE_DENSE,
+                                            PROF_TAIL, PROF_TOPK, PROF_USER)
+    names = {PROF_USER: "user", PROF_GATHER: "gather", PROF_TOPK: "topk", PROF_SE_DENSE: "se_dense",
+             PROF_CHAIN: "chain (fc1+fc2+fc3)", PROF_TAIL: "tail (fc4+fc5+head)", PROF_MLP_F32: "mlp_f32 (all layers)"}
+    for l in range(len(sch.widths) - 1):
+        names[PROF_FC + l] = f"gemm fc{l + 1}" + ("+head" if l == len(sch.widths) - 2 else "")
+    fc_kinds = {PROF_CHAIN, PROF_TAIL, PROF_MLP_F32} | {PROF_FC + l for l in range(len(sch.widths) - 1)}
+    total = float(prof_ms.sum())
+    out = {}
+    for kind, name in names.items():
+        if not prof_n[kind]:
+            continue
+        d = {"launches": int(prof_n[kind]), "avg_us": float(prof_ms[kind] / prof_n[kind] * 1e3),
+             "share": float(prof_ms[kind] / total), "total_ms": float(prof_ms[kind]), "fc": kind in fc_kinds}
+        if prof_fl[kind] > 0:
+            d["tflops"] = float(prof_fl[kind] / (prof_ms[kind] / 1e3) / 1e12)
+            d["flop_per_launch"] = float(prof_fl[kind] / prof_n[kind])
+        out[name] = d
+    return out
+
+
+def load_ncu_summary():
+    """profiles/ncu_traffic.json: per-kernel ncu --set full figures of the committed capture (DRAM bytes
+    per launch and per ad, tensor-pipe %), with the commit it was taken at."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f)
+
+
+def fc_roofline(classes, peaks, peak_src, clocks, ncu):
+    """Roofline of the dominant FC kernel class (the largest share of the step): algorithmic TFLOP/s
+    over its CUDA-event time against the measured bf16 peaks (fp16 runs at the bf16 rate on sm_100):
+    `frac` = burst (a plain cuBLAS 8192^3 bf16 GEMM, MEASURED_PEAKS.json), `frac_sustained` = the
+    seconds-long loop, and `frac_sustained_at_run_clock` = that sustained figure scaled from the clock
+    it was measured at to this run's median SM clock (the kernel's honest fraction when the run sat at
+    a higher power-capped clock than the peak measurement). `tensor_active_ncu` is ncu's
+    sm__pipe_tensor_cycles_active of the committed capture of the same kernel."""
+    fc = {k: v for k, v in classes.items() if v.get("fc")}
+    if not fc:
+        return None
+    name, d = max(fc.items(), key=lambda kv: kv[1]["total_ms"])
+    burst = float(peaks.get("bf16_tflops"))
+    sus = float(peaks.get("bf16_tflops_sustained", burst))
+    sus_mhz = (peaks.get("clocks_under_load") or {}).get("sm_mhz_median")
+    run_mhz = (clocks or {}).get("sm_mhz")
+    a = d.get("tflops", 0.0)
+    r = {"bound": "tensor", "kernel": name, "achieved": a, "peak": burst, "unit": "TFLOP/s", "frac": a / burst,
+         "frac_burst": a / burst, "frac_sustained": a / sus, "peak_sustained": sus,
+         "peak_source": f"bf16_tflops (burst) {peak_src}; fp16 runs at the bf16 rate",
+         "algorithmic": f"{d.get('flop_per_launch', 0):.4g} FLOP per launch (rows x 2 sum(in x out) of the covered "
+                        f"layers), avg launch {d['avg_us']:.1f} us"}
+    if sus_mhz and run_mhz:
+        at_clock = sus * float(run_mhz) / float(sus_mhz)
+        r["peak_sustained_at_run_clock"] = at_clock
+        r["frac_sustained_at_run_clock"] = a / at_clock
+        r["clock_note"] = (f"sustained peak measured at a median {sus_mhz:.0f} MHz; this run's median SM clock "
+                           f"{run_mhz:.0f} MHz")
+    k = ncu.get("kernels", {}).get(name.split(" ")[0], {})
+    r["traffic"] = None
+    if k.get("dram_bytes_per_ad") and k.get("flop_per_ad") and d.get("flop_per_launch"):
+        # the capture's bytes per ad x this run's ads per launch (FLOPs per launch / FLOPs per ad)
+        r["traffic"] = k["dram_bytes_per_ad"] * d["flop_per_launch"] / k["flop_per_ad"]
+        r["traffic_note"] = f"ncu dram read+write of the committed capture: {k['dram_bytes_per_ad']:.0f} B/ad"
+    r["tensor_active_ncu"] = k.get("tensor_active_pct")
+    r["ncu_commit"] = ncu.get("commit")
+    bad = [k for k, v in fc.items() if v.get("tflops", 0.0) > 1.2 * sus]
+    if bad:
+        r["suspect"] = (f"{bad}: above 1.2x the measured sustained peak, i.e. the timed launches did not do "
+                        f"the counted work; do not use this line")
+    return r
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -685,8 +851,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2007_16122_b200 import Batch, Context
-    from paper_2007_16122_b200.cold import PROF_FC, PROF_GATHER, PROF_SE_DENSE, PROF_TOPK, PROF_USER
-    from paper_2007_16122_b200.dist import gather_topk, request_block
+    from paper_2007_16122_b200.cold import PROF_GATHER
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -699,30 +864,37 @@ def main():
     sch = schema_for(args)
     t_setup = time.perf_counter()
     params = coldgen.make_params(sch, seed=args.seed, precision=args.precision)
-    batch = coldgen.make_batch(sch, request_block(args.requests, rank), args.ads, seed=args.seed + 1)
+    reqs, r_pad = rank_requests(args, world, rank)
+    batch = coldgen.make_batch(sch, reqs, args.ads, seed=args.seed + 1)
     N = batch.n_ads
     ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, device=local, max_ads=N,
-                  max_requests=args.requests, chunk_ads=args.chunk, se_mode="dense" if args.se_dense else "group")
+                  max_requests=max(batch.R, 1), chunk_ads=args.chunk, se_mode="dense" if args.se_dense else "group")
     load_ctx_params(ctx, params, dense_se_params(sch, args.seed + 17) if args.se_dense else None)
-    db = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs)
     K = args.topk
-    scores = torch.empty(N, dtype=torch.float32, device=dev)
-    idx = torch.empty(args.requests * K, dtype=torch.int32, device=dev)
-    key = torch.empty(args.requests * K, dtype=torch.float32, device=dev)
-    g_idx = torch.empty(world * args.requests * K, dtype=torch.int32, device=dev) if world > 1 else None
-    g_key = torch.empty(world * args.requests * K, dtype=torch.float32, device=dev) if world > 1 else None
+    step = RankStep(ctx, batch, K, world, r_pad, dev)
     stream = torch.cuda.current_stream()
     setup_s = time.perf_counter() - t_setup
+    n_all = [N]
+    if world > 1:
+        t = torch.tensor([N], device=dev, dtype=torch.int64)
+        gl = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(gl, t)
+        n_all = [int(x.item()) for x in gl]
 
-    def step(b, out_idx, out_key):
-        ctx.score_batch(b, scores)
-        ctx.topk(scores, db.ad_offsets, batch.ad_offsets, K, out_idx, out_key)
-        if world > 1:
-            gather_topk(idx, key, g_idx, g_key)
+    def max_over_ranks(ms):
+        if world == 1:
+            return ms, [ms]
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        gl = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(gl, t)
+        per = [float(x.item()) for x in gl]
+        return max(per), per
 
-    def timed(b, out_idx, out_key, steps, sampler=None, profile=False):
+    def timed(fn, steps, sampler=None, profile=False):
+        """W warm-up steps, barrier + sync, `steps` timed steps between CUDA events on the launching
+        stream, sync + barrier; returns the max over ranks."""
         for _ in range(args.warmup):
-            step(b, out_idx, out_key)
+            fn()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -733,23 +905,19 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
-            step(b, out_idx, out_key)
+            fn()
         e1.record(stream)
         e1.synchronize()
         torch.cuda.synchronize()
         clocks = sampler.stop() if sampler else None
         prof = None
         if profile:
-            prof = ctx.profile_read()
+            prof = ctx.profile_read(with_flop=True)
             ctx.profile(False)
         if world > 1:
             dist.barrier()
-        ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms, clocks, prof
+        ms, per = max_over_ranks(e0.elapsed_time(e1))
+        return ms, per, clocks, prof
 
     gpu_id = local
     try:
@@ -757,73 +925,45 @@ def main():
     except Exception:
         pass
     sampler = ClockSampler(gpu_id)
-    ms, clocks, _ = timed(db, idx, key, args.steps, sampler=sampler, profile=False)
+    ms, per_rank_ms, clocks, _ = timed(step, args.steps, sampler=sampler)
     ms_step = ms / args.steps
-    total_ads = N * world * args.steps
+    total_ads = sum(n_all) * args.steps
     value = total_ads / (ms / 1e3)
     # per-kernel device time: the same steps again with a CUDA-event pair around every launch
     # (the library records them on the launching stream); kept out of the `value` region because
     # an event record between kernels serialises their tails.
-    ms_prof, _, prof = timed(db, idx, key, args.steps, profile=True)
+    step.gather_events = [] if world > 1 else None
+    ms_prof, _, _, prof = timed(step, args.steps, profile=True)
+    gather_ms = None
+    if step.gather_events:
+        torch.cuda.synchronize()
+        g = sum(a.elapsed_time(b) for a, b in step.gather_events[-args.steps:]) / args.steps
+        gather_ms, _ = max_over_ranks(g)
+    step.gather_events = None
 
-    # ---- roofline of the dominant kernel (FC2, the largest layer: 54.7% of FLOPs) ----
     peaks, peak_src = measured_peaks()
-    prof_ms, prof_n = prof
+    prof_ms, prof_n, prof_fl = prof
     info = ctx.info()
-    d_ac = info["d_ad"]
-    layer_flops = fc_flops_per_ad(sch, d_ac)
-    per_kernel = {}
-    names = {PROF_USER: "user", PROF_GATHER: "gather", PROF_TOPK: "topk", PROF_SE_DENSE: "se_dense"}
-    n_layers = len(sch.widths)
-    # a profiled FC kind covers its layer up to the next kind that launched (fused kernels);
-    # the last one also covers the head
-    fc_kinds = [l for l in range(n_layers) if prof_n[PROF_FC + l]]
-    covers = {}
-    for i, l in enumerate(fc_kinds):
-        hi = fc_kinds[i + 1] if i + 1 < len(fc_kinds) else n_layers
-        covers[l] = list(range(l, hi))
-        names[PROF_FC + l] = "+".join(f"fc{j + 1}" for j in covers[l])
-    step_kernel_ms = float(prof_ms.sum())
-    for kind, name in names.items():
-        if prof_n[kind]:
-            per_kernel[name] = {"launches": int(prof_n[kind]), "avg_us": float(prof_ms[kind] / prof_n[kind] * 1e3),
-                                "share": float(prof_ms[kind] / step_kernel_ms)}
-    for l, layers in covers.items():
-        kind = PROF_FC + l
-        fl = N * args.steps * sum(layer_flops[j] for j in layers)
-        per_kernel[names[kind]]["tflops"] = fl / (prof_ms[kind] / 1e3) / 1e12
+    classes = kernel_classes(sch, prof_ms, prof_n, prof_fl)
+    ncu = load_ncu_summary()
+    roofline = fc_roofline(classes, peaks, peak_src, clocks, ncu)
     gb_per_ad, rows_per_ad = gather_bytes_per_ad(sch, 2 if args.precision != "f32" else 4)
-    if prof_n[PROF_GATHER]:
-        per_kernel["gather"]["gbs"] = N * args.steps * gb_per_ad / (prof_ms[PROF_GATHER] / 1e3) / 1e9
-    dom = PROF_FC + 1 if 1 in covers else PROF_FC
-    peak_tf = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-    achieved = per_kernel[names[dom]]["tflops"]
-    traffic, traffic_g = None, None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        with open(tpath) as f:
-            tj = json.load(f)
-        traffic = tj.get("dominant_dram_bytes_per_launch", tj.get("fc2_dram_bytes_per_launch"))
-        if tj.get("gather_dram_bytes_per_ad") and prof_n[PROF_GATHER]:
-            # the capture's gather launch covered a different span: scale per ad to this run's launches
-            traffic_g = tj["gather_dram_bytes_per_ad"] * N * args.steps / float(prof_n[PROF_GATHER])
-    roofline = {"bound": "tensor", "kernel": names[dom], "achieved": achieved, "peak": peak_tf,
-                "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
-                "peak_source": f"bf16_tflops_sustained {peak_src} (fp16 runs at the bf16 rate; kernel timed "
-                               f"inside a long step)",
-                "algorithmic": f"{sum(layer_flops[j] for j in covers[dom - PROF_FC])} FLOP/ad x ads per launch"}
     roofline_gather = None
     if prof_n[PROF_GATHER]:
         hb = float(peaks["hbm_gbs"])
-        ga = per_kernel["gather"]["gbs"]
+        ga = N * args.steps * gb_per_ad / (prof_ms[PROF_GATHER] / 1e3) / 1e9
+        classes["gather"]["gbs"] = ga
+        gk = ncu.get("kernels", {}).get("gather", {})
+        traffic_g = gk["dram_bytes_per_ad"] * N * args.steps / float(prof_n[PROF_GATHER]) \
+            if gk.get("dram_bytes_per_ad") else None
         roofline_gather = {"bound": "hbm", "kernel": "gather", "achieved": ga, "peak": hb, "unit": "GB/s",
                            "frac": ga / hb, "traffic": traffic_g,
-                           "traffic_note": "ncu dram read+write bytes per ad (profiles/ncu_traffic.json) x ads per "
-                                           "launch: below the algorithmic bytes because L2 serves repeated rows of "
-                                           "the column-wise gather",
+                           "traffic_note": "ncu dram read+write bytes per ad of the committed capture "
+                                           "(profiles/ncu_traffic.json) x ads per launch: below the algorithmic "
+                                           "bytes because L2 serves repeated rows of the column-wise gather",
                            "algorithmic": f"{gb_per_ad:.0f} B/ad ({rows_per_ad:.0f} rows x {sch.k} x 2 B + ids "
                                           f"+ X_ac write)"}
-        span_ads = min(N, info["chunk_ads"] * int(os.environ.get("COLD_GSPAN", "16")))
+        span_ads = min(N, info["chunk_ads"] * int(info.get("gather_span_chunks", 16) or 16))
         model = gather_access_model(sch, span_ads, 2 if args.precision != "f32" else 4, hb)
         g_ads = N * args.steps / (prof_ms[PROF_GATHER] / 1e3)
         model.update({"achieved_ads_per_s": g_ads,
@@ -834,48 +974,38 @@ def main():
                               "from the per-group L2 / DRAM split of the column-wise span, DRAM and L2 time "
                               "overlapped (max) or serial (sum)"})
         roofline_gather["random_access_model"] = model
-    fc_total_ms = sum(prof_ms[PROF_FC + l] for l in covers)
-    fc_flops_all = N * args.steps * sum(layer_flops)
-    fc_stack = {"tflops": fc_flops_all / (fc_total_ms / 1e3) / 1e12,
-                "frac": fc_flops_all / (fc_total_ms / 1e3) / 1e12 / peak_tf}
+    fc_ms = sum(v["total_ms"] for v in classes.values() if v.get("fc"))
+    fc_flop = sum(v.get("flop_per_launch", 0.0) * v["launches"] for v in classes.values() if v.get("fc"))
+    fc_stack = {"tflops": fc_flop / (fc_ms / 1e3) / 1e12 if fc_ms else None,
+                "note": "every FC kernel class of the profiled region: algorithmic FLOPs / summed device time"}
+    if fc_ms:
+        fc_stack["frac_burst"] = fc_stack["tflops"] / float(peaks["bf16_tflops"])
     gpu_launches = int(prof_n.sum())
 
-    # ---- e2e: host (pinned) inputs through the C ABI, top-K back to host, every step ----
+    # ---- e2e: host (pinned) inputs through the C ABI; the step's top-K (gathered at N > 1) lands in
+    # device memory and is read back to pinned host memory inside the timed region ----
     e2e = None
     if not args.no_e2e:
         hb = Batch.from_numpy(batch.ad_offsets, batch.ids, batch.offs, pin=True)
-        h_idx = torch.empty(args.requests * K, dtype=torch.int32).pin_memory()
-        h_key = torch.empty(args.requests * K, dtype=torch.float32).pin_memory()
+        res_idx, res_key = step.result()
+        h_idx = torch.empty(res_idx.numel(), dtype=torch.int32).pin_memory()
+        h_key = torch.empty(res_key.numel(), dtype=torch.float32).pin_memory()
+        reader = rank == 0          # at N > 1 the merged result is consumed on rank 0
 
-        def e2e_step(b, oi, ok):
-            ctx.score_batch(hb, scores)
-            ctx.topk(scores, db.ad_offsets, batch.ad_offsets, K, h_idx, h_key)
-            if world > 1:
-                gather_topk(idx, key, g_idx, g_key)
+        def e2e_step():
+            step(hb)
+            if reader:
+                h_idx.copy_(res_idx, non_blocking=True)
+                h_key.copy_(res_key, non_blocking=True)
 
-        # same procedure as `timed`
-        for _ in range(args.warmup):
-            e2e_step(hb, h_idx, h_key)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step(hb, h_idx, h_key)
-        e1.record(stream)
-        e1.synchronize()
-        torch.cuda.synchronize()
-        ms_e = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([ms_e], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms_e = float(t.item())
+        ms_e, _, _, _ = timed(e2e_step, args.steps)
         h2d = sum(int(x.nbytes) for x in batch.ids if x is not None) + \
             sum(int(x.nbytes) for x in batch.offs if x is not None) + int(batch.ad_offsets.nbytes)
-        d2h = args.requests * K * 8
+        d2h = int(h_idx.numel() * 4 + h_key.numel() * 4)
         e2e = {"value": total_ads / (ms_e / 1e3), "unit": "ads/s", "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e / args.steps}
+               "d2h_bytes_per_step": d2h, "ms_per_step": ms_e / args.steps,
+               "note": "per rank: the rank's pinned-host ids staged by the library (H2D inside the timed region); "
+                       "top-K to device, gathered over NCCL at N > 1, D2H of the (gathered) top-K on rank 0"}
 
     # ---- p50 / p99 request latency at configs[1] (1 user x 4000 ads), device-timed ----
     latency = None
@@ -928,33 +1058,15 @@ def main():
                 one = coldgen.sub_batch(lb, [i])
                 ao_s, ids_s, offs_s, _ = slice_requests(one.ad_offsets, one.ids, one.offs, sides, world, rank)
                 mine.append(Batch.from_numpy(ao_s, ids_s, offs_s))
-            n_mine = int(ao_s[-1])
-            sscores = torch.empty(n_mine, dtype=torch.float32, device=dev)
-            lidx = torch.empty(K, dtype=torch.int32, device=dev)
-            lkey = torch.empty(K, dtype=torch.float32, device=dev)
-            cidx = torch.empty(world * K, dtype=torch.int32, device=dev)
-            ckey = torch.empty(world * K, dtype=torch.float32, device=dev)
-            midx = torch.empty(K, dtype=torch.int32, device=dev)
-            mkey = torch.empty(K, dtype=torch.float32, device=dev)
-            ao_full = np.asarray([0, args.ads], np.int32)
-            d_ao_full = torch.from_numpy(ao_full).to(dev)
-            ao_loc = np.asarray([0, n_mine], np.int32)
-
-            def split_request(b):
-                ctx.score_request(b, sscores)
-                ctx.topk(sscores, b.ad_offsets, ao_loc, K, lidx, lkey)
-                dist.all_gather_into_tensor(ckey, lkey)
-                dist.all_gather_into_tensor(cidx, lidx)
-                ctx.merge_topk(ckey, cidx, world, K, d_ao_full, ao_full, K, midx, mkey)
-
+            split = SplitRequest(ctx, args.ads, int(ao_s[-1]), K, world, dev)
             for i in range(min(10, nl)):
-                split_request(mine[i])
+                split(mine[i])
             torch.cuda.synchronize()
             dist.barrier()
             evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(nl)]
             for i in range(nl):
                 evs[i][0].record(stream)
-                split_request(mine[i])
+                split(mine[i])
                 evs[i][1].record(stream)
             torch.cuda.synchronize()
             lat = torch.tensor([a.elapsed_time(b) for a, b in evs], dtype=torch.float64, device=dev)
@@ -975,17 +1087,23 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "ads/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": args.precision, "data": "synthetic (seeded ids, tables, weights)",
-            "config": config_dict(args, sch),
+            "config": config_dict(args, sch, world),
             "roofline": roofline, "roofline_gather": roofline_gather, "fc_stack": fc_stack,
-            "kernels": per_kernel, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+            "kernels": classes, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
             "clocks": clocks, "latency": latency, "latency_split": latency_split, "setup_s": setup_s,
             "compressed_activations": bool(info.get("compressed_activations", 0)),
             "profiled_region": {"ms_per_step": ms_prof / args.steps,
                                 "note": "per-kernel CUDA events (kernels, roofline) come from this second timed "
                                         "region of the same steps"},
         }
+        if world > 1:
+            line["ranks"] = {"ads_per_rank": n_all, "ms_per_step_per_rank": [m / args.steps for m in per_rank_ms],
+                             "imbalance_max_over_min": max(per_rank_ms) / min(per_rank_ms),
+                             "topk_gather_ms_per_step": gather_ms,
+                             "gather_note": "max over ranks of CUDA events around the NCCL all-gather of the "
+                                            "per-request top-K (profiled region)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -149,7 +149,12 @@ typedef struct {
   const int32_t* const* offs;    /* host array [M] of pointers: USER -> [R+1]; AD pooled -> [N_tot+1];
                                     otherwise NULL */
   const int32_t* const* offs_host;/* host array [M] of host copies of `offs` (NULL entries allowed when
-                                    ids are device memory; required for pooled groups of a host batch) */
+                                    ids are device memory; required for pooled groups of a host batch).
+                                    Every non-NULL entry is validated on the host before any launch:
+                                    offs[0] == 0 and non-decreasing over its R+1 (USER) or N_tot+1 (AD)
+                                    entries, else COLD_ERR_INVALID_ARG. Bag offsets given only in device
+                                    memory are NOT checked (a precondition: malformed device offsets read
+                                    out of bounds). */
 } cold_batch;
 
 typedef struct {
@@ -161,6 +166,7 @@ typedef struct {
   int32_t tensor_core;           /* 1 if the FC stack runs on tcgen05 */
   int64_t device_bytes;          /* device memory owned by the ctx */
   int32_t compressed_activations;/* 1 if the activation buffers got compressible memory (COLD_COMPRESS=1) */
+  int32_t gather_span_chunks;    /* chunks per column-wise gather pass */
 } cold_info;
 
 /* Create a context on config->device: validates the schema (AMB-1..AMB-18 readings in
@@ -242,17 +248,27 @@ cold_status cold_select_groups(const double* mean_s, int32_t M, int32_t K, int32
 
 /* ---- per-kernel timing (bench) -------------------------------------------------------- */
 
-/* Kernel classes reported by cold_profile_read. */
-enum { COLD_PROF_USER = 0, COLD_PROF_GATHER = 1, COLD_PROF_TOPK = 2, COLD_PROF_FC = 3 /* + layer */,
-       COLD_PROF_SE_DENSE = 3 + 16 /* the dense SE gate kernel */, COLD_PROF_KINDS = 3 + 16 + 1 };
+/* Kernel classes reported by cold_profile_read. Every launch is recorded under the class of the
+ * kernel that ran, so a call that mixes the chain with the layer-by-layer GEMMs (e.g. a small last
+ * chunk) never attributes one kernel's time to another's FLOPs. */
+enum { COLD_PROF_USER = 0, COLD_PROF_GATHER = 1, COLD_PROF_TOPK = 2,
+       COLD_PROF_FC = 3 /* + layer: one layer-by-layer tcgen05 GEMM (the last hidden one with the head fused) */,
+       COLD_PROF_SE_DENSE = 3 + 16 /* the dense SE gate kernel */,
+       COLD_PROF_CHAIN = 20 /* chain_kernel: FC1 -> FC2 -> FC3 in one launch */,
+       COLD_PROF_TAIL = 21 /* fused tail: FC(L-2) -> FC(L-1) -> head (tail45) or FC(L-3) .. head */,
+       COLD_PROF_MLP_F32 = 22 /* fp32 SIMT network (every layer) */,
+       COLD_PROF_KINDS = 23 };
 
 /* enable = 1: reset counters and record a CUDA event pair around every kernel the library
  * launches (on the launching stream); enable = 0: stop recording. */
 cold_status cold_profile(cold_ctx* ctx, int32_t enable);
 
 /* Synchronises the recorded events and returns, per kernel class, the summed device time
- * (ms) and launch count since the last cold_profile(ctx, 1). Arrays of COLD_PROF_KINDS. */
-cold_status cold_profile_read(cold_ctx* ctx, double* total_ms, int64_t* launches);
+ * (ms), the launch count and the ALGORITHMIC FLOPs those launches computed since the last
+ * cold_profile(ctx, 1): 2 * rows * sum(in_l * out_l) over the layers the launch covers (FC
+ * classes; the hoisted user GEMV counts 2 * D_u * H per request under COLD_PROF_USER; 0 for the
+ * other classes). Arrays of COLD_PROF_KINDS; `flop` may be NULL. */
+cold_status cold_profile_read(cold_ctx* ctx, double* total_ms, int64_t* launches, double* flop);
 
 /* ---- parity hooks (tests) ------------------------------------------------------------ */
 

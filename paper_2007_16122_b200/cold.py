@@ -29,8 +29,9 @@ EXPORTS = ["cold_create", "cold_destroy", "cold_load_params", "cold_score_batch"
            "cold_topk", "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
            "cold_status_string", "cold_last_error", "cold_profile", "cold_profile_read", "cold_se_stats",
            "cold_select_groups", "cold_merge_topk", "cold_vps_score", "cold_ctx_clone"]
-PROF_KINDS = 3 + 16 + 1
+PROF_KINDS = 23
 PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC, PROF_SE_DENSE = 0, 1, 2, 3, 3 + 16
+PROF_CHAIN, PROF_TAIL, PROF_MLP_F32 = 20, 21, 22
 
 
 class ColdError(RuntimeError):
@@ -71,7 +72,8 @@ class cold_batch(C.Structure):
 class cold_info(C.Structure):
     _fields_ = [("version", C.c_uint64), ("d_in", C.c_int32), ("d_user", C.c_int32), ("d_ad", C.c_int32),
                 ("chunk_ads", C.c_int32), ("kernels_per_chunk", C.c_int32), ("kernels_per_call", C.c_int32),
-                ("tensor_core", C.c_int32), ("device_bytes", C.c_int64), ("compressed_activations", C.c_int32)]
+                ("tensor_core", C.c_int32), ("device_bytes", C.c_int64), ("compressed_activations", C.c_int32),
+                ("gather_span_chunks", C.c_int32)]
 
 
 _lib = None
@@ -105,7 +107,7 @@ def lib() -> C.CDLL:
                                      C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.cold_ctx_clone.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
         L.cold_profile.argtypes = [C.c_void_p, C.c_int32]
-        L.cold_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.cold_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.cold_status_string.restype = C.c_char_p
         L.cold_status_string.argtypes = [C.c_int]
         L.cold_last_error.restype = C.c_char_p
@@ -286,12 +288,13 @@ class Context:
     def profile(self, enable: bool):
         _check(lib().cold_profile(self.ctx, int(enable)))
 
-    def profile_read(self):
-        """{kind: (total_ms, launches)} since profile(True)."""
+    def profile_read(self, with_flop: bool = False):
+        """(total_ms, launches[, algorithmic FLOPs]) per kernel class (PROF_*) since profile(True)."""
         ms = np.zeros(PROF_KINDS, np.float64)
         n = np.zeros(PROF_KINDS, np.int64)
-        _check(lib().cold_profile_read(self.ctx, ms.ctypes.data, n.ctypes.data))
-        return ms, n
+        fl = np.zeros(PROF_KINDS, np.float64)
+        _check(lib().cold_profile_read(self.ctx, ms.ctypes.data, n.ctypes.data, fl.ctypes.data))
+        return (ms, n, fl) if with_flop else (ms, n)
 
     def se_stats(self, batch: Batch, stream=None) -> np.ndarray:
         """Mean SE importance weight of every schema group over the batch's ads (cold_se_stats)."""

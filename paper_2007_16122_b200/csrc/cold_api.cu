@@ -220,8 +220,10 @@ struct cold_ctx {
   std::vector<cudaEvent_t> prof_events;       // pool
   size_t prof_used = 0;
   std::vector<int> prof_kind;                 // kind of each recorded pair
+  std::vector<double> prof_fl;                // algorithmic FLOPs of each recorded pair
   double prof_ms[COLD_PROF_KINDS] = {0};
   int64_t prof_n[COLD_PROF_KINDS] = {0};
+  double prof_flop[COLD_PROF_KINDS] = {0};
 
   bool owns_params = true;           // false for cold_ctx_clone contexts (parameters shared)
   cold_ctx* clone_of = nullptr;
@@ -290,6 +292,15 @@ struct cold_ctx {
     return alloc(p, bytes);
   }
   int elem() const { return precision == COLD_FP32 ? 4 : 2; }
+  // input width of layer l as the kernels see it (layer 0: the ad + cross part, or all of D_in under
+  // dense SE; the hoisted user block is counted with the user kernel)
+  int layer_k(int l) const { return l == 0 ? d_x : widths[l - 1]; }
+  // algorithmic FLOPs of layers [l0, l1) over n rows (l1 == L includes the head)
+  double layer_flop(int l0, int l1, int64_t n) const {
+    double f = 0.0;
+    for (int l = l0; l < l1; l++) f += 2.0 * (double)layer_k(l) * (double)widths[l];
+    return f * (double)n;
+  }
   // bracket one kernel launch with an event pair (only while profiling)
   void mark_begin(cudaStream_t st) {
     if (!prof) return;
@@ -300,10 +311,11 @@ struct cold_ctx {
     }
     cudaEventRecord(prof_events[prof_used], st);
   }
-  void mark_end(int kind, cudaStream_t st) {
+  void mark_end(int kind, cudaStream_t st, double flop = 0.0) {
     if (!prof) return;
     cudaEventRecord(prof_events[prof_used + 1], st);
     prof_kind.push_back(kind);
+    prof_fl.push_back(flop);
     prof_used += 2;
     if (prof_used >= 8192) flush_profile();
   }
@@ -315,8 +327,10 @@ struct cold_ctx {
       cudaEventElapsedTime(&ms, prof_events[2 * i], prof_events[2 * i + 1]);
       prof_ms[prof_kind[i]] += ms;
       prof_n[prof_kind[i]] += 1;
+      prof_flop[prof_kind[i]] += prof_fl[i];
     }
     prof_kind.clear();
+    prof_fl.clear();
     prof_used = 0;
   }
 };
@@ -968,6 +982,14 @@ static cold_status plan_batch(cold_ctx* c, const cold_batch* b, CallPlan& pl, bo
     if (is_device_ptr(b->ids[g]) == pl.host) return fail(COLD_ERR_INVALID_ARG, "a batch must be all-host or all-device");
     if (pl.host && has_offs && (!b->offs_host || !b->offs_host[g]))
       return fail(COLD_ERR_INVALID_ARG, "host batch needs offs_host for bag groups");
+    if (has_offs && b->offs_host && b->offs_host[g]) {   // CSR bag offsets: 0-based, non-decreasing
+      const int32_t* o = b->offs_host[g];
+      const int64_t len = (G.side == COLD_USER ? (int64_t)R : pl.N) + 1;
+      if (o[0] != 0) return fail(COLD_ERR_INVALID_ARG, "bag offsets must start at 0 (group " + std::to_string(g) + ")");
+      for (int64_t i = 1; i < len; i++)
+        if (o[i] < o[i - 1])
+          return fail(COLD_ERR_INVALID_ARG, "bag offsets must be non-decreasing (group " + std::to_string(g) + ")");
+    }
   }
   memset(&pl.bv, 0, sizeof(pl.bv));
   if (!pl.host) {
@@ -1176,7 +1198,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     m.scores = scores_out;
     c->mark_begin(st);
     launch_mlp_f32(m, st);
-    c->mark_end(COLD_PROF_FC, st);
+    c->mark_end(COLD_PROF_MLP_F32, st, c->layer_flop(0, c->L, n));
     return;
   }
   int n_gemm = c->L - 1 - c->n_tail;
@@ -1230,7 +1252,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     static const bool gbias = getenv("COLD_CHAIN_GBIAS") && atoi(getenv("COLD_CHAIN_GBIAS")) != 0;
     cp.gbias = gbias ? 1 : 0;
     launch_chain(tm, (int)n, c->precision == COLD_BF16 ? 1 : 0, cp, c->num_sms, c->pdl && !c->prof, st);
-    c->mark_end(COLD_PROF_FC, st);
+    c->mark_end(COLD_PROF_CHAIN, st, c->layer_flop(0, c->chain_tail ? c->L : 3, n));
     n_gemm = 0;
     if (c->chain_tail) return;   // FC4 / FC5 / head done inside the chain
   }
@@ -1281,7 +1303,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     else
       launch_gemm(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
                   c->precision == COLD_BF16 ? 1 : 0, c->cs[l], c->resb[l], ep, c->num_sms, c->pdl && !c->prof, st);
-    c->mark_end(COLD_PROF_FC + l, st);
+    c->mark_end(COLD_PROF_FC + l, st, c->layer_flop(l, head ? c->L : l + 1, n));
   }
   if (c->tail_mode == 2) {
     const int l4 = c->L - 3;
@@ -1300,7 +1322,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     c->mark_begin(st);
     launch_tail45(tmA_of(l4), &c->tmB[l4], &c->tmB[l4 + 1], (int)n, c->precision == COLD_BF16 ? 1 : 0, tp,
                   c->num_sms, c->pdl && !c->prof, st);
-    c->mark_end(COLD_PROF_FC + l4, st);
+    c->mark_end(COLD_PROF_TAIL, st, c->layer_flop(l4, c->L, n));
   }
   if (c->tail_mode == 1) {
     const int l3 = c->L - 4;
@@ -1316,7 +1338,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     c->mark_begin(st);
     launch_tail(tmA_of(l3), &c->tmB[l3], &c->tmB[l3 + 1], &c->tmB[l3 + 2], (int)n, K3,
                 c->precision == COLD_BF16 ? 1 : 0, tp, c->num_sms, c->pdl && !c->prof, st);
-    c->mark_end(COLD_PROF_FC + l3, st);
+    c->mark_end(COLD_PROF_TAIL, st, c->layer_flop(l3, c->L, n));
   }
 }
 
@@ -1339,6 +1361,7 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
   const bool scores_dev = mode == RUN_SCORE && is_device_ptr(scores);
   c->cur_adoff = d_adoff;
   UserArgs ua = make_user_args(c, pl, d_adoff, dbg);
+  const double user_flop = c->dense_se ? 0.0 : 2.0 * c->d_u * c->widths[0] * (double)pl.R;
   // Latency path (a few requests, scoring): the user side (pooling, u1 GEMV, ad -> request map) does not
   // feed the gather, which finds an ad's request by searching ad_offsets, so the two run concurrently
   // (fork onto the side stream, join before the FC stack). COLD_USER_FORK=0 serialises them.
@@ -1356,12 +1379,12 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
   if (fork && !gather_side) {
     c->mark_begin(c->side_stream);
     launch_user(ua, pl.R, c->precision, c->side_stream);
-    c->mark_end(COLD_PROF_USER, c->side_stream);
+    c->mark_end(COLD_PROF_USER, c->side_stream, user_flop);
     CK(cudaEventRecord(c->ev_user, c->side_stream));
   } else {
     c->mark_begin(st);
     launch_user(ua, pl.R, c->precision, st);
-    c->mark_end(COLD_PROF_USER, st);
+    c->mark_end(COLD_PROF_USER, st, user_flop);
     if (gather_side) gst = c->side_stream;
   }
   CK(cudaGetLastError());
@@ -1800,17 +1823,21 @@ extern "C" cold_status cold_profile(cold_ctx* c, int32_t enable) {
   CK(cudaSetDevice(c->device));
   if (enable) {
     c->flush_profile();
-    for (int i = 0; i < COLD_PROF_KINDS; i++) { c->prof_ms[i] = 0; c->prof_n[i] = 0; }
+    for (int i = 0; i < COLD_PROF_KINDS; i++) { c->prof_ms[i] = 0; c->prof_n[i] = 0; c->prof_flop[i] = 0; }
   }
   c->prof = enable != 0;
   return COLD_OK;
 }
 
-extern "C" cold_status cold_profile_read(cold_ctx* c, double* total_ms, int64_t* launches) {
+extern "C" cold_status cold_profile_read(cold_ctx* c, double* total_ms, int64_t* launches, double* flop) {
   if (!c || !total_ms || !launches) return fail(COLD_ERR_INVALID_ARG, "null");
   CK(cudaSetDevice(c->device));
   c->flush_profile();
-  for (int i = 0; i < COLD_PROF_KINDS; i++) { total_ms[i] = c->prof_ms[i]; launches[i] = c->prof_n[i]; }
+  for (int i = 0; i < COLD_PROF_KINDS; i++) {
+    total_ms[i] = c->prof_ms[i];
+    launches[i] = c->prof_n[i];
+    if (flop) flop[i] = c->prof_flop[i];
+  }
   return COLD_OK;
 }
 
@@ -1828,5 +1855,6 @@ extern "C" cold_status cold_get_info(const cold_ctx* c, cold_info* out) {
   for (int g = 0; g < c->M && g < (int)c->d_tables.size(); g++) b += c->groups[g].cardinality * c->k * c->elem();
   out->device_bytes = b;
   out->compressed_activations = c->compressed ? 1 : 0;
+  out->gather_span_chunks = c->gspan;
   return COLD_OK;
 }

@@ -1,9 +1,24 @@
 // internal.h — launchers shared between the host runtime (cold_api.cu) and the kernel files.
 #pragma once
+#include <atomic>
 #include <cuda.h>
 #include "common.cuh"
 
 namespace cold {
+
+// cudaFuncSetAttribute (dynamic shared-memory opt-in, cluster sizes) applies per device context, and a
+// process may hold contexts on several GPUs (cold_config.device): remember the opt-in per device ordinal.
+struct DevOnce {
+  std::atomic<unsigned long long> bits{0};
+  // true the first time it is called on the current device
+  bool first() {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long bit = 1ull << (d & 63);
+    return (bits.fetch_or(bit) & bit) == 0;
+  }
+};
+
 
 struct UserArgs {
   const DevGroup* groups;

@@ -339,11 +339,10 @@ cudaError_t launch_chain(const CUtensorMap* tm[12], int M, int bf16, const Chain
   if (M <= 0) return cudaSuccess;
   auto kern = bf16 ? (cp.tail ? chain_kernel<true, true> : chain_kernel<true, false>)
                    : (cp.tail ? chain_kernel<false, true> : chain_kernel<false, false>);
-  static bool attr[4] = {false, false, false, false};
+  static DevOnce attr[4];
   const int ai = (bf16 ? 2 : 0) + (cp.tail ? 1 : 0);
-  if (!attr[ai]) {
+  if (attr[ai].first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_SMEM);
-    attr[ai] = true;
   }
   const int num_pm = (M + 2 * BM - 1) / (2 * BM);
   const int pairs = num_pm < num_sms / 2 ? num_pm : num_sms / 2;

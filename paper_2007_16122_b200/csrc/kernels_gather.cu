@@ -656,10 +656,9 @@ static void user_dispatch(const UserArgs& a, int R, cudaStream_t s) {
     case 8: user_kernel<T, 8><<<grid, 256, smem, s>>>(a); break;
     case 16: user_kernel<T, 16><<<grid, 256, smem, s>>>(a); break;
     case 32: {
-      static bool attr = false;
-      if (!attr) {   // 8 warps x 32 rows x 32 floats = 32 KB of staging + x_u
+      static DevOnce attr;
+      if (attr.first()) {   // 8 warps x 32 rows x 32 floats = 32 KB of staging + x_u
         cudaFuncSetAttribute(user_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        attr = true;
       }
       user_kernel<T, 32><<<grid, 256, smem, s>>>(a);
       break;

@@ -382,12 +382,11 @@ template <int BN, bool BF16, int CS, bool RESB>
 static cudaError_t launch_t(const CUtensorMap* tmA, const CUtensorMap* tmB, const CUtensorMap* tmC, int M, int N,
                             int K, const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s) {
   using Cfg = GemmCfg<BN, RESB>;
-  static bool attr = false;
+  static DevOnce attr;
   auto kern = gemm_kernel<BN, BF16, CS, RESB>;
-  if (!attr) {
+  if (attr.first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (CS > 1) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    attr = true;
   }
   const int num_m = (M + BM - 1) / BM;
   const int num_n = N / BN;
@@ -399,7 +398,10 @@ static cudaError_t launch_t(const CUtensorMap* tmA, const CUtensorMap* tmB, cons
     grid = groups * num_n;
   } else {
     const int items = ((num_m + CS - 1) / CS) * num_n;
-    static int max_clusters = 0;
+    static int max_clusters_dev[64] = {0};   // per device ordinal (occupancy is a per-device property)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& max_clusters = max_clusters_dev[dev & 63];
     if (max_clusters == 0) {
       max_clusters = num_sms / CS;
       if (CS > 1) {

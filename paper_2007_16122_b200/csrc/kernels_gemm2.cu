@@ -372,10 +372,9 @@ static cudaError_t launch_pair_t(const CUtensorMap* tmA, const CUtensorMap* tmB,
                                  const EpiParams& ep, int num_sms, bool pdl, cudaStream_t s) {
   using Cfg = PairCfg<BN, U1, RES>;
   auto kern = gemm_pair_kernel<BN, BF16, U1, RES>;
-  static bool attr = false;
-  if (!attr) {
+  static DevOnce attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    attr = true;
   }
   const int num_pm = (M + 2 * BM - 1) / (2 * BM), num_n = N / BN;
   const int items = num_pm * num_n;

@@ -101,10 +101,9 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_f32_kernel(MlpF32Args a) {
 void launch_mlp_f32(const MlpF32Args& a, cudaStream_t s) {
   if (a.n <= 0) return;
   size_t smem = 2 * (size_t)MLP_TILE * a.max_w * sizeof(float);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DevOnce attr_set;
+  if (attr_set.first()) {
     cudaFuncSetAttribute(mlp_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_set = true;
   }
   mlp_f32_kernel<<<(unsigned)((a.n + MLP_TILE - 1) / MLP_TILE), MLP_THREADS, smem, s>>>(a);
 }

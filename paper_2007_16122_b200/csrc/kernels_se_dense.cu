@@ -147,10 +147,12 @@ __global__ void __launch_bounds__(128) se_dense_kernel(SeDenseArgs a) {
 template <typename T, int K, int JB, bool V4>
 static void se_dense_launch(const SeDenseArgs& a, cudaStream_t s) {
   const size_t smem = se_dense_smem(a.d_in, a.n_sel);
-  static size_t attr = 0;   // opt in (static + dynamic > 48 KB needs it)
-  if (smem > attr) {
+  static std::atomic<size_t> attr[64];   // opt in per device (static + dynamic > 48 KB needs it)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (smem > attr[dev & 63].load()) {
     cudaFuncSetAttribute(se_dense_kernel<T, K, JB, V4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
+    attr[dev & 63].store(smem);
   }
   se_dense_kernel<T, K, JB, V4><<<(unsigned)((a.n + 127) / 128), 128, smem, s>>>(a);
 }

@@ -276,10 +276,9 @@ cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const 
                         cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   auto kern = bf16 ? tail_kernel<true> : tail_kernel<false>;
-  static bool attr[2] = {false, false};
-  if (!attr[bf16 ? 1 : 0]) {
+  static DevOnce attr[2];
+  if (attr[bf16 ? 1 : 0].first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T_SMEM);
-    attr[bf16 ? 1 : 0] = true;
   }
   const int tiles = (M + BM - 1) / BM;
   cudaLaunchConfig_t cfg = {};

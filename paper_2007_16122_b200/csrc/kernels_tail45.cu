@@ -238,10 +238,9 @@ cudaError_t launch_tail45(const CUtensorMap* tmA4, const CUtensorMap* tmB4, cons
                           const TailParams& tp, int num_sms, bool pdl, cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
   auto kern = bf16 ? tail45_kernel<true> : tail45_kernel<false>;
-  static bool attr[2] = {false, false};
-  if (!attr[bf16 ? 1 : 0]) {
+  static DevOnce attr[2];
+  if (attr[bf16 ? 1 : 0].first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM);
-    attr[bf16 ? 1 : 0] = true;
   }
   const int tiles = (M + BM - 1) / BM;
   cudaLaunchConfig_t cfg = {};

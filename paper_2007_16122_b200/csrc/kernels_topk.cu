@@ -177,11 +177,10 @@ void launch_topk(const TopkArgs& a0, cudaStream_t s) {
   while (P < a.K) P <<= 1;
   a.stage = (a.max_n > 0 && a.max_n <= TOPK_STAGE) ? a.max_n : 0;
   const size_t smem = (size_t)P * sizeof(unsigned long long) + (size_t)a.stage * sizeof(uint32_t);
-  static bool attr = false;
-  if (!attr) {
+  static DevOnce attr;
+  if (attr.first()) {
     cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          TOPK_MAX_K * (int)sizeof(unsigned long long) + TOPK_STAGE * (int)sizeof(uint32_t));
-    attr = true;
   }
   topk_kernel<<<a.R, TOPK_THREADS, smem, s>>>(a);
 }

@@ -29,7 +29,10 @@ def split_even(total: int, world: int, rank: int) -> range:
 def gather_topk(idx: torch.Tensor, key: torch.Tensor, out_idx: torch.Tensor = None,
                 out_key: torch.Tensor = None) -> Tuple[torch.Tensor, torch.Tensor]:
     """All-gather equal-sized per-rank top-K blocks: returns [world * R_local * K] idx / key in rank
-    order (the global request order under `request_block`)."""
+    order (the global request order under `request_block` / `split_even`; ranks with fewer requests
+    pad their blocks, see `unpad_gathered`). NCCL gathers the device tensors in place over
+    NVLink; gloo (the CPU tests, and the one-GPU multi-process test) stages device tensors through
+    host memory around the same all_gather_into_tensor call."""
     world = dist.get_world_size()
     if out_idx is None:
         out_idx = torch.empty(world * idx.numel(), dtype=idx.dtype, device=idx.device)
@@ -38,9 +41,22 @@ def gather_topk(idx: torch.Tensor, key: torch.Tensor, out_idx: torch.Tensor = No
         dist.all_gather_into_tensor(out_idx, idx)
         dist.all_gather_into_tensor(out_key, key)
     else:
-        dist.all_gather(list(out_idx.chunk(world)), idx)
-        dist.all_gather(list(out_key.chunk(world)), key)
+        hi, hk = idx.cpu(), key.cpu()
+        gi = torch.empty(world * hi.numel(), dtype=hi.dtype)
+        gk = torch.empty(world * hk.numel(), dtype=hk.dtype)
+        dist.all_gather_into_tensor(gi, hi)
+        dist.all_gather_into_tensor(gk, hk)
+        out_idx.copy_(gi)
+        out_key.copy_(gk)
     return out_idx, out_key
+
+
+def unpad_gathered(g: "np.ndarray", counts, r_pad: int, K: int):
+    """[world * r_pad * K] gathered blocks -> [sum(counts), K]: the first counts[r] requests of
+    rank r's block, in rank order."""
+    import numpy as np
+    g = np.asarray(g).reshape(len(counts), r_pad, K)
+    return np.concatenate([g[r, :c] for r, c in enumerate(counts)], axis=0)
 
 
 def ad_slice(n: int, world: int, rank: int) -> range:

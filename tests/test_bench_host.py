@@ -50,3 +50,32 @@ def test_usable_rate_more_servers_more_rate():
     r1 = bench.usable_rate(s, 1.0)
     r4 = bench.usable_rate(s, 1.0, servers=4)
     assert r1 < r4 < 4 * 1e4
+
+
+def test_kernel_classes_attribute_mixed_chain_and_gemm_steps():
+    """A step whose big chunks ran the chain and whose last chunk ran the layer-by-layer GEMMs: every
+    class gets its own launches' time and FLOPs (counted by the library from the rows each launch
+    covered), so no class can read above the peak because another kernel's work landed on it."""
+    from paper_2007_16122_b200.cold import PROF_CHAIN, PROF_FC, PROF_KINDS, PROF_TAIL
+    sch = coldgen.schema_paper()
+    ms = np.zeros(PROF_KINDS)
+    n = np.zeros(PROF_KINDS, np.int64)
+    fl = np.zeros(PROF_KINDS)
+    f123 = 2 * (256 * 1024 + 1024 * 512 + 512 * 256)
+    ms[PROF_CHAIN], n[PROF_CHAIN], fl[PROF_CHAIN] = 10 * 0.27, 10, 10 * 151552 * f123
+    ms[PROF_FC], n[PROF_FC], fl[PROF_FC] = 0.01, 1, 2 * 256 * 1024 * 4000          # fc1 GEMM, 4000 rows
+    ms[PROF_FC + 1], n[PROF_FC + 1], fl[PROF_FC + 1] = 0.012, 1, 2 * 1024 * 512 * 4000
+    ms[PROF_TAIL], n[PROF_TAIL], fl[PROF_TAIL] = 11 * 0.024, 11, 2 * (256 * 128 + 128 * 64 + 64 * 2) * (10 * 151552 + 4000)
+    cls = bench.kernel_classes(sch, ms, n, fl)
+    assert set(cls) == {"chain (fc1+fc2+fc3)", "gemm fc1", "gemm fc2", "tail (fc4+fc5+head)"}
+    assert abs(cls["chain (fc1+fc2+fc3)"]["tflops"] - 151552 * f123 / 0.27e-3 / 1e12) < 1e-6
+    assert abs(cls["gemm fc1"]["tflops"] - 2 * 256 * 1024 * 4000 / 0.01e-3 / 1e12) < 1e-6
+    peaks = {"bf16_tflops": 1627.7, "bf16_tflops_sustained": 1362.4, "clocks_under_load": {"sm_mhz_median": 1237.0}}
+    r = bench.fc_roofline(cls, peaks, "measured", {"sm_mhz": 1665.0}, {})
+    assert r["kernel"] == "chain (fc1+fc2+fc3)" and r["peak"] == 1627.7
+    assert abs(r["frac"] - r["achieved"] / 1627.7) < 1e-12 and abs(r["frac_sustained"] - r["achieved"] / 1362.4) < 1e-12
+    assert abs(r["frac_sustained_at_run_clock"] - r["achieved"] / (1362.4 * 1665 / 1237)) < 1e-12
+    assert "suspect" not in r
+    ms[PROF_CHAIN] = 0.001                                                            # impossible rate: flagged
+    r = bench.fc_roofline(bench.kernel_classes(sch, ms, n, fl), peaks, "measured", None, {})
+    assert "suspect" in r

@@ -332,6 +332,30 @@ def test_ll_order_variants_agree_when_gate_is_one():
     np.testing.assert_allclose(a, b, rtol=1e-15)
 
 
+def test_ll_order_variants_closed_form_with_constant_gate():
+    """AMB-3 ("put a linear_log operator in the first layer"; P:229-235 SE): with w_g = 0 the gate
+    is the constant s_g = sigma(b_g) != 1, so the two orders have closed forms over the raw pooled sums e
+    (LL off, gate 1): default (LL before SE) x = s_g * LL(e); ll_after_se x = LL(s_g * e). LL is pinned
+    by its own closed forms (P-1). A swapped order, or LL applied twice / not at all, fails one side."""
+    sch, p_id, batch = small_case("paper", R=2, n_ads=(7, 4), se="identity", cap=2000)
+    raw = oracle.features(oracle.Model(sch, p_id, linear_log=False), batch)   # x = e (s = 1 exactly)
+    assert np.abs(raw).max() > 1.5 and np.abs(raw).min() < 1.0   # both LL branches are hit
+    b = np.linspace(-2.0, 1.5, sch.M)
+    s = np.array([oracle.sigmoid(x) for x in b])
+    assert np.all(np.abs(s - 1.0) > 0.1)
+    params = coldgen.Params(tables=p_id.tables, table_dtype=p_id.table_dtype, se_w=np.zeros_like(p_id.se_w),
+                            se_b=b, fc_w=p_id.fc_w, fc_b=p_id.fc_b, precision=p_id.precision, init=p_id.init,
+                            seed=p_id.seed)
+    k = sch.k
+    scol = np.repeat(s, k)[None, :]
+    ll = np.vectorize(oracle.linear_log)
+    default = oracle.features(oracle.Model(sch, params), batch)
+    after = oracle.features(oracle.Model(sch, params, ll_after_se=True), batch)
+    np.testing.assert_allclose(default, scol * ll(raw), rtol=1e-14, atol=1e-300)
+    np.testing.assert_allclose(after, ll(scol * raw), rtol=1e-14, atol=1e-300)
+    assert np.abs(default - after).max() > 1e-3                               # the orders really differ
+
+
 def test_pooled_f32_mode():
     """fp32-ordered gather: single ids are exact copies; pooled sums equal a sequential
     float32 sum over the twin's rows in bag order."""
