@@ -433,7 +433,8 @@ def test_split_request_merge_topk_equals_unsplit(G):
         np.testing.assert_array_equal(got_idx, full_idx)
         np.testing.assert_array_equal(got_key, full_key)
         # and the oracle's brute-force sort of the same keys (P-10; ties by position, AMB-13)
-        oidx, okey = oracle.topk_batch(keys.astype(np.float64), ao, K)
+        # (the GPU ranks the fp32 keys it was given)
+        oidx, okey = oracle.topk_batch(np.asarray(keys, np.float32).astype(np.float64), ao, K)
         np.testing.assert_array_equal(got_idx, oidx)
         np.testing.assert_array_equal(got_key.astype(np.float64), okey)
     # NaN keys rank last and ties resolve by position in the merge too

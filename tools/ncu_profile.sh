@@ -7,8 +7,8 @@ TAG=${1:-r02}
 shift
 KERNELS=${@:-gather chain tail45}
 OUT=gpurun_out
-# 32 requests x 9472 ads = 2 full 151552-ad chunks per step (one gather span)
-ARGS=${NCU_ARGS:-"--requests 32 --ads 9472 --steps 2 --warmup 1 --no-e2e --no-latency --no-cpu"}
+# 256 requests x 9472 ads = 16 full 151552-ad chunks per step (one 16-chunk gather span)
+ARGS=${NCU_ARGS:-"--requests 256 --ads 9472 --steps 2 --warmup 1 --no-e2e --no-latency --no-cpu"}
 python -m paper_2007_16122_b200.build >/dev/null
 # 1. launch list (cold-cache, serialised: compare shares)
 timeout 400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv \
@@ -30,6 +30,6 @@ for k in $KERNELS; do
 done
 for f in $OUT/prof_*_$TAG.ncu-rep; do python tools/ncu_summary.py $f; done > $OUT/ncu_summary_$TAG.txt 2>&1
 python tools/ncu_traffic.py --commit "${GIT_SHA:-unknown}" --source "ncu --set full, bench.py $ARGS, tag $TAG" \
-  --ads chain=151552 --ads tail=151552 --ads gather=303104 \
+  --ads chain=151552 --ads tail=151552 --ads gather=2424832 \
   --flop-per-ad chain=1835008 --flop-per-ad tail=82176 --out $OUT/ncu_traffic_$TAG.json $REPS > /dev/null 2>&1
 ls -la $OUT

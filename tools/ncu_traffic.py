@@ -14,8 +14,13 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import summary  # noqa: E402
 
 
+UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
 def num(v):
-    return float(str(v).split()[0].replace(",", ""))
+    parts = str(v).split()
+    x = float(parts[0].replace(",", ""))
+    return x * UNIT.get(parts[1], 1.0) if len(parts) > 1 else x
 
 
 def main():
@@ -34,7 +39,7 @@ def main():
         name, rep = item.split("=", 1)
         d = summary(rep)[0]
         rd, wr = num(d["dram__bytes_read.sum"]), num(d["dram__bytes_write.sum"])
-        k = {"kernel_name": d.get("Kernel Name", "").split()[0], "dram_read_bytes": rd, "dram_write_bytes": wr,
+        k = {"kernel_name": d.get("Kernel Name", "").replace("void ", "").split("(")[0], "dram_read_bytes": rd, "dram_write_bytes": wr,
              "dram_bytes_per_launch": rd + wr, "duration": d.get("gpu__time_duration.sum"),
              "tensor_active_pct": num(d.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "0")),
              "dram_throughput_pct": num(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "0")),
