@@ -279,6 +279,12 @@ def make_params(schema: Schema, seed: int = 1234, precision: str = "f16",
     return Params(tables, table_dtype, se_w, se_b, fc_w, fc_b, precision, init, seed)
 
 
+def prelu_slopes(schema: Schema, seed: int = 1234, lo: float = 0.05, hi: float = 0.3) -> list:
+    """Seeded per-channel PReLU slopes for the hidden layers (the F2 activation variant): [L-1] float32
+    arrays of the hidden widths, uniform in [lo, hi)."""
+    return [_rng(seed, 404, l).uniform(lo, hi, w).astype(np.float32) for l, w in enumerate(schema.widths[:-1])]
+
+
 # --------------------------------------------------------------------------------------
 # requests
 

@@ -52,7 +52,8 @@ class _Model(C.Structure):
                 ("linear_log", C.c_int32), ("ll_after_se", C.c_int32),
                 ("L", C.c_int32), ("widths", C.POINTER(C.c_int32)),
                 ("W", C.POINTER(C.POINTER(C.c_double))), ("b", C.POINTER(C.POINTER(C.c_double))),
-                ("in_scale", C.POINTER(C.c_double)), ("in_shift", C.POINTER(C.c_double))]
+                ("in_scale", C.POINTER(C.c_double)), ("in_shift", C.POINTER(C.c_double)),
+                ("activation", C.c_int32), ("slope", C.POINTER(C.POINTER(C.c_double)))]
 
 
 class _Batch(C.Structure):
@@ -112,7 +113,8 @@ class Model:
 
     def __init__(self, schema: coldgen.Schema, params: coldgen.Params, selected: Optional[Sequence[int]] = None,
                  linear_log: Optional[bool] = None, ll_after_se: bool = False,
-                 se_dense: Optional[tuple] = None, in_norm: Optional[tuple] = None):
+                 se_dense: Optional[tuple] = None, in_norm: Optional[tuple] = None,
+                 prelu: Optional[Sequence] = None):
         self.schema, self.params = schema, params
         sel = list(range(schema.M)) if selected is None else sorted(selected)
         self._keep = []
@@ -147,6 +149,14 @@ class Model:
             self.isc = np.ascontiguousarray(in_norm[0], np.float64)
             self.ish = np.ascontiguousarray(in_norm[1], np.float64)
             m.in_scale, m.in_shift = _ptr(self.isc, C.c_double), _ptr(self.ish, C.c_double)
+        if prelu is not None:     # PReLU slopes [L-1] each [out_l]
+            assert len(prelu) == len(self.W) - 1
+            self.slopes = [np.ascontiguousarray(a, np.float64) for a in prelu]
+            for a, w in zip(self.slopes, self.W):
+                assert a.shape == (w.shape[0],)
+            sp = (C.POINTER(C.c_double) * len(self.slopes))(*[_ptr(a, C.c_double) for a in self.slopes])
+            self._sp = sp
+            m.activation, m.slope = 1, C.cast(sp, C.POINTER(C.POINTER(C.c_double)))
         self.m = m
 
 

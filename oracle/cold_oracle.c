@@ -198,7 +198,9 @@ static int max_width(const orc_model* m) {
   return w;
 }
 
-/* FC stack P:328: h_l = ReLU(W_l h_{l-1} + b_l) (AMB-6), last layer linear;
+/* FC stack P:328: h_l = act(W_l h_{l-1} + b_l), last layer linear. act = ReLU (AMB-6: the paper never
+ * names the activation), or PReLU with a per-channel slope a_j (act(x) = x for x > 0, a_j x otherwise;
+ * the model variant of SURVEY §8(f) F2);
  * score P:163 / AMB-7: p = sigma(z1 - z0) for a 2-wide head, sigma(z) for 1-wide. */
 static void fcn(const orc_model* m, const double* x, double* buf0, double* buf1, double* p, double* zo) {
   int in = m->n_sel * m->k;
@@ -210,7 +212,9 @@ static void fcn(const orc_model* m, const double* x, double* buf0, double* buf1,
     for (int j = 0; j < o; j++) {
       double acc = m->b[l][j];
       for (int i = 0; i < in; i++) acc += W[(size_t)j * in + i] * h[i];
-      out[j] = (l < m->L - 1) ? (acc > 0.0 ? acc : 0.0) : acc;
+      if (l == m->L - 1) out[j] = acc;
+      else if (m->activation == 1) out[j] = acc > 0.0 ? acc : m->slope[l][j] * acc;
+      else out[j] = acc > 0.0 ? acc : 0.0;
     }
     h = out;
     out = (out == buf0) ? buf1 : buf0;

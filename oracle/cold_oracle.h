@@ -52,6 +52,8 @@ typedef struct {
   const double* const* b;       /* [L] each [out] */
   const double* in_scale;       /* [n_sel * k] or NULL: input batch norm folded to x_j * in_scale[j] +  */
   const double* in_shift;       /* in_shift[j] (P:276's alternative to linear_log)  */
+  int32_t activation;           /* hidden activation: 0 ReLU (AMB-6), 1 PReLU */
+  const double* const* slope;   /* PReLU: [L-1] each [out_l], h = x if x > 0 else slope * x */
 } orc_model;
 
 typedef struct {

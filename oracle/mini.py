@@ -76,8 +76,9 @@ def rows(schema, batch, g, r, a):
     return [cross_row(g, x, y, grp.card) for x in xs for y in ys]
 
 
-def score_ad(schema, params, batch, r, a, selected=None, linear_log_on=None):
-    """p and z for ad a (global index) of request r; every step written out."""
+def score_ad(schema, params, batch, r, a, selected=None, linear_log_on=None, prelu=None):
+    """p and z for ad a (global index) of request r; every step written out. prelu: per-layer slope
+    lists (PReLU hidden activation, x if x > 0 else slope x), else ReLU."""
     sel = list(range(schema.M)) if selected is None else sorted(selected)
     ll = schema.linear_log if linear_log_on is None else linear_log_on
     k = schema.k
@@ -100,17 +101,22 @@ def score_ad(schema, params, batch, r, a, selected=None, linear_log_on=None):
             acc = float(b[j])
             for i in range(len(h)):
                 acc += float(W[j][i]) * h[i]
-            out.append(max(acc, 0.0) if l < L - 1 else acc)
+            if l == L - 1:
+                out.append(acc)
+            elif prelu is not None:
+                out.append(acc if acc > 0.0 else float(prelu[l][j]) * acc)
+            else:
+                out.append(max(acc, 0.0))
         h = out
     z = h[1] - h[0] if len(h) == 2 else h[0]
     return sigmoid(z), z
 
 
-def score(schema, params, batch, selected=None, linear_log_on=None):
+def score(schema, params, batch, selected=None, linear_log_on=None, prelu=None):
     ps, zs = [], []
     for r in range(batch.R):
         for a in range(int(batch.ad_offsets[r]), int(batch.ad_offsets[r + 1])):
-            p, z = score_ad(schema, params, batch, r, a, selected, linear_log_on)
+            p, z = score_ad(schema, params, batch, r, a, selected, linear_log_on, prelu)
             ps.append(p)
             zs.append(z)
     return ps, zs

@@ -448,3 +448,68 @@ def test_input_norm_folds_into_fc1():
     p_id, _ = oracle.score(oracle.Model(sch, params, in_norm=(np.ones(d), np.zeros(d))), batch)
     p_none, _ = oracle.score(oracle.Model(sch, params), batch)
     np.testing.assert_array_equal(p_id, p_none)
+
+
+# ---- F2 PReLU hidden activation (the paper never names the activation, AMB-6) ----
+
+def _prelu_torch_reference(sch, params, batch, slopes):
+    """LL off, SE pinned to s = 1: MLP(concat(embedding_bag_sum)) with torch's F.prelu between layers."""
+    import torch
+    import torch.nn.functional as F
+    feats = []
+    for g, grp in enumerate(sch.groups):
+        bags = []
+        for r in range(batch.R):
+            for a in range(batch.ad_offsets[r], batch.ad_offsets[r + 1]):
+                bags.append(mini.rows(sch, batch, g, r, a))
+        flat = torch.tensor([x for b in bags for x in b], dtype=torch.long)
+        offs = torch.tensor(np.cumsum([0] + [len(b) for b in bags[:-1]]), dtype=torch.long)
+        feats.append(F.embedding_bag(flat, torch.tensor(params.table_f64(g)), offs, mode="sum"))
+    h = torch.cat(feats, 1)
+    L = len(params.fc_w)
+    for l in range(L):
+        h = F.linear(h, torch.tensor(params.fc_w[l], dtype=torch.float64), torch.tensor(params.fc_b[l], dtype=torch.float64))
+        if l < L - 1:
+            h = F.prelu(h, torch.tensor(np.asarray(slopes[l], np.float64)))
+    return (h[:, 0] if h.shape[1] == 1 else h[:, 1] - h[:, 0]).numpy()
+
+
+def test_prelu_reduces_to_torch_prelu_mlp():
+    """P-6 style reduction with the PReLU variant: the oracle equals torch's embedding_bag + linear +
+    F.prelu (per-channel slopes) + sigmoid; a slope applied to the wrong channel or layer fails it."""
+    pytest.importorskip("torch")
+    sch, params, batch = small_case("tiny", R=3, n_ads=(6, 11, 2), precision="f32", se="identity")
+    slopes = coldgen.prelu_slopes(sch, seed=9)
+    p, z = oracle.score(oracle.Model(sch, params, linear_log=False, prelu=slopes), batch)
+    zt = _prelu_torch_reference(sch, params, batch, slopes)
+    np.testing.assert_allclose(z, zt, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(p, 1.0 / (1.0 + np.exp(-zt)), rtol=1e-12, atol=1e-14)
+    p_relu, _ = oracle.score(oracle.Model(sch, params, linear_log=False), batch)
+    assert np.abs(p - p_relu).max() > 1e-4                       # the negative branch is exercised
+
+
+def test_prelu_special_slopes():
+    """Slope 0 is ReLU exactly; slope 1 makes every hidden layer the identity, so the network is the
+    affine map z = W_L (... (W_1 x + b_1) ...) + b_L of the (separately pinned) features x."""
+    sch, params, batch = small_case("paper", R=2, n_ads=(5, 3), precision="f32", cap=2000, seed=13)
+    m_relu = oracle.Model(sch, params)
+    p_relu, z_relu = oracle.score(m_relu, batch)
+    zeros = [np.zeros(w.shape[0]) for w in params.fc_w[:-1]]
+    p0, z0 = oracle.score(oracle.Model(sch, params, prelu=zeros), batch)
+    np.testing.assert_array_equal(z0, z_relu)
+    ones = [np.ones(w.shape[0]) for w in params.fc_w[:-1]]
+    _, z1 = oracle.score(oracle.Model(sch, params, prelu=ones), batch)
+    h = oracle.features(m_relu, batch).T
+    for W, b in zip(params.fc_w, params.fc_b):
+        h = W.astype(np.float64) @ h + b.astype(np.float64)[:, None]
+    za = h[1] - h[0] if h.shape[0] == 2 else h[0]
+    np.testing.assert_allclose(z1, za, rtol=1e-10, atol=1e-12)
+
+
+def test_prelu_c_oracle_matches_python_twin():
+    sch, params, batch = small_case("tiny", R=2, n_ads=(7, 5), seed=17)
+    slopes = coldgen.prelu_slopes(sch, seed=18)
+    p, z = oracle.score(oracle.Model(sch, params, prelu=slopes), batch)
+    pm, zm = mini.score(sch, params, batch, prelu=slopes)
+    np.testing.assert_allclose(p, pm, rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(z, zm, rtol=1e-13, atol=1e-14)
