@@ -63,7 +63,9 @@ typedef enum {
 
 enum { COLD_USER = 0, COLD_AD = 1, COLD_CROSS = 2 };          /* feature-group side */
 enum { COLD_FP32 = 0, COLD_FP16 = 1, COLD_BF16 = 2 };         /* compute / storage precision */
-enum { COLD_RELU = 0 };                                        /* hidden activation (AMB-6) */
+/* hidden activation: ReLU (AMB-6: the paper never names it), or PReLU with a learned slope per channel,
+ * h = x for x > 0 and a_c x otherwise (the model-variant row SURVEY §8(f) F2; cold_params.act_slope) */
+enum { COLD_RELU = 0, COLD_PRELU = 1 };
 
 /* config.flags */
 #define COLD_VALIDATE_IDS 1u   /* check every id against its cardinality (one D2H sync per call);
@@ -92,7 +94,9 @@ typedef struct {
   const int32_t* widths;         /* [L] FC output widths; input of layer 0 = D_in = k * #selected;
                                     last width in {1, 2}. Tensor-core path (FP16/BF16): L >= 2,
                                     hidden widths multiples of 64, last hidden width <= 256. */
-  int32_t activation;            /* COLD_RELU */
+  int32_t activation;            /* COLD_RELU or COLD_PRELU (slopes in cold_params.act_slope); every kernel
+                                    path applies either (with PReLU, widths that would use the 3-layer
+                                    fused tail run those layers as GEMMs instead) */
   int32_t linear_log;            /* 1 = apply linear_log to every pooled group embedding */
   int32_t precision;             /* COLD_FP32 (SIMT FFMA, no TF32), COLD_FP16, COLD_BF16 (tcgen05) */
   int32_t device;                /* CUDA device ordinal */
@@ -137,6 +141,9 @@ typedef struct {
    * schema order; fp32, kept fp32 on the device (the gate is computed with fp32 FFMA). */
   const float* se_w_dense;       /* [n_sel x D_in] */
   const float* se_b_dense;       /* [n_sel] */
+  /* activation == COLD_PRELU only (NULL otherwise): [L-1] each [out_l], the per-channel slopes of the
+   * hidden layers, kept fp32 (COLD_ERR_PARAMS when missing). */
+  const float* const* act_slope;
 } cold_params;
 
 /* One call's requests. Column-major per group ("column based computation"). */

@@ -60,7 +60,8 @@ class cold_params(C.Structure):
                 ("se_w", C.c_void_p), ("se_b", C.c_void_p),
                 ("fc_w", C.POINTER(C.c_void_p)), ("fc_b", C.POINTER(C.c_void_p)),
                 ("in_scale", C.c_void_p), ("in_shift", C.c_void_p),
-                ("se_w_dense", C.c_void_p), ("se_b_dense", C.c_void_p)]
+                ("se_w_dense", C.c_void_p), ("se_b_dense", C.c_void_p),
+                ("act_slope", C.POINTER(C.c_void_p))]
 
 
 class cold_batch(C.Structure):
@@ -188,7 +189,7 @@ class Context:
     def __init__(self, groups, emb_dim: int, widths: Sequence[int], precision: str = "f16",
                  selected: Optional[Sequence[int]] = None, linear_log: bool = True, device: int = 0,
                  max_ads: int = 1 << 20, max_requests: int = 1024, chunk_ads: int = 0, validate_ids: bool = False,
-                 se_mode: str = "group"):
+                 se_mode: str = "group", activation: str = "relu"):
         L = lib()
         M = len(groups)
         self._groups = (cold_group * M)()
@@ -202,7 +203,7 @@ class Context:
         cfg.num_selected = len(self._sel)
         cfg.selected = self._sel.ctypes.data_as(C.POINTER(C.c_int32)) if len(self._sel) else None
         cfg.num_layers, cfg.widths = len(self._widths), self._widths.ctypes.data_as(C.POINTER(C.c_int32))
-        cfg.activation, cfg.linear_log = 0, int(linear_log)
+        cfg.activation, cfg.linear_log = {"relu": 0, "prelu": 1}[activation], int(linear_log)
         cfg.precision, cfg.device = PRECISION[precision], device
         cfg.max_ads_per_call, cfg.max_requests_per_call = max_ads, max_requests
         cfg.chunk_ads, cfg.flags = chunk_ads, VALIDATE_IDS if validate_ids else 0
@@ -234,11 +235,11 @@ class Context:
             pass
 
     def load_params(self, tables, se_w, se_b, fc_w, fc_b, table_dtype: str = "f32", in_scale=None,
-                    in_shift=None, se_dense=None) -> int:
+                    in_shift=None, se_dense=None, act_slope=None) -> int:
         """Host arrays: tables[g] [card, k] (float32, or uint16/float16 bit patterns in the compute
         precision), se_w [M, k], se_b [M], fc_w[l] [out, in], fc_b[l] [out] (float32); optional folded
         input batch norm in_scale / in_shift [D_in] (float32); se_dense = (W [n_sel, D_in], b [n_sel])
-        for a se_mode="dense" context."""
+        for a se_mode="dense" context; act_slope [L-1] each [out_l] (float32) for activation="prelu"."""
         keep = [np.ascontiguousarray(t) for t in tables]
         sw = np.ascontiguousarray(se_w, np.float32)
         sb = np.ascontiguousarray(se_b, np.float32)
@@ -253,10 +254,15 @@ class Context:
         if se_dense is not None:
             sdw = np.ascontiguousarray(se_dense[0], np.float32)
             sdb = np.ascontiguousarray(se_dense[1], np.float32)
+        sl, slp = None, None
+        if act_slope is not None:
+            sl = [np.ascontiguousarray(a, np.float32) for a in act_slope]
+            slp = (C.c_void_p * len(sl))(*[a.ctypes.data for a in sl])
         p = cold_params(PRECISION[table_dtype], C.cast(tp, C.POINTER(C.c_void_p)), sw.ctypes.data, sb.ctypes.data,
                         C.cast(wp, C.POINTER(C.c_void_p)), C.cast(bp, C.POINTER(C.c_void_p)),
                         None if isc is None else isc.ctypes.data, None if ish is None else ish.ctypes.data,
-                        None if sdw is None else sdw.ctypes.data, None if sdb is None else sdb.ctypes.data)
+                        None if sdw is None else sdw.ctypes.data, None if sdb is None else sdb.ctypes.data,
+                        None if slp is None else C.cast(slp, C.POINTER(C.c_void_p)))
         v = C.c_uint64()
         _check(lib().cold_load_params(self.ctx, C.byref(p), C.byref(v)))
         return v.value

@@ -163,6 +163,8 @@ struct cold_ctx {
   float* d_in_shift = nullptr;
   float* d_sewd_t = nullptr;         // dense SE: Wd^T [D_in][n_sel] fp32
   float* d_sebd = nullptr;           // dense SE: bd [n_sel]
+  bool prelu = false;                // COLD_PRELU hidden activation (F2)
+  float* d_slope[COLD_MAX_LAYERS] = {nullptr};   // PReLU slopes of hidden layer l [out_l] fp32
   CUtensorMap tmB[COLD_MAX_LAYERS];
   // ---- workspace ----
   float* d_u1 = nullptr;
@@ -267,7 +269,8 @@ struct cold_ctx {
       if (d_w[l]) cudaFree(d_w[l]);
       if (d_b[l]) cudaFree(d_b[l]);
       if (d_wt[l]) cudaFree(d_wt[l]);
-      d_w[l] = nullptr; d_b[l] = nullptr; d_wt[l] = nullptr;
+      if (d_slope[l]) cudaFree(d_slope[l]);
+      d_w[l] = nullptr; d_b[l] = nullptr; d_wt[l] = nullptr; d_slope[l] = nullptr;
     }
   }
   cudaError_t alloc(void** p, size_t bytes) {
@@ -416,7 +419,8 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   if (cfg->num_layers < 1 || cfg->num_layers > COLD_MAX_LAYERS || !cfg->widths)
     return fail(COLD_ERR_SHAPE, "num_layers must be in [1, 16]");
   if (cfg->precision < COLD_FP32 || cfg->precision > COLD_BF16) return fail(COLD_ERR_INVALID_ARG, "bad precision");
-  if (cfg->activation != COLD_RELU) return fail(COLD_ERR_UNSUPPORTED, "only ReLU");
+  if (cfg->activation != COLD_RELU && cfg->activation != COLD_PRELU)
+    return fail(COLD_ERR_UNSUPPORTED, "activation must be COLD_RELU or COLD_PRELU");
   if (cfg->max_ads_per_call < 1 || cfg->max_requests_per_call < 1)
     return fail(COLD_ERR_INVALID_ARG, "capacities must be >= 1");
   for (int l = 0; l < cfg->num_layers; l++)
@@ -440,6 +444,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   c->precision = cfg->precision;
   c->device = cfg->device;
   c->linear_log = cfg->linear_log ? 1 : 0;
+  c->prelu = cfg->activation == COLD_PRELU;
   c->flags = cfg->flags;
   c->groups.assign(cfg->groups, cfg->groups + cfg->num_groups);
   c->widths.assign(cfg->widths, cfg->widths + cfg->num_layers);
@@ -575,7 +580,8 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       const int k4 = (Lg - 2 == 0) ? c->d_ac_pad : (Lg >= 3 ? c->widths[Lg - 3] : 0);
       const int k3 = (Lg - 3 == 0) ? c->d_ac_pad : (Lg >= 4 ? c->widths[Lg - 4] : 0);
       if (want == 2 && Lg >= 2 && tail45_supported(c->widths[Lg - 2], c->widths[Lg - 1], k4)) c->tail_mode = 2;
-      else if (want >= 1 && Lg >= 3 && tail_supported(c->widths[Lg - 3], c->widths[Lg - 2], c->widths[Lg - 1], k3))
+      else if (want >= 1 && Lg >= 3 && !c->prelu &&   // (the 3-layer tail kernel has no PReLU epilogue)
+               tail_supported(c->widths[Lg - 3], c->widths[Lg - 2], c->widths[Lg - 1], k3))
         c->tail_mode = 1;
       c->n_tail = c->tail_mode == 1 ? 3 : (c->tail_mode == 2 ? 2 : 0);
     }
@@ -647,7 +653,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     // COLD_CHAIN=2 also folds FC4 / FC5 / head into the chain: measured slower than the separate
     // resident-weight tail kernel (N = 128 / 64 pair tiles, larger live L2 set), so off by default
     c->chain_tail = c->chain && chain_tail_supported(c->widths[3], c->widths[4], c->widths[2]) &&
-                    c->widths[5] <= 2 && env_chain != nullptr && atoi(env_chain) == 2;
+                    c->widths[5] <= 2 && env_chain != nullptr && atoi(env_chain) == 2 && !c->prelu;
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       [&] {   // the user kernel is on the latency path's critical chain: highest stream priority
@@ -689,7 +695,7 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
   cfg.selected = src->sel.data();
   cfg.num_layers = src->L;
   cfg.widths = src->widths.data();
-  cfg.activation = COLD_RELU;
+  cfg.activation = src->prelu ? COLD_PRELU : COLD_RELU;
   cfg.linear_log = src->linear_log;
   cfg.precision = src->precision;
   cfg.device = src->device;
@@ -723,6 +729,7 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
     c->d_w[l] = src->d_w[l];
     c->d_b[l] = src->d_b[l];
     c->d_wt[l] = src->d_wt[l];
+    c->d_slope[l] = src->d_slope[l];
     c->tmB[l] = src->tmB[l];
   }
   c->tmW4h = src->tmW4h;
@@ -841,6 +848,15 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
     if (s) return s;
     s = upload(c, (void**)&c->d_in_shift, sizeof(float) * c->d_in, [&](uint8_t* h) { memcpy(h, p->in_shift, sizeof(float) * c->d_in); });
     if (s) return s;
+  }
+  if (c->prelu) {   // PReLU slopes of the hidden layers, fp32 (F2)
+    if (!p->act_slope) return fail(COLD_ERR_PARAMS, "activation PReLU needs act_slope");
+    for (int l = 0; l < c->L - 1; l++) {
+      if (!p->act_slope[l]) return fail(COLD_ERR_PARAMS, "act_slope[l] is NULL");
+      s = upload(c, (void**)&c->d_slope[l], sizeof(float) * c->widths[l],
+                 [&](uint8_t* h) { memcpy(h, p->act_slope[l], sizeof(float) * c->widths[l]); });
+      if (s) return s;
+    }
   }
   if (c->dense_se) {   // Wd^T [D_in][n_sel] and bd, fp32
     if (!p->se_w_dense || !p->se_b_dense) return fail(COLD_ERR_PARAMS, "se_mode dense needs se_w_dense and se_b_dense");
@@ -1195,6 +1211,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
       mw = std::max(mw, c->widths[l]);
     }
     m.max_w = (mw + 3) / 4 * 4;   // float4 activation reads
+    for (int l = 0; l < c->L - 1; l++) m.slope[l] = c->d_slope[l];
     m.scores = scores_out;
     c->mark_begin(st);
     launch_mlp_f32(m, st);
@@ -1209,6 +1226,9 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     memset(&cp, 0, sizeof(cp));
     cp.b2 = c->d_b[1];
     cp.b3 = c->d_b[2];
+    cp.s1 = c->d_slope[0];
+    cp.s2 = c->d_slope[1];
+    cp.s3 = c->d_slope[2];
     cp.u1 = c->d_u1;
     cp.ld_u1 = c->widths[0];
     cp.req_of_ad = c->d_req;
@@ -1265,6 +1285,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
     ep.relu = 1;
+    ep.slope = c->d_slope[l];
     if (l == 0) {
       ep.u1 = c->d_u1;
       ep.ld_u1 = c->widths[0];
@@ -1315,6 +1336,8 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     tp.head_b = c->d_head_b;
     tp.head_n = c->widths[c->L - 1];
     tp.scores = scores_out;
+    tp.s4 = c->d_slope[l4];
+    tp.s5 = c->d_slope[l4 + 1];
     {
       static const bool rev = !(getenv("COLD_TAIL_REV") && atoi(getenv("COLD_TAIL_REV")) == 0);
       tp.reverse = rev ? 1 : 0;
@@ -1327,6 +1350,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
   if (c->tail_mode == 1) {
     const int l3 = c->L - 4;
     TailParams tp;
+    memset(&tp, 0, sizeof(tp));
     tp.b3 = c->d_b[l3];
     tp.b4 = c->d_b[l3 + 1];
     tp.b5 = c->d_b[l3 + 2];

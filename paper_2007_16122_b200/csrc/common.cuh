@@ -21,6 +21,9 @@ __device__ __forceinline__ float linear_log(float x) {
   return x;
 }
 
+// PReLU hidden activation: x for x > 0, slope a x otherwise (NaN stays NaN).
+__device__ __forceinline__ float prelu(float x, float a) { return x > 0.0f ? x : a * x; }
+
 // sigma, branch form that never overflows expf.
 __device__ __forceinline__ float sigmoid(float z) {
   if (z >= 0.0f) return 1.0f / (1.0f + expf(-z));

@@ -28,7 +28,8 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
                                                uint8_t* group_buf, const CUtensorMap* tmC, int col_base,
                                                int tile_row0, int q, int h, int lane, int dbg = 0,
                                                unsigned long long* tacc = nullptr, void* gout = nullptr,
-                                               int ldo = 0, int M = 0, uint64_t store_policy = 0) {
+                                               int ldo = 0, int M = 0, uint64_t store_policy = 0,
+                                               const float* __restrict__ slope = nullptr) {
   const uint32_t sbuf = smem_u32(group_buf) + (uint32_t)q * EPI_WIDE_BOX;
   const bool elected = (q == 0) && (lane == 0);
   // debug timing (tacc != null, lane 0): cycles in [0] TMEM load+wait, [1] math+pack, [2] wait for the
@@ -74,7 +75,16 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
       }
     }
     uint32_t pk[32];
-    if (relu) {
+    if (slope) {                          // PReLU (F2): per-column slope, then the plain RNE pack
+#pragma unroll
+      for (int i = 0; i < 64; i += 4) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(slope + col0 + i));
+        f[i] = prelu(f[i], a.x); f[i + 1] = prelu(f[i + 1], a.y);
+        f[i + 2] = prelu(f[i + 2], a.z); f[i + 3] = prelu(f[i + 3], a.w);
+      }
+#pragma unroll
+      for (int i = 0; i < 32; i++) pk[i] = Pack<BF16>::two(f[2 * i], f[2 * i + 1]);
+    } else if (relu) {
 #pragma unroll
       for (int i = 0; i < 32; i++) pk[i] = Pack<BF16>::two_relu(f[2 * i], f[2 * i + 1]);
     } else {

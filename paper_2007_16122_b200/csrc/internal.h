@@ -133,6 +133,7 @@ struct MlpF32Args {
   const float* wt[COLD_MAX_LAYERS];  // layer 0: W1_ac^T [d_ac][W0]; l>0: W_l^T [in][out]
   const float* b[COLD_MAX_LAYERS];   // layer 0 unused (inside u1)
   int width[COLD_MAX_LAYERS];
+  const float* slope[COLD_MAX_LAYERS];   // PReLU slopes of hidden layer l (F2; null: ReLU)
   int max_w;
   float* scores;                   // chunk-local [n]
 };
@@ -150,6 +151,7 @@ struct EpiParams {
   int head_n;                      // 0: no head; 1 or 2: fused last layer + sigmoid
   float* scores;                   // chunk-local [M]
   int relu;
+  const float* slope;              // PReLU slopes [N] (F2; null: ReLU when relu)
   unsigned long long* instr;       // debug: per-role wait-cycle counters [8] (null = off)
   int direct;                      // epilogue writes rows with st.global (no smem staging / TMA store)
   int dbg_mode;                    // timing experiments only (results invalid): 1 = epilogue only drains
@@ -179,6 +181,7 @@ struct TailParams {
   float* scores;                   // chunk-local [M]
   int reverse;                     // tail45: walk tiles last-first (the most recently written H3 rows are
                                    // the ones still in L2)
+  const float* s4; const float* s5;  // tail45 PReLU slopes of FC(L-3) / FC(L-2) (F2; null: ReLU)
 };
 bool tail_supported(int n3, int n4, int n5, int k3);
 cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const CUtensorMap* tmB4,
@@ -188,6 +191,7 @@ cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const 
 // FC1 -> FC2 -> FC3 in one persistent CTA-pair kernel over 256-row blocks (kernels_chain.cu)
 struct ChainParams {
   const float* b2; const float* b3;      // FC2 / FC3 biases (FC1's bias is inside u1)
+  const float* s1; const float* s2; const float* s3;   // PReLU slopes of FC1..FC3 (F2; null: ReLU)
   const float* u1; int ld_u1;            // FC1 fallback for blocks spanning > U1_NSLOT requests
   const int32_t* req_of_ad; int64_t a0;
   int n1, n2, n3, k1;                    // widths of FC1..FC3 and FC1's K (D_ac_pad)

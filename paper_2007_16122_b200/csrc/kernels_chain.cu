@@ -284,9 +284,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           bias_s = smem_u32(sBias) + (uint32_t)((l == 1 ? 0 : cp.n2) + nb * tn[l]) * 4u;
           bias = nullptr;
         }
+        const float* slope = l == 0 ? cp.s1 : (l == 1 ? cp.s2 : (l == 2 ? cp.s3 : nullptr));
         epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, bias_s, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
                              nb * tn[l], trow0, q, h, lane, 0, nullptr, nullptr, 0, 0,
-                             (!TAIL && l == 2 && cp.h3_evict_first) ? pol_h3 : 0ull);
+                             (!TAIL && l == 2 && cp.h3_evict_first) ? pol_h3 : 0ull, slope);
       }
       tc_fence_before();
       __syncwarp();

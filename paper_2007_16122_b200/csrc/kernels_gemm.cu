@@ -272,7 +272,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int c_stop = ep.dbg_mode == 1 ? c_begin : c_end;
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
         epi_store_wide<BF16>(tbase, c_begin, c_stop, ep.bias, u1s, u1row, ep.relu,
-                             sOut + h * EPI_GROUP_BOX, &tmC, nb * BN, row0 - q * 32, q, h, lane, ep.dbg_mode);
+                             sOut + h * EPI_GROUP_BOX, &tmC, nb * BN, row0 - q * 32, q, h, lane, ep.dbg_mode,
+                             nullptr, nullptr, 0, 0, 0ull, ep.slope);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -312,7 +313,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             f[i] += b.x; f[i + 1] += b.y; f[i + 2] += b.z; f[i + 3] += b.w;
           }
         }
-        if (ep.relu) {
+        if (ep.slope) {   // PReLU (F2)
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(ep.slope + col0 + i));
+            f[i] = prelu(f[i], a.x); f[i + 1] = prelu(f[i + 1], a.y);
+            f[i + 2] = prelu(f[i + 2], a.z); f[i + 3] = prelu(f[i + 3], a.w);
+          }
+        } else if (ep.relu) {
 #pragma unroll
           for (int i = 0; i < 32; i++) f[i] = fmaxf(f[i], 0.0f);
         }

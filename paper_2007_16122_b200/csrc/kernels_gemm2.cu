@@ -268,7 +268,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>
         const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN);
         epi_store_wide<BF16>(tbase, c_begin, c_stop, ep.bias, u1s, u1row, ep.relu,
                              sOut + h * EPI_GROUP_BOX, &tmC, nb * BN, row0 - q * 32, q, h, lane, ep.dbg_mode,
-                             ep.instr, ep.direct ? ep.out : nullptr, ep.ldo, M);
+                             ep.instr, ep.direct ? ep.out : nullptr, ep.ldo, M, 0ull, ep.slope);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
@@ -306,7 +306,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>
             f[i] += b.x; f[i + 1] += b.y; f[i + 2] += b.z; f[i + 3] += b.w;
           }
         }
-        if (ep.relu) {
+        if (ep.slope) {   // PReLU (F2)
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(ep.slope + col0 + i));
+            f[i] = prelu(f[i], a.x); f[i + 1] = prelu(f[i + 1], a.y);
+            f[i + 2] = prelu(f[i + 2], a.z); f[i + 3] = prelu(f[i + 3], a.w);
+          }
+        } else if (ep.relu) {
 #pragma unroll
           for (int i = 0; i < 32; i++) f[i] = fmaxf(f[i], 0.0f);
         }

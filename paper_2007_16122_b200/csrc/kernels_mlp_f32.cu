@@ -84,7 +84,9 @@ __global__ void __launch_bounds__(MLP_THREADS) mlp_f32_kernel(MlpF32Args a) {
       for (int q = 0; q < 4; q++) {
         if (!jv[q]) continue;
 #pragma unroll
-        for (int t = 0; t < MLP_TILE; t++) o[t * a.max_w + js[q]] = last ? acc[q][t] : fmaxf(acc[q][t], 0.0f);
+        for (int t = 0; t < MLP_TILE; t++)
+          o[t * a.max_w + js[q]] = last ? acc[q][t]
+                                        : (a.slope[l] ? prelu(acc[q][t], __ldg(a.slope[l] + js[q])) : fmaxf(acc[q][t], 0.0f));
       }
     }
     __syncthreads();

@@ -176,10 +176,19 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
         const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + 8 * j));
         const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + 8 * j + 4));
         uint4 w;
-        w.x = Pack<BF16>::two_relu(__uint_as_float(v[o + 0]) + b0.x, __uint_as_float(v[o + 1]) + b0.y);
-        w.y = Pack<BF16>::two_relu(__uint_as_float(v[o + 2]) + b0.z, __uint_as_float(v[o + 3]) + b0.w);
-        w.z = Pack<BF16>::two_relu(__uint_as_float(v[o + 4]) + b1.x, __uint_as_float(v[o + 5]) + b1.y);
-        w.w = Pack<BF16>::two_relu(__uint_as_float(v[o + 6]) + b1.z, __uint_as_float(v[o + 7]) + b1.w);
+        if (tp.s4) {   // PReLU (F2)
+          const float4 a0 = __ldg(reinterpret_cast<const float4*>(tp.s4 + 64 * h + 8 * j));
+          const float4 a1 = __ldg(reinterpret_cast<const float4*>(tp.s4 + 64 * h + 8 * j + 4));
+          w.x = Pack<BF16>::two(prelu(__uint_as_float(v[o + 0]) + b0.x, a0.x), prelu(__uint_as_float(v[o + 1]) + b0.y, a0.y));
+          w.y = Pack<BF16>::two(prelu(__uint_as_float(v[o + 2]) + b0.z, a0.z), prelu(__uint_as_float(v[o + 3]) + b0.w, a0.w));
+          w.z = Pack<BF16>::two(prelu(__uint_as_float(v[o + 4]) + b1.x, a1.x), prelu(__uint_as_float(v[o + 5]) + b1.y, a1.y));
+          w.w = Pack<BF16>::two(prelu(__uint_as_float(v[o + 6]) + b1.z, a1.z), prelu(__uint_as_float(v[o + 7]) + b1.w, a1.w));
+        } else {
+          w.x = Pack<BF16>::two_relu(__uint_as_float(v[o + 0]) + b0.x, __uint_as_float(v[o + 1]) + b0.y);
+          w.y = Pack<BF16>::two_relu(__uint_as_float(v[o + 2]) + b0.z, __uint_as_float(v[o + 3]) + b0.w);
+          w.z = Pack<BF16>::two_relu(__uint_as_float(v[o + 4]) + b1.x, __uint_as_float(v[o + 5]) + b1.y);
+          w.w = Pack<BF16>::two_relu(__uint_as_float(v[o + 6]) + b1.z, __uint_as_float(v[o + 7]) + b1.w);
+        }
         sts128(smem_u32(atom) + sw128_offset(r, j), w);
       }
       fence_async_smem();      // generic-proxy smem writes -> visible to the tensor core (async proxy)
@@ -201,7 +210,8 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
         float z0 = 0.0f, z1 = 0.0f;
 #pragma unroll
         for (int i = 0; i < 64; i++) {
-          const float a = fmaxf(__uint_as_float(i < 32 ? v0[i] : v1[i - 32]) + __ldg(tp.b5 + i), 0.0f);
+          const float x5 = __uint_as_float(i < 32 ? v0[i] : v1[i - 32]) + __ldg(tp.b5 + i);
+          const float a = tp.s5 ? prelu(x5, __ldg(tp.s5 + i)) : fmaxf(x5, 0.0f);
           z0 = fmaf(__ldg(tp.head_w + i), a, z0);
           if (tp.head_n == 2) z1 = fmaf(__ldg(tp.head_w + Q_N5 + i), a, z1);
         }

@@ -16,7 +16,7 @@ def make_ctx(schema, params, precision=None, selected=None, linear_log=None, max
     return ctx
 
 
-def load_params(ctx, params):
+def load_params(ctx, params, **kw):
     tables = params.tables
     tdt = params.table_dtype
     if ctx.precision == "f32" and tdt != "f32":          # widen stored 16-bit values (exact)
@@ -24,7 +24,7 @@ def load_params(ctx, params):
         tdt = "f32"
     elif tdt == "f16":
         tables = [t.view(np.uint16) for t in tables]
-    return ctx.load_params(tables, params.se_w, params.se_b, params.fc_w, params.fc_b, table_dtype=tdt)
+    return ctx.load_params(tables, params.se_w, params.se_b, params.fc_w, params.fc_b, table_dtype=tdt, **kw)
 
 
 def device_batch(batch: coldgen.Batch, pin=False):

@@ -731,3 +731,33 @@ def test_graph_replay_matches_direct_call():
         p, z = oracle.score(oracle.Model(sch, params), singles[i])
         _check_scores(got_sc.cpu().numpy().astype(np.float64), p, z, "f16", f"graph replay request {i}")
     ctx.close()
+
+
+# ---- F2: PReLU hidden activation (per-channel slopes) ----------------------------------------
+
+@pytest.mark.parametrize("prec,chain_min", [("f32", None), ("f16", None), ("bf16", None), ("f16", "0"),
+                                            ("bf16", "0")])
+def test_prelu_variant(prec, chain_min, monkeypatch):
+    """activation = COLD_PRELU: every hidden layer h = x (x > 0) or a_c x with per-channel fp32 slopes,
+    on the fp32 SIMT path, the tcgen05 layer-by-layer pair GEMMs + fused FC4/FC5/head tail, and (chain_min
+    0) the FC1->FC3 chain; vs the oracle's PReLU mode; ReLU scores differ (the slopes matter)."""
+    from paper_2007_16122_b200 import Context
+    if chain_min is not None:
+        monkeypatch.setenv("COLD_CHAIN_MIN", chain_min)
+    cap = 20000
+    sch, params, batch = small_case("paper", R=3, n_ads=(1200, 33, 700), precision=prec, cap=cap, seed=101)
+    slopes = coldgen.prelu_slopes(sch, seed=102)
+    ctx = Context(sch.groups, sch.k, sch.widths, precision=prec, max_ads=1 << 16, max_requests=64,
+                  activation="prelu")
+    load_params(ctx, params, act_slope=slopes)
+    got = gpu_scores(ctx, batch)
+    p, z = oracle.score(oracle.Model(sch, params, prelu=slopes), batch)
+    _check_scores(got, p, z, prec, f"prelu {prec}")
+    p_relu, _ = oracle.score(oracle.Model(sch, params), batch)
+    assert np.max(np.abs(p - p_relu) / p_relu) > 5 * TOL[prec]       # (0.24 on this case)
+    # missing slopes: COLD_ERR_PARAMS
+    from paper_2007_16122_b200 import ColdError
+    ctx2 = Context(sch.groups, sch.k, sch.widths, precision=prec, max_ads=4096, max_requests=8, activation="prelu")
+    with pytest.raises(ColdError) as e:
+        load_params(ctx2, params)
+    assert e.value.name == "COLD_ERR_PARAMS"
