@@ -186,6 +186,7 @@ struct cold_ctx {
   CUtensorMap tmW4h, tmW5h;          // W4 / W5 with half-N boxes (CTA-pair tiles)
   std::vector<CUtensorMap> tmOH;     // per chunk slot of the span
   int gspan = 1;                     // chunks per column-wise gather pass (X_ac holds gspan * chunk rows)
+  int gather_ring = 0;               // > 0: cross-bag columns through a cp.async ring of this depth
   CUtensorMap tmC[COLD_MAX_LAYERS];  // epilogue TMA-store maps (32 x 32 boxes)
   int cs[COLD_MAX_LAYERS] = {0};     // cluster size (weight-tile multicast) per GEMM layer
   bool resb[COLD_MAX_LAYERS] = {false};  // weight slice resident in shared memory (K x BN <= 128 KB)
@@ -506,6 +507,11 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   }
   c->max_ads = cfg->max_ads_per_call;
   c->max_req = cfg->max_requests_per_call;
+  {
+    const char* env_ring = getenv("COLD_GATHER_RING");
+    c->gather_ring = env_ring ? atoi(env_ring) : 0;
+    if (c->gather_ring != 4 && c->gather_ring != 5 && c->gather_ring != 8) c->gather_ring = 0;
+  }
 
   if (cudaSetDevice(c->device) != cudaSuccess) { delete c; return fail(COLD_ERR_CUDA, "cudaSetDevice failed"); }
   cudaDeviceProp prop;
@@ -1481,6 +1487,27 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
       c->mark_begin(st);
       launch_gather(g1, c->precision, st);
       c->mark_end(COLD_PROF_GATHER, st);
+    } else if (c->gather_ring && c->tensor && c->k * c->elem() == 32 && !dbg.pooled && !dbg.feat &&
+               s1 - s0 >= 148 * 128 * 4) {
+      // cross-bag columns (user bag x single ad id) through the cp.async-ring build, then the rest
+      GatherArgs gb = ga, gr = ga;
+      gb.n_ac = gr.n_ac = 0;
+      gb.n_single = 0;
+      gb.ohot = nullptr;
+      gb.ring = c->gather_ring;
+      for (int j = 0; j < ga.n_ac; j++) {
+        const int g = ga.ac_g[ga.order[j]];
+        const cold_group& G = c->groups[g];
+        const bool bagx = G.side == COLD_CROSS && c->groups[G.user_ref].pooled && !c->groups[G.ad_ref].pooled;
+        GatherArgs& d = bagx ? gb : gr;
+        d.ac_g[d.n_ac] = g;
+        d.order[d.n_ac] = d.n_ac;
+        d.n_ac++;
+      }
+      c->mark_begin(gst);
+      if (gb.n_ac) launch_gather(gb, c->precision, gst);
+      launch_gather(gr, c->precision, gst);
+      c->mark_end(COLD_PROF_GATHER, gst);
     } else {
       c->mark_begin(gst);
       launch_gather(ga, c->precision, gst);

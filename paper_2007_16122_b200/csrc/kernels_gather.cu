@@ -429,12 +429,104 @@ __device__ __forceinline__ void singles_column(const GatherArgs& a) {
   }
 }
 
+// ---- cp.async (LDGSTS) helpers: 16 B global -> shared copies that complete asynchronously, tracked
+// per thread in commit groups (no registers held while a row is in flight)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Cross group of a user bag x a single-valued ad id (S-paper: clk_cate x cate, clk_shop x shop,
+// clk_brand x brand: 48 of the 61 rows of an ad). The thread's APT ads x L bag rows form one row
+// stream: a producer cursor issues row j + RING (two 16 B cp.async into ring slot (j + RING) % RING of
+// this thread) while the consumer adds row j from its slot, so RING rows stay in flight continuously
+// instead of bursts of RB register-held rows with a full round trip between bursts. The ring is
+// [RING][128 threads][32 B] (a warp reads 1 KB contiguous per slot: no bank conflicts). Rows are
+// still summed one at a time in bag order (x-major), so the fp32 sums are unchanged (D-3).
+template <typename T, int K, bool FAST, int APT, int RING>
+__device__ __forceinline__ void cross_bag_ring(const GatherArgs& a, const DevGroup& G, int g, const T* __restrict__ tab,
+                                               uint64_t card, const uint64_t (*s_hx)[HX_HALF], const int64_t* ul,
+                                               int rfirst, const BatchGroup& BA, const DevGroup& A,
+                                               const float* sew, float seb, const int64_t* loc, const bool* ok) {
+  static_assert(K * (int)sizeof(T) == 32, "ring rows are 32 B");
+  extern __shared__ __align__(16) uint8_t ring_smem[];
+  const uint32_t my = smem_addr(ring_smem) + threadIdx.x * 32u;
+  constexpr uint32_t SLOT = 128u * 32u;
+  uint64_t y[APT];
+  int sl[APT], len[APT];
+#pragma unroll
+  for (int i = 0; i < APT; i++) {
+    y[i] = (uint64_t)checked(BA.ids[a.a0 + loc[i] - BA.id_shift], A.card, a.validate, a.err);
+    sl[i] = (req_at(a, a.a0 + loc[i]) == rfirst) ? 0 : 1;
+    len[i] = (int)ul[sl[i]];
+  }
+  // producer cursor (ad pi, bag element px) and the ring slot it fills next
+  int pi = 0, px = 0, ps = 0;
+  while (pi < APT && len[pi] == 0) pi++;
+  auto issue = [&]() {
+    if (pi < APT) {
+      uint64_t yy = y[0];
+      int ss = sl[0], ll = len[0];
+#pragma unroll
+      for (int i = 1; i < APT; i++)
+        if (pi == i) { yy = y[i]; ss = sl[i]; ll = len[i]; }
+      const uint4* src = reinterpret_cast<const uint4*>(tab + cross_row_from_hx(s_hx[ss][px], yy, card) * K);
+      const uint32_t dst = my + (uint32_t)ps * SLOT;
+      cp_async16(dst, src);
+      cp_async16(dst + 16u, src + 1);
+      if (++px == ll) {
+        px = 0;
+        do pi++; while (pi < APT && len[pi] == 0);
+      }
+    }
+    cp_async_commit();   // (an empty group once the stream is exhausted keeps the wait count uniform)
+    ps = ps + 1 == RING ? 0 : ps + 1;
+  };
+#pragma unroll
+  for (int r = 0; r < RING; r++) issue();
+  int cs = 0;
+#pragma unroll
+  for (int i = 0; i < APT; i++) {
+    float e[K];
+#pragma unroll
+    for (int d = 0; d < K; d++) e[d] = 0.0f;
+#pragma unroll 1
+    for (int x = 0; x < len[i]; x++) {
+      cp_async_wait<RING - 1>();   // the oldest group (this row) has landed
+      const uint32_t src = my + (uint32_t)cs * SLOT;
+      uint4 q0, q1;
+      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(q0.x), "=r"(q0.y), "=r"(q0.z), "=r"(q0.w) : "r"(src));
+      asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(q1.x), "=r"(q1.y), "=r"(q1.z), "=r"(q1.w)
+                   : "r"(src + 16u));
+      cs = cs + 1 == RING ? 0 : cs + 1;
+      issue();                     // refill: the slot just read is reused RING rows later
+      const T* t0 = reinterpret_cast<const T*>(&q0);
+      const T* t1 = reinterpret_cast<const T*>(&q1);
+#pragma unroll
+      for (int d = 0; d < 8; d++) e[d] = Store<T>::add(e[d], t0[d]);
+#pragma unroll
+      for (int d = 0; d < 8; d++) e[8 + d] = Store<T>::add(e[8 + d], t1[d]);
+    }
+    if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb);
+  }
+  cp_async_wait<0>();
+}
+
 // APT: ads per thread (4 for large spans; 1 for small batches, where per-thread serial work is the latency)
-template <typename T, int K, bool FAST, int MINB = 4, int GATHER_APT = 4>
+// RING > 0: cross-bag columns stream their rows through a RING-deep cp.async ring (dynamic smem
+// RING * 4 KB); 0: register-held bursts of GATHER_RB rows
+template <typename T, int K, bool FAST, int MINB = 4, int GATHER_APT = 4, int RING = 0>
 __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
+  if constexpr (RING == 0) {
   if (a.n_single > 0 && (int)blockIdx.y == a.n_ac) {
     if constexpr ((K * (int)sizeof(T)) % 16 == 0) singles_column<T, K, FAST, GATHER_APT>(a);
     return;
+  }
   }
   if ((int)blockIdx.y == a.n_ac + (a.n_single > 0 ? 1 : 0)) {   // FC1's one-hot u1 operand rows
     for (int i = 0; i < GATHER_APT; i++) {
@@ -473,7 +565,8 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
     loc[i] = ok[i] ? l : a.n - 1;           // clamped: loads stay in range, results are dropped
   }
 
-  if (G.side == 1) {                        // ---------------- AD group ----------------
+  // (the RING build is launched over cross-bag columns only: no AD-group code in it)
+  if (RING == 0 && G.side == 1) {           // ---------------- AD group ----------------
     const BatchGroup& B = a.bv.g[g];
     if (!G.pooled && VEC) {
       int64_t row[GATHER_APT];
@@ -536,7 +629,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
         s_hx[q][i] = fmix64((uint64_t)checked(BU.ids[ub[q] + i], U.card, a.validate, a.err) ^ salt);
     __syncthreads();
   }
-  if (shared_hx && !A.pooled && VEC && ul[0] == 1 && ul[1] == 1) {
+  if (RING == 0 && shared_hx && !A.pooled && VEC && ul[0] == 1 && ul[1] == 1) {
     // single-id user group x single-id ad group: one row per ad, all APT rows in flight
     int64_t row[GATHER_APT];
 #pragma unroll
@@ -559,6 +652,12 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
     return;
   }
 
+  if constexpr (RING > 0 && K * (int)sizeof(T) == 32) {
+    if (shared_hx && !A.pooled) {
+      cross_bag_ring<T, K, FAST, GATHER_APT, RING>(a, G, g, tab, card, s_hx, ul, rfirst, BA, A, sew, seb, loc, ok);
+      return;
+    }
+  }
   for (int i = 0; i < GATHER_APT; i++) {
     const int64_t li = base + threadIdx.x + i * 128;
     if (li >= a.n) break;
@@ -684,7 +783,10 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
     case 16: {
       static const int minb = getenv("COLD_GATHER_MINB") ? atoi(getenv("COLD_GATHER_MINB")) : 8;
       static const int apt = getenv("COLD_GATHER_APT") ? atoi(getenv("COLD_GATHER_APT")) : 4;
-      if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
+      if (sizeof(T) == 2 && a.ring == 4) gather_kernel<T, 16, FAST, 8, 4, 4><<<grid, 128, 4 * 4096, s>>>(a);
+      else if (sizeof(T) == 2 && a.ring == 5) gather_kernel<T, 16, FAST, 8, 4, 5><<<grid, 128, 5 * 4096, s>>>(a);
+      else if (sizeof(T) == 2 && a.ring == 8) gather_kernel<T, 16, FAST, 6, 4, 8><<<grid, 128, 8 * 4096, s>>>(a);
+      else if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
       else if (apt == 2) gather_kernel<T, 16, FAST, 8, 2><<<grid_for(2), 128, 0, s>>>(a);
       else if (apt == 1) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);
       else if (minb >= 16) gather_kernel<T, 16, FAST, 16><<<grid, 128, 0, s>>>(a);

@@ -761,3 +761,20 @@ def test_prelu_variant(prec, chain_min, monkeypatch):
     with pytest.raises(ColdError) as e:
         load_params(ctx2, params)
     assert e.value.name == "COLD_ERR_PARAMS"
+
+
+@pytest.mark.parametrize("ring", ["4", "5", "8"])
+def test_gather_ring_equals_register_path(ring, monkeypatch):
+    """The cp.async-ring build of the cross-bag columns (COLD_GATHER_RING) sums the same rows in the same
+    bag order as the register path, so whole-span scores are bit-identical; a sample is checked against
+    the oracle. Spans of >= 75,776 ads take the ring; requests of mixed sizes put 1-3 requests in a CTA."""
+    sizes = [5000, 37, 20000, 1, 3000] * 6
+    sch, params, batch = small_case("paper", R=len(sizes), n_ads=tuple(sizes), precision="f16", cap=50000, seed=111)
+    monkeypatch.setenv("COLD_GATHER_RING", "0")
+    ref = gpu_scores(make_ctx(sch, params, max_ads=batch.n_ads, max_requests=64), batch)
+    monkeypatch.setenv("COLD_GATHER_RING", ring)
+    got = gpu_scores(make_ctx(sch, params, max_ads=batch.n_ads, max_requests=64), batch)
+    np.testing.assert_array_equal(got, ref)
+    ads = np.random.default_rng(3).choice(batch.n_ads, 300, replace=False)
+    p, z = oracle.score(oracle.Model(sch, params), batch, ad_list=ads)
+    _check_scores(got[ads], p, z, "f16", f"ring {ring}")
