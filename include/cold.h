@@ -71,6 +71,20 @@ enum { COLD_RELU = 0, COLD_PRELU = 1 };
 #define COLD_VALIDATE_IDS 1u   /* check every id against its cardinality (one D2H sync per call);
                                   without it out-of-range ids are clamped to card-1 */
 
+/* config.kernel_flags: kernel-selection overrides. 0 selects the measured-fastest kernels;
+ * the others exist so that the tests cover every kernel the library can fall back to (non-paper
+ * widths, small calls) and for A/B measurement. Results are identical up to the stated tolerances. */
+#define COLD_K_LAYERWISE    1u   /* FC1..FC3 as separate GEMM launches instead of the chain kernel */
+#define COLD_K_NO_U1_MMA    2u   /* FC1 adds u1[request] in the epilogue instead of one extra K=16 MMA */
+#define COLD_K_SINGLE_CTA   4u   /* single-CTA tcgen05 GEMMs instead of CTA pairs (cta_group::2) */
+#define COLD_K_PAIR_STREAM  8u   /* CTA-pair GEMMs stream their weight half instead of keeping it resident */
+#define COLD_K_STREAM_B    16u   /* single-CTA GEMMs stream the weight tile instead of keeping it resident */
+#define COLD_K_TAIL_NONE   32u   /* no fused tail kernel: every hidden layer a GEMM (head fused into the last) */
+#define COLD_K_TAIL3       64u   /* the FC(L-3)..head fused tail instead of FC(L-2)..head (tail45) */
+#define COLD_K_CHAIN_TAIL 128u   /* FC4/FC5/head inside the chain kernel (measured 4% slower; ReLU only) */
+#define COLD_K_SERIAL_USER 256u  /* calls of <= 4 requests: user kernel before the gather, one stream */
+#define COLD_K_NO_PDL     512u   /* no programmatic dependent launch between the kernels */
+
 /* A feature group ("the embedding of the i-th feature group e_i"). */
 typedef struct {
   int32_t side;          /* COLD_USER / COLD_AD / COLD_CROSS */
@@ -111,6 +125,13 @@ typedef struct {
                                     so the user block is no longer hoisted into u1 (FC1 runs over all D_in
                                     columns; cold_params.se_w_dense / se_b_dense are required, se_w / se_b
                                     are ignored). Not with cold_se_stats (COLD_ERR_UNSUPPORTED). */
+  uint32_t kernel_flags;         /* COLD_K_* overrides; 0 = default kernel selection */
+  int32_t gather_span_chunks;    /* chunks per column-wise gather pass; 0 = default (16) */
+  int64_t chain_min_ads;         /* chunks of fewer ads run FC1..FC3 layer by layer (the chain needs >= 2
+                                    256-row blocks per CTA pair to fill the GPU); 0 = default (256 x SMs),
+                                    1 = the chain for every chunk */
+  int32_t gather_ring;           /* cross-bag gather columns through a cp.async ring of this depth (4, 5 or
+                                    8 rows per thread); 0 = default, -1 = register-held row bursts */
 } cold_config;
 
 enum { COLD_SE_GROUP = 0, COLD_SE_DENSE = 1 };

@@ -32,6 +32,9 @@ EXPORTS = ["cold_create", "cold_destroy", "cold_load_params", "cold_score_batch"
 PROF_KINDS = 23
 PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC, PROF_SE_DENSE = 0, 1, 2, 3, 3 + 16
 PROF_CHAIN, PROF_TAIL, PROF_MLP_F32 = 20, 21, 22
+# cold_config.kernel_flags (include/cold.h COLD_K_*)
+K_LAYERWISE, K_NO_U1_MMA, K_SINGLE_CTA, K_PAIR_STREAM, K_STREAM_B = 1, 2, 4, 8, 16
+K_TAIL_NONE, K_TAIL3, K_CHAIN_TAIL, K_SERIAL_USER, K_NO_PDL = 32, 64, 128, 256, 512
 
 
 class ColdError(RuntimeError):
@@ -52,7 +55,9 @@ class cold_config(C.Structure):
                 ("num_layers", C.c_int32), ("widths", C.POINTER(C.c_int32)),
                 ("activation", C.c_int32), ("linear_log", C.c_int32), ("precision", C.c_int32),
                 ("device", C.c_int32), ("max_ads_per_call", C.c_int64), ("max_requests_per_call", C.c_int32),
-                ("chunk_ads", C.c_int32), ("flags", C.c_uint32), ("se_mode", C.c_int32)]
+                ("chunk_ads", C.c_int32), ("flags", C.c_uint32), ("se_mode", C.c_int32),
+                ("kernel_flags", C.c_uint32), ("gather_span_chunks", C.c_int32), ("chain_min_ads", C.c_int64),
+                ("gather_ring", C.c_int32)]
 
 
 class cold_params(C.Structure):
@@ -189,7 +194,10 @@ class Context:
     def __init__(self, groups, emb_dim: int, widths: Sequence[int], precision: str = "f16",
                  selected: Optional[Sequence[int]] = None, linear_log: bool = True, device: int = 0,
                  max_ads: int = 1 << 20, max_requests: int = 1024, chunk_ads: int = 0, validate_ids: bool = False,
-                 se_mode: str = "group", activation: str = "relu"):
+                 se_mode: str = "group", activation: str = "relu", kernel_flags: int = 0,
+                 gather_span_chunks: int = 0, chain_min_ads: int = 0, gather_ring: int = 0):
+        """kernel_flags (K_* below), gather_span_chunks, chain_min_ads, gather_ring: kernel-selection
+        overrides of include/cold.h (0 = the library's default selection)."""
         L = lib()
         M = len(groups)
         self._groups = (cold_group * M)()
@@ -208,6 +216,8 @@ class Context:
         cfg.max_ads_per_call, cfg.max_requests_per_call = max_ads, max_requests
         cfg.chunk_ads, cfg.flags = chunk_ads, VALIDATE_IDS if validate_ids else 0
         cfg.se_mode = {"group": 0, "dense": 1}[se_mode]   # AMB-1 readings (include/cold.h)
+        cfg.kernel_flags, cfg.gather_span_chunks = int(kernel_flags), int(gather_span_chunks)
+        cfg.chain_min_ads, cfg.gather_ring = int(chain_min_ads), int(gather_ring)
         self.precision = precision
         self.device = device
         self.ctx = C.c_void_p()

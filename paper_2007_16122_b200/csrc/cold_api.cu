@@ -55,81 +55,6 @@ static EncodeTiledFn get_encode() {
   return fn;
 }
 
-// ---- compressible device memory (Blackwell generic compression; activations after ReLU are
-// zero-rich, so their HBM write/read traffic shrinks). Driver VMM entry points fetched at run time.
-typedef CUresult (*PFN_memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long);
-typedef CUresult (*PFN_memAddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long);
-typedef CUresult (*PFN_memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long);
-typedef CUresult (*PFN_memSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t);
-typedef CUresult (*PFN_memGetGran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags);
-typedef CUresult (*PFN_memUnmap)(CUdeviceptr, size_t);
-typedef CUresult (*PFN_memRelease)(CUmemGenericAllocationHandle);
-typedef CUresult (*PFN_memAddressFree)(CUdeviceptr, size_t);
-typedef CUresult (*PFN_memGetProp)(CUmemAllocationProp*, CUmemGenericAllocationHandle);
-template <typename F>
-static F drv(const char* name) {
-  void* p = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-    return nullptr;
-  return reinterpret_cast<F>(p);
-}
-struct CompAlloc {
-  CUdeviceptr ptr = 0;
-  size_t size = 0;
-  CUmemGenericAllocationHandle h = 0;
-};
-// returns nullptr if compressible memory is unavailable (caller falls back to cudaMalloc)
-static void* comp_alloc(int device, size_t bytes, CompAlloc& out, bool& compressed) {
-  static auto create = drv<PFN_memCreate>("cuMemCreate");
-  static auto reserve = drv<PFN_memAddressReserve>("cuMemAddressReserve");
-  static auto map = drv<PFN_memMap>("cuMemMap");
-  static auto access = drv<PFN_memSetAccess>("cuMemSetAccess");
-  static auto gran = drv<PFN_memGetGran>("cuMemGetAllocationGranularity");
-  static auto getprop = drv<PFN_memGetProp>("cuMemGetAllocationPropertiesFromHandle");
-  static auto release = drv<PFN_memRelease>("cuMemRelease");
-  static auto afree = drv<PFN_memAddressFree>("cuMemAddressFree");
-  compressed = false;
-  if (!create || !reserve || !map || !access || !gran || !release || !afree) return nullptr;
-  CUmemAllocationProp prop;
-  memset(&prop, 0, sizeof(prop));
-  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-  prop.location.id = device;
-  prop.allocFlags.compressionType = CU_MEM_ALLOCATION_COMP_GENERIC;
-  size_t g = 0;
-  if (gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || g == 0) return nullptr;
-  const size_t size = (bytes + g - 1) / g * g;
-  CUmemGenericAllocationHandle h;
-  if (create(&h, size, &prop, 0) != CUDA_SUCCESS) return nullptr;
-  CUdeviceptr ptr = 0;
-  if (reserve(&ptr, size, g, 0, 0) != CUDA_SUCCESS) { release(h); return nullptr; }
-  if (map(ptr, size, 0, h, 0) != CUDA_SUCCESS) { afree(ptr, size); release(h); return nullptr; }
-  CUmemAccessDesc ad;
-  memset(&ad, 0, sizeof(ad));
-  ad.location = prop.location;
-  ad.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  if (access(ptr, size, &ad, 1) != CUDA_SUCCESS) { afree(ptr, size); release(h); return nullptr; }
-  if (getprop) {
-    CUmemAllocationProp got;
-    memset(&got, 0, sizeof(got));
-    if (getprop(&got, h) == CUDA_SUCCESS) compressed = got.allocFlags.compressionType == CU_MEM_ALLOCATION_COMP_GENERIC;
-  }
-  out.ptr = ptr;
-  out.size = size;
-  out.h = h;
-  return reinterpret_cast<void*>(ptr);
-}
-static void comp_free(const CompAlloc& a) {
-  static auto unmap = drv<PFN_memUnmap>("cuMemUnmap");
-  static auto release = drv<PFN_memRelease>("cuMemRelease");
-  static auto afree = drv<PFN_memAddressFree>("cuMemAddressFree");
-  if (!a.ptr) return;
-  if (unmap) unmap(a.ptr, a.size);
-  if (release) release(a.h);
-  if (afree) afree(a.ptr, a.size);
-}
-
 struct cold_ctx {
   // ---- configuration ----
   int M = 0, k = 0, L = 0, precision = 0, device = 0, linear_log = 1;
@@ -187,6 +112,9 @@ struct cold_ctx {
   std::vector<CUtensorMap> tmOH;     // per chunk slot of the span
   int gspan = 1;                     // chunks per column-wise gather pass (X_ac holds gspan * chunk rows)
   int gather_ring = 0;               // > 0: cross-bag columns through a cp.async ring of this depth
+  uint32_t kflags = 0;               // cold_config.kernel_flags
+  int64_t cfg_chain_min = 0;         // cold_config.chain_min_ads / gather_span_chunks / gather_ring as given
+  int cfg_span = 0, cfg_ring = 0;    //   (cold_ctx_clone recreates the same selection)
   CUtensorMap tmC[COLD_MAX_LAYERS];  // epilogue TMA-store maps (32 x 32 boxes)
   int cs[COLD_MAX_LAYERS] = {0};     // cluster size (weight-tile multicast) per GEMM layer
   bool resb[COLD_MAX_LAYERS] = {false};  // weight slice resident in shared memory (K x BN <= 128 KB)
@@ -216,8 +144,6 @@ struct cold_ctx {
   size_t topk_out_bytes = 0;
   int64_t device_bytes = 0;
   std::vector<void*> allocs;
-  std::vector<CompAlloc> comp_allocs;  // compressible activation buffers (COLD_COMPRESS)
-  bool compressed = false;
   // per-kernel event profiling
   bool prof = false;
   std::vector<cudaEvent_t> prof_events;       // pool
@@ -236,7 +162,6 @@ struct cold_ctx {
     cudaDeviceSynchronize();
     if (clone_of) clone_of->clones--;
     for (void* p : allocs) cudaFree(p);
-    for (const CompAlloc& a : comp_allocs) comp_free(a);
     for (int i = 0; i < 2; i++) {
       if (d_stage[i]) cudaFree(d_stage[i]);
       if (ev_copied[i]) cudaEventDestroy(ev_copied[i]);
@@ -278,22 +203,6 @@ struct cold_ctx {
     cudaError_t e = cudaMalloc(p, bytes < 16 ? 16 : bytes);
     if (e == cudaSuccess) { allocs.push_back(*p); device_bytes += (int64_t)bytes; }
     return e;
-  }
-  // activation buffers: compressible memory when requested and granted, else cudaMalloc
-  cudaError_t alloc_act(void** p, size_t bytes, bool want_comp) {
-    if (want_comp) {
-      CompAlloc a;
-      bool comp = false;
-      void* q = comp_alloc(device, bytes < 16 ? 16 : bytes, a, comp);
-      if (q) {
-        comp_allocs.push_back(a);
-        *p = q;
-        device_bytes += (int64_t)a.size;
-        compressed = compressed || comp;
-        return cudaSuccess;
-      }
-    }
-    return alloc(p, bytes);
   }
   int elem() const { return precision == COLD_FP32 ? 4 : 2; }
   // input width of layer l as the kernels see it (layer 0: the ad + cross part, or all of D_in under
@@ -478,23 +387,6 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       const int cls = G.side == COLD_CROSS ? 0 : (G.pooled ? 1 : 2);
       if (cls == pass) c->gather_order.push_back((int)j);
     }
-  // COLD_GATHER_ORDER=1: interleave the L2-bound cross-bag columns with the DRAM-bound single-row
-  // columns (heavy, light, heavy, light, ...) instead of all heavy columns first
-  if (getenv("COLD_GATHER_ORDER") && atoi(getenv("COLD_GATHER_ORDER")) == 1) {
-    std::vector<int> heavy, light, mixed;
-    for (int j : c->gather_order) {
-      const cold_group& G = c->groups[c->sel_ac[j]];
-      const bool bagx = G.side == COLD_CROSS && (c->groups[G.user_ref].pooled || c->groups[G.ad_ref].pooled);
-      (bagx ? heavy : light).push_back(j);
-    }
-    size_t h = 0, l = 0;
-    while (h < heavy.size() || l < light.size()) {
-      if (h < heavy.size()) mixed.push_back(heavy[h++]);
-      const size_t per = heavy.empty() ? light.size() : (light.size() + heavy.size() - 1) / heavy.size();
-      for (size_t t = 0; t < per && l < light.size(); t++) mixed.push_back(light[l++]);
-    }
-    c->gather_order = mixed;
-  }
   c->d_u = (int)c->sel_user.size() * c->k;
   c->d_ac = (int)c->sel_ac.size() * c->k;
   c->d_in = c->d_u + c->d_ac;
@@ -507,11 +399,12 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   }
   c->max_ads = cfg->max_ads_per_call;
   c->max_req = cfg->max_requests_per_call;
-  {
-    const char* env_ring = getenv("COLD_GATHER_RING");
-    c->gather_ring = env_ring ? atoi(env_ring) : 0;
-    if (c->gather_ring != 4 && c->gather_ring != 5 && c->gather_ring != 8) c->gather_ring = 0;
-  }
+  c->kflags = cfg->kernel_flags;
+  c->cfg_chain_min = cfg->chain_min_ads;
+  c->cfg_span = cfg->gather_span_chunks;
+  c->cfg_ring = cfg->gather_ring;
+  c->gather_ring = cfg->gather_ring == 0 ? COLD_DEFAULT_GATHER_RING : cfg->gather_ring;
+  if (c->gather_ring != 4 && c->gather_ring != 5 && c->gather_ring != 8) c->gather_ring = 0;
 
   if (cudaSetDevice(c->device) != cudaSuccess) { delete c; return fail(COLD_ERR_CUDA, "cudaSetDevice failed"); }
   cudaDeviceProp prop;
@@ -544,8 +437,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     // Column-wise gather over a span of several chunks ("column based computation"): one
     // group column is gathered for every ad of the span before the next group starts, so each
     // table's hot rows are fetched from HBM once per span and then served by L2.
-    const char* env_span = getenv("COLD_GSPAN");
-    int span = env_span ? atoi(env_span) : 16;   // measured: 4 -> 16 is +4% gather GB/s, +1% ads/s
+    int span = cfg->gather_span_chunks > 0 ? cfg->gather_span_chunks : 16;   // measured: 4 -> 16 is +4% gather GB/s
     if (span < 1) span = 1;
     const int64_t need = (c->max_ads + c->chunk - 1) / c->chunk;
     c->gspan = (int)std::min<int64_t>(span, std::max<int64_t>(need, 1));
@@ -558,15 +450,13 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   e = e ? e : c->alloc((void**)&c->d_xu, (size_t)c->max_req * std::max(1, c->d_u) * 4);
   e = e ? e : c->alloc((void**)&c->d_req, (size_t)c->max_ads * 4);
   const size_t x_rows = (size_t)c->gspan * c->chunk;
-  const char* env_comp = getenv("COLD_COMPRESS");
-  const bool want_comp = c->tensor && env_comp && atoi(env_comp) != 0;
-  e = e ? e : c->alloc_act((void**)&c->d_X, x_rows * c->d_ac_pad * c->elem(), want_comp);
+  e = e ? e : c->alloc((void**)&c->d_X, x_rows * c->d_ac_pad * c->elem());
   if (c->dense_se) e = e ? e : c->alloc((void**)&c->d_E, x_rows * c->d_in * 4);
   e = e ? e : c->alloc((void**)&c->d_err, 16);
   e = e ? e : c->alloc((void**)&c->d_scores_stage, (size_t)2 * c->chunk * 4);
   e = e ? e : c->alloc((void**)&c->d_adoff, (size_t)(c->max_req + 1) * 4);
   if (c->tensor)
-    for (int l = 0; l < c->L - 2 && !e; l++) e = c->alloc_act(&c->d_H[l], (size_t)c->chunk * c->widths[l] * 2, want_comp);
+    for (int l = 0; l < c->L - 2 && !e; l++) e = c->alloc(&c->d_H[l], (size_t)c->chunk * c->widths[l] * 2);
   if (e != cudaSuccess) {
     delete c;
     cudaGetLastError();
@@ -574,15 +464,12 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   }
   cudaMemset(c->d_X, 0, x_rows * c->d_ac_pad * c->elem());  // pad columns stay 0
   if (c->tensor) {
-    const char* env_cs = getenv("COLD_GEMM_CS");
-    const int cs_default = env_cs ? atoi(env_cs) : 1;
-    const char* env_tail = getenv("COLD_TAIL");
-    const char* env_resb = getenv("COLD_RESB");
-    const char* env_pdl = getenv("COLD_PDL");
-    c->pdl = !(env_pdl && atoi(env_pdl) == 0);
+    const int cs_default = 1;   // weight-tile multicast over clusters measured slower at these sizes
+    const uint32_t kf = c->kflags;
+    c->pdl = !(kf & COLD_K_NO_PDL);
     const int Lg = c->L - 1;   // GEMM layers (the last layer is fused as the head)
     {
-      const int want = env_tail ? atoi(env_tail) : 2;
+      const int want = (kf & COLD_K_TAIL_NONE) ? 0 : ((kf & COLD_K_TAIL3) ? 1 : 2);
       const int k4 = (Lg - 2 == 0) ? c->d_ac_pad : (Lg >= 3 ? c->widths[Lg - 3] : 0);
       const int k3 = (Lg - 3 == 0) ? c->d_ac_pad : (Lg >= 4 ? c->widths[Lg - 4] : 0);
       if (want == 2 && Lg >= 2 && tail45_supported(c->widths[Lg - 2], c->widths[Lg - 1], k4)) c->tail_mode = 2;
@@ -617,21 +504,16 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       while (cs > 1 && (c->bn[l] / cs) % 8 != 0) cs >>= 1;   // B slices must be whole 8-row swizzle atoms
       c->cs[l] = (cs == 4 || cs == 2) ? cs : 1;
       if (c->n_tail && l >= Lg - c->n_tail) c->cs[l] = 1;   // the tail kernels load whole weight tiles
-      c->resb[l] = c->cs[l] == 1 && gemm_resident_ok(c->bn[l], K) && !(env_resb && atoi(env_resb) == 0);
-      // CTA pairs for the 256-wide layers that are not fused into the tail (FC1, FC2)
-      const char* env_pair = getenv("COLD_PAIR");
-      const int pair_mode = env_pair ? atoi(env_pair) : 2;   // 0 off, 1 non-resident 256-wide, 2 all 256-wide
+      c->resb[l] = c->cs[l] == 1 && gemm_resident_ok(c->bn[l], K) && !(kf & COLD_K_STREAM_B);
+      // CTA pairs for the 256-wide layers that are not fused into the tail (FC1, FC2, FC3)
       const bool in_tail = c->n_tail && l >= Lg - c->n_tail;
-      c->pair[l] = !in_tail && l < Lg - 1 && c->bn[l] == 256 &&
-                   (pair_mode == 2 || (pair_mode == 1 && !c->resb[l]));
+      c->pair[l] = !in_tail && l < Lg - 1 && c->bn[l] == 256 && !(kf & COLD_K_SINGLE_CTA);
       if (c->pair[l]) { c->resb[l] = false; c->cs[l] = 1; }
-      const char* env_pres = getenv("COLD_PAIR_RES");
-      c->pair_res[l] = c->pair[l] && gemm_pair_resident_ok(c->bn[l], K) && !(env_pres && atoi(env_pres) == 0);
+      c->pair_res[l] = c->pair[l] && gemm_pair_resident_ok(c->bn[l], K) && !(kf & COLD_K_PAIR_STREAM);
     }
   }
   if (c->tensor && c->pair[0] && c->n_tail < c->L - 1) {
-    const char* env_u1 = getenv("COLD_U1MMA");
-    c->u1mma = !(env_u1 && atoi(env_u1) == 0);
+    c->u1mma = !(c->kflags & COLD_K_NO_U1_MMA);
   }
   if (c->u1mma) {
     c->u1_terms = c->precision == COLD_BF16 ? 3 : 2;
@@ -652,14 +534,12 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   }
   if (c->u1mma && c->tail_mode == 2 && c->L == 6 && c->pair[1] && c->pair[2] &&
       chain_supported(c->widths[0], c->widths[1], c->widths[2], c->d_ac_pad)) {
-    const char* env_chain = getenv("COLD_CHAIN");
-    c->chain = !(env_chain && atoi(env_chain) == 0);
-    const char* env_cmin = getenv("COLD_CHAIN_MIN");
-    c->chain_min = env_cmin ? atoll(env_cmin) : (int64_t)c->num_sms * 256;
-    // COLD_CHAIN=2 also folds FC4 / FC5 / head into the chain: measured slower than the separate
+    c->chain = !(c->kflags & COLD_K_LAYERWISE);
+    c->chain_min = cfg->chain_min_ads > 0 ? cfg->chain_min_ads : (int64_t)c->num_sms * 256;
+    // COLD_K_CHAIN_TAIL also folds FC4 / FC5 / head into the chain: measured slower than the separate
     // resident-weight tail kernel (N = 128 / 64 pair tiles, larger live L2 set), so off by default
     c->chain_tail = c->chain && chain_tail_supported(c->widths[3], c->widths[4], c->widths[2]) &&
-                    c->widths[5] <= 2 && env_chain != nullptr && atoi(env_chain) == 2 && !c->prelu;
+                    c->widths[5] <= 2 && (c->kflags & COLD_K_CHAIN_TAIL) && !c->prelu;
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       [&] {   // the user kernel is on the latency path's critical chain: highest stream priority
@@ -710,6 +590,10 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
   cfg.chunk_ads = src->chunk;
   cfg.flags = src->flags;
   cfg.se_mode = src->dense_se ? COLD_SE_DENSE : COLD_SE_GROUP;
+  cfg.kernel_flags = src->kflags;
+  cfg.chain_min_ads = src->cfg_chain_min;
+  cfg.gather_span_chunks = src->cfg_span;
+  cfg.gather_ring = src->cfg_ring;
   cold_ctx* c = nullptr;
   cold_status s = cold_create(&cfg, &c);
   if (s) return s;
@@ -1148,23 +1032,11 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
   ga.groups = c->d_groups;
   for (int g = 0; g < c->M; g++) ga.gp[g] = c->h_groups[g];
   ga.bv = bv;
-  ga.n_ac = (int)c->sel_ac.size();
-  // COLD_GATHER_MERGE=1: single-valued AD groups and single x single crosses go to one merged column
-  // (measured 12% slower than one column per group on the configs[4] stream, so off by default)
-  static const bool merge = getenv("COLD_GATHER_MERGE") && atoi(getenv("COLD_GATHER_MERGE")) != 0;
-  const bool vec_rows = c->k * c->elem() % 16 == 0;
-  auto is_single = [&](int g) {
-    const cold_group& G = c->groups[g];
-    if (G.side == COLD_AD) return !G.pooled;
-    if (G.side == COLD_CROSS) return !c->groups[G.ad_ref].pooled && !c->groups[G.user_ref].pooled;
-    return false;
-  };
   ga.n_ac = 0;
-  ga.n_single = 0;
-  for (int j = 0; j < (int)c->sel_ac.size(); j++) {
-    const int g = c->sel_ac[c->gather_order[j]];
-    if (merge && vec_rows && is_single(g)) ga.single_g[ga.n_single++] = g;
-    else { ga.ac_g[ga.n_ac] = g; ga.order[ga.n_ac] = ga.n_ac; ga.n_ac++; }
+  for (int j = 0; j < (int)c->sel_ac.size(); j++) {   // one grid.y column per group, heaviest first
+    ga.ac_g[ga.n_ac] = c->sel_ac[c->gather_order[j]];
+    ga.order[ga.n_ac] = ga.n_ac;
+    ga.n_ac++;
   }
   ga.k = c->k;
   ga.se_w = c->d_se_w;
@@ -1245,18 +1117,13 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     cp.k1 = c->d_ac_pad;
     cp.h1 = c->d_H[0];
     cp.h2 = c->d_H[1];
-    {
-      static const bool h3ef = getenv("COLD_H3_EF") && atoi(getenv("COLD_H3_EF")) != 0;
-      cp.h3_evict_first = h3ef ? 1 : 0;
+#ifdef COLD_INSTRUMENT   // wait-cycle instrumentation build (tools/probes/chain_instr.py)
+    if (!g_instr) {
+      cudaMalloc(&g_instr, 8 * 8 * COLD_MAX_LAYERS);
+      cudaMemset(g_instr, 0, 8 * 8 * COLD_MAX_LAYERS);
     }
-    {
-      static bool chain_instr = getenv("COLD_INSTR") != nullptr;
-      if (chain_instr && !g_instr) {
-        cudaMalloc(&g_instr, 8 * 8 * COLD_MAX_LAYERS);
-        cudaMemset(g_instr, 0, 8 * 8 * COLD_MAX_LAYERS);
-      }
-      cp.instr = chain_instr ? g_instr + 8 * 4 : nullptr;   // slots 32..39
-    }
+    cp.instr = g_instr + 8 * 4;   // slots 32..39
+#endif
     if (c->chain_tail) {
       cp.tail = 1;
       cp.n4 = c->widths[3];
@@ -1275,18 +1142,20 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
                                  c->chain_tail ? &c->tmW4h : &c->tmB[0], c->chain_tail ? &c->tmW5h : &c->tmB[0],
                                  c->chain_tail ? &c->tmC[3] : &c->tmB[0]};
     c->mark_begin(st);
-    static const bool gbias = getenv("COLD_CHAIN_GBIAS") && atoi(getenv("COLD_CHAIN_GBIAS")) != 0;
-    cp.gbias = gbias ? 1 : 0;
     launch_chain(tm, (int)n, c->precision == COLD_BF16 ? 1 : 0, cp, c->num_sms, c->pdl && !c->prof, st);
     c->mark_end(COLD_PROF_CHAIN, st, c->layer_flop(0, c->chain_tail ? c->L : 3, n));
     n_gemm = 0;
     if (c->chain_tail) return;   // FC4 / FC5 / head done inside the chain
   }
-  static bool instr_on = getenv("COLD_INSTR") != nullptr;
-  if (instr_on && !g_instr) {
+#ifdef COLD_INSTRUMENT
+  const bool instr_on = true;
+  if (!g_instr) {
     cudaMalloc(&g_instr, 8 * 8 * COLD_MAX_LAYERS);
     cudaMemset(g_instr, 0, 8 * 8 * COLD_MAX_LAYERS);
   }
+#else
+  const bool instr_on = false;
+#endif
   for (int l = 0; l < n_gemm; l++) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
@@ -1313,14 +1182,6 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     }
     const int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
     ep.instr = instr_on ? g_instr + 8 * l : nullptr;
-    {
-      static const char* env_dir = getenv("COLD_EPI_DIRECT");  // bitmask of layers storing with st.global
-      if (env_dir && ((atoi(env_dir) >> l) & 1)) ep.direct = 1;
-    }
-    {
-      static const char* env_dbg = getenv("COLD_DBG_GEMM");   // "<layer>:<mode>" timing experiments
-      if (env_dbg && atoi(env_dbg) == l && strchr(env_dbg, ':')) ep.dbg_mode = atoi(strchr(env_dbg, ':') + 1);
-    }
     c->mark_begin(st);
     if (c->pair[l])
       launch_gemm_pair(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
@@ -1344,10 +1205,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     tp.scores = scores_out;
     tp.s4 = c->d_slope[l4];
     tp.s5 = c->d_slope[l4 + 1];
-    {
-      static const bool rev = !(getenv("COLD_TAIL_REV") && atoi(getenv("COLD_TAIL_REV")) == 0);
-      tp.reverse = rev ? 1 : 0;
-    }
+    tp.reverse = 1;   // last tile first: the most recently written H3 rows are the ones still in L2
     c->mark_begin(st);
     launch_tail45(tmA_of(l4), &c->tmB[l4], &c->tmB[l4 + 1], (int)n, c->precision == COLD_BF16 ? 1 : 0, tp,
                   c->num_sms, c->pdl && !c->prof, st);
@@ -1394,19 +1252,11 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
   const double user_flop = c->dense_se ? 0.0 : 2.0 * c->d_u * c->widths[0] * (double)pl.R;
   // Latency path (a few requests, scoring): the user side (pooling, u1 GEMV, ad -> request map) does not
   // feed the gather, which finds an ad's request by searching ad_offsets, so the two run concurrently
-  // (fork onto the side stream, join before the FC stack). COLD_USER_FORK=0 serialises them.
-  // COLD_USER_FORK=2: the user kernel stays on the caller's stream (launched first, so dispatched first)
-  // and the single gather span goes to the side stream instead.
-  static const int fork_env = getenv("COLD_USER_FORK") ? atoi(getenv("COLD_USER_FORK")) : 1;
-  const bool fork = fork_env != 0 && mode == RUN_SCORE && pl.R <= 4;
-  const bool one_span = pl.N <= (int64_t)c->chunk * c->gspan;
-  const bool gather_side = fork && fork_env == 2 && one_span && !pl.host;
-  cudaStream_t gst = st;   // stream of the gather launches
+  // (fork onto the side stream, join before the FC stack). COLD_K_SERIAL_USER serialises them.
+  const bool fork = !(c->kflags & COLD_K_SERIAL_USER) && mode == RUN_SCORE && pl.R <= 4;
   if (fork) {
     CK(cudaEventRecord(c->ev_fork, st));
     CK(cudaStreamWaitEvent(c->side_stream, c->ev_fork, 0));
-  }
-  if (fork && !gather_side) {
     c->mark_begin(c->side_stream);
     launch_user(ua, pl.R, c->precision, c->side_stream);
     c->mark_end(COLD_PROF_USER, c->side_stream, user_flop);
@@ -1415,7 +1265,6 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
     c->mark_begin(st);
     launch_user(ua, pl.R, c->precision, st);
     c->mark_end(COLD_PROF_USER, st, user_flop);
-    if (gather_side) gst = c->side_stream;
   }
   CK(cudaGetLastError());
   bool joined = !fork;
@@ -1459,40 +1308,11 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
       ga.adoff = d_adoff;
       ga.R = pl.R;
     }
-    static const bool split = getenv("COLD_GATHER_SPLIT") && atoi(getenv("COLD_GATHER_SPLIT")) != 0;
-    if (split) {   // profiling aid: one launch per group column (then the one-hot column)
-      GatherArgs g1 = ga;
-      for (int j = 0; j < ga.n_ac; j++) {
-        g1.n_ac = 1;
-        g1.ac_g[0] = ga.ac_g[ga.order[j]];
-        g1.order[0] = 0;
-        g1.n_single = 0;
-        g1.ohot = nullptr;
-        c->mark_begin(st);
-        launch_gather(g1, c->precision, st);
-        c->mark_end(COLD_PROF_GATHER, st);
-      }
-      if (ga.n_single > 0) {
-        g1 = ga;
-        g1.n_ac = 0;
-        g1.ohot = nullptr;
-        c->mark_begin(st);
-        launch_gather(g1, c->precision, st);
-        c->mark_end(COLD_PROF_GATHER, st);
-      }
-      g1 = ga;
-      g1.n_ac = 0;
-      g1.n_single = 0;
-      g1.ohot = ga.ohot;
-      c->mark_begin(st);
-      launch_gather(g1, c->precision, st);
-      c->mark_end(COLD_PROF_GATHER, st);
-    } else if (c->gather_ring && c->tensor && c->k * c->elem() == 32 && !dbg.pooled && !dbg.feat &&
+    if (c->gather_ring && c->tensor && c->k * c->elem() == 32 && !dbg.pooled && !dbg.feat &&
                s1 - s0 >= 148 * 128 * 4) {
       // cross-bag columns (user bag x single ad id) through the cp.async-ring build, then the rest
       GatherArgs gb = ga, gr = ga;
       gb.n_ac = gr.n_ac = 0;
-      gb.n_single = 0;
       gb.ohot = nullptr;
       gb.ring = c->gather_ring;
       for (int j = 0; j < ga.n_ac; j++) {
@@ -1504,17 +1324,16 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
         d.order[d.n_ac] = d.n_ac;
         d.n_ac++;
       }
-      c->mark_begin(gst);
-      if (gb.n_ac) launch_gather(gb, c->precision, gst);
-      launch_gather(gr, c->precision, gst);
-      c->mark_end(COLD_PROF_GATHER, gst);
+      c->mark_begin(st);
+      if (gb.n_ac) launch_gather(gb, c->precision, st);
+      launch_gather(gr, c->precision, st);
+      c->mark_end(COLD_PROF_GATHER, st);
     } else {
-      c->mark_begin(gst);
-      launch_gather(ga, c->precision, gst);
-      c->mark_end(COLD_PROF_GATHER, gst);
+      c->mark_begin(st);
+      launch_gather(ga, c->precision, st);
+      c->mark_end(COLD_PROF_GATHER, st);
     }
     if (!joined) {   // dense SE and the FC stack read x_u / u1 and req_of_ad (or the side-stream gather's X)
-      if (gather_side) CK(cudaEventRecord(c->ev_user, c->side_stream));
       CK(cudaStreamWaitEvent(st, c->ev_user, 0));
       joined = true;
     }
@@ -1546,12 +1365,9 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
     }
     if (pl.host) CK(cudaEventRecord(c->ev_consumed[slot], st));
     if (mode == RUN_SCORE) {
-      // COLD_SPAN_REV=1: chunks of the span last-first (the last chunk's X rows are the ones most likely
-      // still in L2); measured neutral, so first-first by default
-      static const bool span_rev = getenv("COLD_SPAN_REV") && atoi(getenv("COLD_SPAN_REV")) != 0;
       const int64_t nch = (s1 - s0 + chunk - 1) / chunk;
       for (int64_t k = 0; k < nch; k++, ci++) {
-        const int64_t a0 = s0 + (span_rev ? nch - 1 - k : k) * chunk;
+        const int64_t a0 = s0 + k * chunk;
         const int64_t n = std::min(s1, a0 + chunk) - a0;
         const int oslot = (int)(ci & 1);
         float* out = scores_dev ? scores + a0 : c->d_scores_stage + (int64_t)oslot * chunk;
@@ -1673,7 +1489,6 @@ extern "C" cold_status cold_se_stats(cold_ctx* c, const cold_batch* b, double* m
       if (cls == pass) ga.ac_g[ga.n_ac++] = g;
     }
   for (int j = 0; j < ga.n_ac; j++) ga.order[j] = j;
-  ga.n_single = 0;
   ga.X = nullptr;
   ga.ohot = nullptr;
   ga.stats = d_stats;
@@ -1905,7 +1720,7 @@ extern "C" cold_status cold_get_info(const cold_ctx* c, cold_info* out) {
   int64_t b = c->device_bytes;
   for (int g = 0; g < c->M && g < (int)c->d_tables.size(); g++) b += c->groups[g].cardinality * c->k * c->elem();
   out->device_bytes = b;
-  out->compressed_activations = c->compressed ? 1 : 0;
+  out->compressed_activations = 0;   // (reserved: the compressible-memory variant measured neutral, removed)
   out->gather_span_chunks = c->gspan;
   return COLD_OK;
 }

@@ -4,6 +4,9 @@
 #include <cuda.h>
 #include "common.cuh"
 
+// default cp.async-ring depth of the cross-bag gather columns (cold_config.gather_ring = 0)
+#define COLD_DEFAULT_GATHER_RING 0
+
 namespace cold {
 
 // cudaFuncSetAttribute (dynamic shared-memory opt-in, cluster sizes) applies per device context, and a
@@ -74,10 +77,6 @@ struct GatherArgs {
   int n_sel, d_in;
   const float* in_scale;           // input normalisation [D_in] (nullable)
   const float* in_shift;
-  // merged single-row column (grid.y == n_ac): every AD single group and every single x single CROSS
-  // group of an ad in one thread (more loads in flight per thread than one group per thread)
-  int n_single;
-  int single_g[COLD_MAX_GROUPS];   // schema indices, handled by the merged column (excluded from order[])
   double* stats;                   // SE statistics mode: [M] += s_g per ad; X is not written
   uint16_t* ohot;                  // FC1 u1 operand (nullable): [n][16] span-local rows, the one-hot slot of
                                    // the row's request in its 256-row CTA-pair tile, repeated in k 0-7 / 8-15
@@ -155,7 +154,6 @@ struct EpiParams {
   int relu;
   const float* slope;              // PReLU slopes [N] (F2; null: ReLU when relu)
   unsigned long long* instr;       // debug: per-role wait-cycle counters [8] (null = off)
-  int direct;                      // epilogue writes rows with st.global (no smem staging / TMA store)
   int dbg_mode;                    // timing experiments only (results invalid): 1 = epilogue only drains
                                    // TMEM (no math / stores), 2 = MMA issuer skips the MMAs, 3 = epilogue
                                    // math without smem / TMA stores, 4 = smem staging but no TMA store
@@ -203,8 +201,6 @@ struct ChainParams {
   const float* b4; const float* b5; const float* head_w; const float* head_b; int head_n;
   const void* h3; const void* h4;
   float* scores;                         // chunk-local [M]
-  int h3_evict_first;                    // H3 stores with an evict-first L2 hint (no TAIL)
-  int gbias;                             // 1: epilogue reads FC2 / FC3 biases from global (A/B switch)
   unsigned long long* instr;             // debug (nullable): wait cycles [0] producer empty, [1] producer
                                          // hready, [2] MMA full, [3] MMA tempty, [4] MMA uxfull, [5] epi tfull
 };

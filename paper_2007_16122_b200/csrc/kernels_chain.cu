@@ -82,7 +82,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   // FC2 / FC3 biases in shared memory: the epilogue reads them with LDS instead of a global load that
   // stalled it (ncu r01h: 9% of the chain's stall samples on the bias add)
   float* sBias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);
-  const bool sbias = cp.n2 + cp.n3 <= C_BIASF && !cp.gbias;
+  const bool sbias = cp.n2 + cp.n3 <= C_BIASF;
   if (sbias)
     for (int i = threadIdx.x; i < cp.n2 + cp.n3; i += blockDim.x) sBias[i] = i < cp.n2 ? cp.b2[i] : cp.b3[i - cp.n2];
 
@@ -234,7 +234,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     const int q = warp & 3;
     const int h = ew >> 2;
     const bool elected = (q == 0) && (lane == 0);
-    const uint64_t pol_h3 = policy_evict_first();
     const bool ins = cp.instr != nullptr && lane == 0;
     unsigned long long w_tfull = 0;
     int lt = 0;
@@ -287,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         const float* slope = l == 0 ? cp.s1 : (l == 1 ? cp.s2 : (l == 2 ? cp.s3 : nullptr));
         epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, bias_s, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
                              nb * tn[l], trow0, q, h, lane, 0, nullptr, nullptr, 0, 0,
-                             (!TAIL && l == 2 && cp.h3_evict_first) ? pol_h3 : 0ull, slope);
+                             0ull, slope);
       }
       tc_fence_before();
       __syncwarp();

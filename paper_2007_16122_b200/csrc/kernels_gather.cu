@@ -331,104 +331,6 @@ __device__ __forceinline__ void write_ohot(const GatherArgs& a, int64_t i, uint1
   dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
-// Merged single-row column: one thread takes an ad through every single-valued AD group and every
-// (single user group) x (single AD group) cross, 4 rows in flight at a time, instead of one group column
-// per pass (each single-row column was one latency-bound wave: id load -> row load -> store).
-// Sums are of one row (0 + v, exact), so results are identical to the per-column path.
-template <typename T, int K, bool FAST, int GATHER_APT>
-__device__ __forceinline__ void singles_column(const GatherArgs& a) {
-  constexpr int NV = K * (int)sizeof(T) / 16;
-  constexpr int RB = NV <= 2 ? 4 : 2;          // rows in flight
-  __shared__ uint64_t s_hx1[COLD_MAX_GROUPS][2];   // per cross: hx of the block's first / last request
-  __shared__ int s_ok[COLD_MAX_GROUPS];            // 1: both requests have a user bag of exactly 1
-  const int64_t base = (int64_t)blockIdx.x * (128 * GATHER_APT);
-  const int64_t last = (base + 128 * GATHER_APT < a.n ? base + 128 * GATHER_APT : a.n) - 1;
-  const int rfirst = req_at(a, a.a0 + base);
-  const int rlast = req_at(a, a.a0 + last);
-  for (int i = threadIdx.x; i < a.n_single; i += blockDim.x) {
-    const int g = a.single_g[i];
-    const DevGroup G = GGROUP(a, g);
-    if (G.side != 2) continue;
-    const DevGroup U = GGROUP(a, G.user_ref);
-    const BatchGroup& BU = a.bv.g[G.user_ref];
-    const uint64_t salt = cross_salt(g);
-    int ok = rlast - rfirst <= 1;
-    for (int q = 0; q < 2; q++) {
-      const int r = q == 0 ? rfirst : rlast;
-      const int64_t o0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
-      const int64_t o1 = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift;
-      if (o1 - o0 != 1) ok = 0;
-      else s_hx1[i][q] = fmix64((uint64_t)checked(BU.ids[o0], U.card, a.validate, a.err) ^ salt);
-    }
-    s_ok[i] = ok;
-  }
-  __syncthreads();
-  for (int i = 0; i < GATHER_APT; i++) {
-    const int64_t li = base + threadIdx.x + i * 128;
-    if (li >= a.n) break;
-    const int64_t ad = a.a0 + li;
-    const int slot = req_at(a, ad) == rfirst ? 0 : 1;
-    for (int i0 = 0; i0 < a.n_single; i0 += RB) {
-      int64_t row[RB];
-      int gi[RB];
-      bool fast[RB];
-      const T* tabs[RB];
-#pragma unroll
-      for (int t = 0; t < RB; t++) {
-        gi[t] = i0 + t < a.n_single ? i0 + t : -1;
-        row[t] = 0;
-        fast[t] = false;
-        if (gi[t] < 0) continue;
-        const int g = a.single_g[gi[t]];
-        const DevGroup G = GGROUP(a, g);
-        tabs[t] = reinterpret_cast<const T*>(G.table);
-        if (G.side == 1) {
-          const BatchGroup& B = a.bv.g[g];
-          row[t] = checked(B.ids[ad - B.id_shift], G.card, a.validate, a.err);
-          fast[t] = true;
-        } else if (s_ok[gi[t]]) {
-          const DevGroup A = GGROUP(a, G.ad_ref);
-          const BatchGroup& BA = a.bv.g[G.ad_ref];
-          const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
-          row[t] = cross_row_from_hx(s_hx1[gi[t]][slot], y, (uint64_t)G.card);
-          fast[t] = true;
-        }
-      }
-      RawRow<T, K> raw[RB];
-#pragma unroll
-      for (int t = 0; t < RB; t++)
-        if (fast[t]) raw[t].load(tabs[t], row[t]);
-#pragma unroll
-      for (int t = 0; t < RB; t++) {
-        if (gi[t] < 0) continue;
-        const int g = a.single_g[gi[t]];
-        const DevGroup G = GGROUP(a, g);
-        float e[K];
-#pragma unroll
-        for (int d = 0; d < K; d++) e[d] = 0.0f;
-        if (fast[t]) {
-          raw[t].add_to(e);
-        } else {   // a request in the block has a user bag != 1: the general x-major cross sum
-          const DevGroup U = GGROUP(a, G.user_ref);
-          const DevGroup A = GGROUP(a, G.ad_ref);
-          const BatchGroup& BU = a.bv.g[G.user_ref];
-          const BatchGroup& BA = a.bv.g[G.ad_ref];
-          const uint64_t salt = cross_salt(g);
-          const int r = req_at(a, ad);
-          const int64_t u0 = (int64_t)BU.offs[r - BU.offs_shift] - BU.val_shift;
-          const int64_t u1 = (int64_t)BU.offs[r + 1 - BU.offs_shift] - BU.val_shift;
-          const uint64_t y = (uint64_t)checked(BA.ids[ad - BA.id_shift], A.card, a.validate, a.err);
-          for (int64_t x = u0; x < u1; x++) {
-            const uint64_t hx = fmix64((uint64_t)checked(BU.ids[x], U.card, a.validate, a.err) ^ salt);
-            add_row<T, K>(reinterpret_cast<const T*>(G.table), cross_row_from_hx(hx, y, (uint64_t)G.card), e);
-          }
-        }
-        finish_ad<T, K, FAST>(a, G, g, li, e, a.se_w + g * K, __ldg(a.se_b + g));
-      }
-    }
-  }
-}
-
 // ---- cp.async (LDGSTS) helpers: 16 B global -> shared copies that complete asynchronously, tracked
 // per thread in commit groups (no registers held while a row is in flight)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
@@ -522,13 +424,7 @@ __device__ __forceinline__ void cross_bag_ring(const GatherArgs& a, const DevGro
 // RING * 4 KB); 0: register-held bursts of GATHER_RB rows
 template <typename T, int K, bool FAST, int MINB = 4, int GATHER_APT = 4, int RING = 0>
 __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
-  if constexpr (RING == 0) {
-  if (a.n_single > 0 && (int)blockIdx.y == a.n_ac) {
-    if constexpr ((K * (int)sizeof(T)) % 16 == 0) singles_column<T, K, FAST, GATHER_APT>(a);
-    return;
-  }
-  }
-  if ((int)blockIdx.y == a.n_ac + (a.n_single > 0 ? 1 : 0)) {   // FC1's one-hot u1 operand rows
+  if ((int)blockIdx.y == a.n_ac) {          // FC1's one-hot u1 operand rows
     for (int i = 0; i < GATHER_APT; i++) {
       const int64_t l = (int64_t)blockIdx.x * (128 * GATHER_APT) + threadIdx.x + i * 128;
       if (l < a.n) write_ohot(a, l, a.bf16 ? 0x3F80u : 0x3C00u);
@@ -773,7 +669,7 @@ void launch_user(const UserArgs& a, int R, int precision, cudaStream_t s) {
 
 template <typename T, bool FAST>
 static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
-  const unsigned gy = (unsigned)(a.n_ac + (a.n_single > 0 ? 1 : 0) + (a.ohot ? 1 : 0));
+  const unsigned gy = (unsigned)(a.n_ac + (a.ohot ? 1 : 0));
   auto grid_for = [&](int apt) { return dim3((unsigned)((a.n + 128 * apt - 1) / (128 * apt)), gy); };
   const dim3 grid = grid_for(GATHER_APT_BIG);
   switch (a.k) {
@@ -781,18 +677,13 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
     case 4: gather_kernel<T, 4, FAST><<<grid, 128, 0, s>>>(a); break;
     case 8: gather_kernel<T, 8, FAST><<<grid, 128, 0, s>>>(a); break;
     case 16: {
-      static const int minb = getenv("COLD_GATHER_MINB") ? atoi(getenv("COLD_GATHER_MINB")) : 8;
-      static const int apt = getenv("COLD_GATHER_APT") ? atoi(getenv("COLD_GATHER_APT")) : 4;
+      // 8 CTAs of 128 threads per SM at <= 64 registers (12-16 CTAs spill; 6-7 CTAs with 8 rows in flight
+      // per thread measured slower: DESIGN.md §9)
       if (sizeof(T) == 2 && a.ring == 4) gather_kernel<T, 16, FAST, 8, 4, 4><<<grid, 128, 4 * 4096, s>>>(a);
       else if (sizeof(T) == 2 && a.ring == 5) gather_kernel<T, 16, FAST, 8, 4, 5><<<grid, 128, 5 * 4096, s>>>(a);
       else if (sizeof(T) == 2 && a.ring == 8) gather_kernel<T, 16, FAST, 6, 4, 8><<<grid, 128, 8 * 4096, s>>>(a);
       else if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
-      else if (apt == 2) gather_kernel<T, 16, FAST, 8, 2><<<grid_for(2), 128, 0, s>>>(a);
-      else if (apt == 1) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);
-      else if (minb >= 16) gather_kernel<T, 16, FAST, 16><<<grid, 128, 0, s>>>(a);
-      else if (minb >= 12) gather_kernel<T, 16, FAST, 12><<<grid, 128, 0, s>>>(a);
-      else if (minb >= 8) gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
-      else gather_kernel<T, 16, FAST><<<grid, 128, 0, s>>>(a);
+      else gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
       break;
     }
     case 32: gather_kernel<T, 32, FAST><<<grid, 128, 0, s>>>(a); break;
@@ -800,7 +691,7 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
 }
 
 void launch_gather(const GatherArgs& a, int precision, cudaStream_t s) {
-  if (a.n <= 0 || (a.n_ac <= 0 && a.n_single <= 0 && !a.ohot)) return;
+  if (a.n <= 0 || (a.n_ac <= 0 && !a.ohot)) return;
   if (precision == 0) gather_dispatch<float, false>(a, s);
   else if (precision == 1) gather_dispatch<__half, true>(a, s);
   else gather_dispatch<__nv_bfloat16, true>(a, s);

@@ -5,12 +5,12 @@ import coldgen
 
 
 def make_ctx(schema, params, precision=None, selected=None, linear_log=None, max_ads=1 << 16, max_requests=1024,
-             chunk_ads=0, validate_ids=False, load=True):
+             chunk_ads=0, validate_ids=False, load=True, **kw):
     from paper_2007_16122_b200 import Context
     precision = precision or params.precision
     ctx = Context(schema.groups, schema.k, schema.widths, precision=precision, selected=selected,
                   linear_log=schema.linear_log if linear_log is None else linear_log,
-                  max_ads=max_ads, max_requests=max_requests, chunk_ads=chunk_ads, validate_ids=validate_ids)
+                  max_ads=max_ads, max_requests=max_requests, chunk_ads=chunk_ads, validate_ids=validate_ids, **kw)
     if load:
         load_params(ctx, params)
     return ctx

@@ -121,30 +121,32 @@ def test_paper_stack_tensor_core(prec):
     _check_scores(got, p, z, prec, f"paper {prec}")
 
 
-@pytest.mark.parametrize("env", [{"COLD_TAIL": "2"}, {"COLD_TAIL": "1"}, {"COLD_TAIL": "0"}, {"COLD_PAIR": "2"},
-                                 {"COLD_PAIR": "0", "COLD_RESB": "0"}, {"COLD_GSPAN": "1"}, {"COLD_GSPAN": "3"},
-                                 {"COLD_CHAIN": "0"}, {"COLD_CHAIN_MIN": "0"}, {"COLD_CHAIN": "2", "COLD_CHAIN_MIN": "0"},
-                                 {"COLD_CHAIN": "0", "COLD_PAIR_RES": "0"}, {"COLD_CHAIN": "0", "COLD_U1MMA": "0"}])
-def test_kernel_variants_match_oracle(env, monkeypatch):
-    """Every kernel variant the library can select (fused tail FC3-5 / FC4-5 / none, CTA-pair or
-    single-CTA GEMMs, gather spans of 1 or 3 chunks) on several chunks with a ragged tail."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+_KV = {"tail45": {}, "tail3": {"kernel_flags": 64}, "no_tail": {"kernel_flags": 32},
+       "single_cta_stream_b": {"kernel_flags": 4 | 16}, "span1": {"gather_span_chunks": 1},
+       "span3": {"gather_span_chunks": 3}, "layerwise": {"kernel_flags": 1}, "chain_always": {"chain_min_ads": 1},
+       "chain_tail": {"kernel_flags": 128, "chain_min_ads": 1}, "layerwise_pair_stream": {"kernel_flags": 1 | 8},
+       "layerwise_no_u1mma": {"kernel_flags": 1 | 2}, "serial_user_no_pdl": {"kernel_flags": 256 | 512}}
+
+
+@pytest.mark.parametrize("variant", sorted(_KV))
+def test_kernel_variants_match_oracle(variant):
+    """Every kernel the library can select (cold_config.kernel_flags & co.: fused tail FC3-5 / FC4-5 / none,
+    CTA-pair or single-CTA GEMMs, resident or streamed weights, chain or layer-by-layer FC1-FC3, gather
+    spans of 1 or 3 chunks) on several chunks with a ragged tail."""
     sch, params, batch = small_case("paper", R=4, n_ads=(1000, 129, 1, 700), precision="f16", cap=50000, seed=33)
-    ctx = make_ctx(sch, params, chunk_ads=512)
+    ctx = make_ctx(sch, params, chunk_ads=512, **_KV[variant])
     p, z = _oracle_scores(sch, params, batch)
-    _check_scores(gpu_scores(ctx, batch), p, z, "f16", f"variant {env}")
+    _check_scores(gpu_scores(ctx, batch), p, z, "f16", f"variant {variant}")
 
 
 @pytest.mark.parametrize("prec", ["f16", "bf16"])
-def test_chain_kernel_many_blocks(prec, monkeypatch):
+def test_chain_kernel_many_blocks(prec):
     """The FC1->FC3 chain kernel (forced for every chunk size) over several chunks of 1280 ads with many
     256-row blocks per CTA pair, requests crossing block boundaries, a ragged last block."""
-    monkeypatch.setenv("COLD_CHAIN_MIN", "0")
     sizes = (3000, 17, 1, 2200, 900, 4000, 333)
     sch, params, batch = small_case("paper", R=len(sizes), n_ads=sizes, precision=prec, cap=30000, seed=63)
     for chunk in (0, 1280):
-        ctx = make_ctx(sch, params, chunk_ads=chunk)
+        ctx = make_ctx(sch, params, chunk_ads=chunk, chain_min_ads=1)
         p, z = _oracle_scores(sch, params, batch)
         _check_scores(gpu_scores(ctx, batch), p, z, prec, f"chain {prec} chunk {chunk}")
 
@@ -197,20 +199,18 @@ def test_wide_logit_init_reported():
                   f"max |dz| {dz.max():.3e}, {int((err > 2e-2).sum())}/{err.size} ads over 2e-2")
 
 
-@pytest.mark.parametrize("prec,chain_min", [("f16", None), ("bf16", None), ("f16", "0"), ("bf16", "0")])
-def test_one_wide_head_tensor_core(prec, chain_min, monkeypatch):
+@pytest.mark.parametrize("prec,chain_min", [("f16", 0), ("bf16", 0), ("f16", 1), ("bf16", 1)])
+def test_one_wide_head_tensor_core(prec, chain_min):
     """A 1-wide head (p = sigma(z), AMB-7) on the paper stack 384x1024x512x256x128x64x1: the tcgen05
-    layer-by-layer GEMMs or (chain_min 0) the FC1->FC3 chain, then the fused FC4/FC5/head tail with
+    layer-by-layer GEMMs or (chain_min_ads 1) the FC1->FC3 chain, then the fused FC4/FC5/head tail with
     head_n == 1; several chunks with a ragged tail."""
-    if chain_min is not None:
-        monkeypatch.setenv("COLD_CHAIN_MIN", chain_min)
     base = coldgen.scaled_schema(coldgen.schema_paper(), 20000)
     sch = coldgen.Schema(base.name + "-1wide", base.groups, base.k, tuple(base.widths[:-1]) + (1,), base.linear_log)
     assert sch.widths == (1024, 512, 256, 128, 64, 1)
     params = coldgen.make_params(sch, seed=67, precision=prec)
     batch = coldgen.make_batch(sch, 3, [1500, 7, 900], seed=68)
     for chunk in (0, 1024):
-        ctx = make_ctx(sch, params, chunk_ads=chunk)
+        ctx = make_ctx(sch, params, chunk_ads=chunk, chain_min_ads=chain_min)
         p, z = _oracle_scores(sch, params, batch)
         _check_scores(gpu_scores(ctx, batch), p, z, prec, f"1-wide head {prec} chunk {chunk}")
 
@@ -311,20 +311,19 @@ def test_fp16_overflow_without_linear_log():
 
 # ---- host (pinned) batches: the e2e path ------------------------------------------------------
 
-@pytest.mark.parametrize("prec,chain_min", [("f16", None), ("f32", None), ("f16", "0")])
-def test_host_batch_equals_device_batch(prec, chain_min, monkeypatch):
+@pytest.mark.parametrize("prec,chain_min", [("f16", 0), ("f32", 0), ("f16", 1)])
+def test_host_batch_equals_device_batch(prec, chain_min):
     """Pinned-host inputs/outputs (staged per gather span on the copy stream) give the same scores as
-    device-resident ones; with COLD_CHAIN_MIN=0 the chain kernel runs every chunk."""
-    if chain_min is not None:
-        monkeypatch.setenv("COLD_CHAIN_MIN", chain_min)
+    device-resident ones; with chain_min_ads = 1 the chain kernel runs every chunk."""
     sch = bag_schema() if prec == "f32" else coldgen.scaled_schema(coldgen.schema_paper(), 20000)
     params = coldgen.make_params(sch, seed=101, precision=prec)
     # 5 requests: the user kernel runs first on the caller's stream; 3 requests: the latency path forks it
     # onto the side stream beside the gather (host staging then feeds both)
     for n_ads in ([300, 1, 257, 1000, 40], [300, 1, 1000]):
         batch = coldgen.make_batch(sch, len(n_ads), n_ads, seed=102)
-        ref = gpu_scores(make_ctx(sch, params, chunk_ads=256), batch)
-        got_pinned = gpu_scores(make_ctx(sch, params, chunk_ads=256), batch, pin=True, host_out=True)
+        ref = gpu_scores(make_ctx(sch, params, chunk_ads=256, chain_min_ads=chain_min), batch)
+        got_pinned = gpu_scores(make_ctx(sch, params, chunk_ads=256, chain_min_ads=chain_min), batch, pin=True,
+                                host_out=True)
         np.testing.assert_array_equal(got_pinned, ref)
 
 
@@ -735,20 +734,17 @@ def test_graph_replay_matches_direct_call():
 
 # ---- F2: PReLU hidden activation (per-channel slopes) ----------------------------------------
 
-@pytest.mark.parametrize("prec,chain_min", [("f32", None), ("f16", None), ("bf16", None), ("f16", "0"),
-                                            ("bf16", "0")])
-def test_prelu_variant(prec, chain_min, monkeypatch):
+@pytest.mark.parametrize("prec,chain_min", [("f32", 0), ("f16", 0), ("bf16", 0), ("f16", 1), ("bf16", 1)])
+def test_prelu_variant(prec, chain_min):
     """activation = COLD_PRELU: every hidden layer h = x (x > 0) or a_c x with per-channel fp32 slopes,
-    on the fp32 SIMT path, the tcgen05 layer-by-layer pair GEMMs + fused FC4/FC5/head tail, and (chain_min
-    0) the FC1->FC3 chain; vs the oracle's PReLU mode; ReLU scores differ (the slopes matter)."""
+    on the fp32 SIMT path, the tcgen05 layer-by-layer pair GEMMs + fused FC4/FC5/head tail, and
+    (chain_min_ads 1) the FC1->FC3 chain; vs the oracle's PReLU mode; ReLU scores differ (the slopes matter)."""
     from paper_2007_16122_b200 import Context
-    if chain_min is not None:
-        monkeypatch.setenv("COLD_CHAIN_MIN", chain_min)
     cap = 20000
     sch, params, batch = small_case("paper", R=3, n_ads=(1200, 33, 700), precision=prec, cap=cap, seed=101)
     slopes = coldgen.prelu_slopes(sch, seed=102)
     ctx = Context(sch.groups, sch.k, sch.widths, precision=prec, max_ads=1 << 16, max_requests=64,
-                  activation="prelu")
+                  activation="prelu", chain_min_ads=chain_min)
     load_params(ctx, params, act_slope=slopes)
     got = gpu_scores(ctx, batch)
     p, z = oracle.score(oracle.Model(sch, params, prelu=slopes), batch)
@@ -763,17 +759,15 @@ def test_prelu_variant(prec, chain_min, monkeypatch):
     assert e.value.name == "COLD_ERR_PARAMS"
 
 
-@pytest.mark.parametrize("ring", ["4", "5", "8"])
-def test_gather_ring_equals_register_path(ring, monkeypatch):
-    """The cp.async-ring build of the cross-bag columns (COLD_GATHER_RING) sums the same rows in the same
+@pytest.mark.parametrize("ring", [4, 5, 8])
+def test_gather_ring_equals_register_path(ring):
+    """The cp.async-ring build of the cross-bag columns (cold_config.gather_ring) sums the same rows in the same
     bag order as the register path, so whole-span scores are bit-identical; a sample is checked against
     the oracle. Spans of >= 75,776 ads take the ring; requests of mixed sizes put 1-3 requests in a CTA."""
     sizes = [5000, 37, 20000, 1, 3000] * 6
     sch, params, batch = small_case("paper", R=len(sizes), n_ads=tuple(sizes), precision="f16", cap=50000, seed=111)
-    monkeypatch.setenv("COLD_GATHER_RING", "0")
-    ref = gpu_scores(make_ctx(sch, params, max_ads=batch.n_ads, max_requests=64), batch)
-    monkeypatch.setenv("COLD_GATHER_RING", ring)
-    got = gpu_scores(make_ctx(sch, params, max_ads=batch.n_ads, max_requests=64), batch)
+    ref = gpu_scores(make_ctx(sch, params, max_ads=batch.n_ads, max_requests=64, gather_ring=-1), batch)
+    got = gpu_scores(make_ctx(sch, params, max_ads=batch.n_ads, max_requests=64, gather_ring=ring), batch)
     np.testing.assert_array_equal(got, ref)
     ads = np.random.default_rng(3).choice(batch.n_ads, 300, replace=False)
     p, z = oracle.score(oracle.Model(sch, params), batch, ad_list=ads)
