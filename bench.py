@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--topk", type=int, default=500)
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--cap", type=int, default=0, help="cap cardinalities (quick runs only)")
+    ap.add_argument("--kernel-flags", type=int, default=0, help="cold_config.kernel_flags (A/B runs)")
+    ap.add_argument("--gather-ring", type=int, default=0, help="cold_config.gather_ring (A/B runs)")
+    ap.add_argument("--gather-span", type=int, default=0, help="cold_config.gather_span_chunks (A/B runs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -868,7 +871,8 @@ def main():
     batch = coldgen.make_batch(sch, reqs, args.ads, seed=args.seed + 1)
     N = batch.n_ads
     ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, device=local, max_ads=N,
-                  max_requests=max(batch.R, 1), chunk_ads=args.chunk, se_mode="dense" if args.se_dense else "group")
+                  max_requests=max(batch.R, 1), chunk_ads=args.chunk, se_mode="dense" if args.se_dense else "group",
+                  kernel_flags=args.kernel_flags, gather_ring=args.gather_ring, gather_span_chunks=args.gather_span)
     load_ctx_params(ctx, params, dense_se_params(sch, args.seed + 17) if args.se_dense else None)
     K = args.topk
     step = RankStep(ctx, batch, K, world, r_pad, dev)

@@ -194,10 +194,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       int s = 0, lt = 0, fc1_t = 0;
       uint32_t ph = 0;
       const bool ins = cp.instr != nullptr;
-      unsigned long long w_full = 0, w_tempty = 0, w_ux = 0;
+      unsigned long long w_full = 0, w_tempty = 0, w_ux = 0, wl_full[3] = {0, 0, 0}, wl_te[3] = {0, 0, 0};
+      const long long t_begin = clock64();
       for_tasks([&](int l, int j, int nb) {
         const uint32_t idesc = l < 3 ? id256 : id_tail[l - 3];
         const int acc = lt & 1;
+        const unsigned long long te0 = w_tempty, fu0 = w_full;
         cwait(&tempty[acc], ((lt >> 1) & 1) ^ 1, w_tempty, ins);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * C_BN;
@@ -225,8 +227,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         }
         umma_commit_pair(&tfull[acc]);
         lt++;
+        if (ins && l < 3) { wl_full[l] += w_full - fu0; wl_te[l] += w_tempty - te0; }
       });
-      if (ins) { atomicAdd(cp.instr + 2, w_full); atomicAdd(cp.instr + 3, w_tempty); atomicAdd(cp.instr + 4, w_ux); }
+      if (ins) {
+        atomicAdd(cp.instr + 2, w_full); atomicAdd(cp.instr + 3, w_tempty); atomicAdd(cp.instr + 4, w_ux);
+        atomicAdd(cp.instr + 6, (unsigned long long)(clock64() - t_begin));
+        for (int l = 0; l < 3; l++) { atomicAdd(cp.instr + 8 + l, wl_full[l]); atomicAdd(cp.instr + 11 + l, wl_te[l]); }
+      }
     }
   } else {
     // ===== epilogue warps 2..9 (both CTAs): TMEM lane quadrant q, column half h =====

@@ -1,5 +1,5 @@
-"""Run a short scoring loop with COLD_INSTR=1 and print the GEMM pipeline wait cycles per layer.
-usage (GPU): COLD_INSTR=1 python tools/instr.py [requests]"""
+"""Run a short scoring loop in the -DCOLD_INSTRUMENT build and print the GEMM pipeline wait cycles per layer.
+usage (GPU): bash tools/ab_build.sh instr -DCOLD_INSTRUMENT; COLD_LIB_AB=$PWD/paper_2007_16122_b200/_ab/instr.so python tools/instr.py [requests]"""
 import ctypes as C
 import os
 import sys

@@ -1,4 +1,4 @@
-"""chain_kernel wait cycles per role (COLD_INSTR=1): kcycles per CTA over one scoring call."""
+"""chain_kernel wait cycles per role (-DCOLD_INSTRUMENT build, tools/ab_build.sh): kcycles per CTA over one scoring call."""
 import ctypes as C
 import os
 import sys
@@ -32,10 +32,14 @@ e1.record()
 torch.cuda.synchronize()
 L.cold_debug_instr(buf.ctypes.data, len(buf))
 ms = e0.elapsed_time(e1)
-v = buf[32:38].astype(np.float64)
-names = ["prod_empty", "prod_hready", "mma_full", "mma_tempty", "mma_uxfull", "epi_tfull(sum of 8 warps)"]
+v = buf[32:46].astype(np.float64)
+names = ["prod_empty", "prod_hready", "mma_full", "mma_tempty", "mma_uxfull", "epi_tfull(sum of 8 warps)",
+         "mma_issuer_elapsed", "-", "mma_full_fc1", "mma_full_fc2", "mma_full_fc3", "mma_tempty_fc1", "mma_tempty_fc2",
+         "mma_tempty_fc3"]
 ctas = 148.0
 print(f"call {ms:.2f} ms = {ms * 1.92e3:.0f} kcycles at 1.92 GHz; per CTA (leader-only for MMA rows: /74):")
 for i, n in enumerate(names):
-    div = 74.0 if i in (2, 3, 4) else ctas
+    if n == "-":
+        continue
+    div = 74.0 if i in (2, 3, 4) or i >= 6 else ctas
     print(f"  {n}: {v[i] / div / 1e3:.1f} kcycles")

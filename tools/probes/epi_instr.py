@@ -1,4 +1,4 @@
-"""Epilogue section timing of the CTA-pair GEMMs (COLD_INSTR=1): per epilogue warp, kcycles spent in
+"""Epilogue section timing of the CTA-pair GEMMs (-DCOLD_INSTRUMENT build, tools/ab_build.sh): per epilogue warp, kcycles spent in
 [TMEM load+wait, math+pack, staging-buffer wait, smem write+fence, store issue] over one scoring call."""
 import ctypes as C
 import os
