@@ -67,6 +67,11 @@ def parse():
     ap.add_argument("--vps-dim", type=int, default=64)
     ap.add_argument("--se-dense", action="store_true",
                     help="F2: the dense SE reading (AMB-1, P:229-234 Doc B) on the same workload")
+    ap.add_argument("--serve", action="store_true",
+                    help="serving path: the request-coalescing server (cold_server_*) under open-loop Poisson "
+                         "arrivals of configs[1]-shaped requests; p50/p99 end-to-end latency and usable rate")
+    ap.add_argument("--serve-requests", type=int, default=6000)
+    ap.add_argument("--serve-batch", type=int, default=16, help="max requests coalesced into one call")
     ap.add_argument("--latency-sweep", action="store_true",
                     help="SURVEY §8(d) C2: p50/p95/p99 vs N, multi-stream serving (S contexts sharing one "
                          "parameter copy), fp32 / fp16 / bf16 ads/s (the analogue of Table tab:qps_cuda)")
@@ -566,6 +571,75 @@ def graph_latency(ctx, sch, n, count, K, seed, dist="uniform", dev=None):
                       "Lindley-recursion open-loop Poisson arrivals over these measured service times (P:442 rule)"}
 
 
+def serve_rates(srv, hb, n_ads, rates, seed=11):
+    """Open-loop Poisson arrivals at each offered rate (requests/s): the C-side submit enqueues request i
+    at its arrival time; latency = completion (dispatcher publishes the top-K to host memory) - arrival,
+    host CLOCK_MONOTONIC. Returns one row per rate."""
+    rows = []
+    R = len(hb.ad_offsets_host) - 1
+    for lam in rates:
+        gaps = np.random.default_rng(seed).exponential(1e9 / lam, R)
+        arrival = (time.monotonic_ns() + 5_000_000 + np.cumsum(gaps)).astype(np.int64)
+        _, _, done = srv.submit(hb, arrival_ns=arrival)
+        calls, reqs = srv.drain()
+        lat = (done - arrival) / 1e6
+        span = (done.max() - arrival.min()) / 1e9
+        rows.append({"offered_rps": float(lam), "offered_ads_per_s": float(lam * n_ads),
+                     "achieved_ads_per_s": float(R * n_ads / span), "p50_ms": float(np.percentile(lat, 50)),
+                     "p99_ms": float(np.percentile(lat, 99)), "mean_ms": float(lat.mean()),
+                     "failed": int((done < 0).sum())})
+    return rows
+
+
+def run_serve(args):
+    """Serving path (P:298 / P:690-692: the paper's GPU was idle between small queries until MPS let them
+    share it; "usable QPS"): configs[1]-shaped requests (1 user x 4000 ads, S-paper, fp16, top-500)
+    arrive as an open-loop Poisson stream from the host; the cold_server dispatcher coalesces the requests
+    that arrived while the GPU was busy into one cold_score_batch + cold_topk call. Latency is end to end
+    (host ids in, top-K back in host memory). Reports the closed-loop capacity, p50/p99 per offered rate,
+    and the usable rate at p99 <= 1 ms / 10 ms."""
+    import torch
+    from paper_2007_16122_b200 import Batch, Context, Server
+    torch.cuda.set_device(0)
+    sch = schema_for(args)
+    n = 4000
+    K = args.topk
+    params = coldgen.make_params(sch, seed=args.seed, precision=args.precision)
+    B = args.serve_batch
+    ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, max_ads=B * n, max_requests=B)
+    load_ctx_params(ctx, params)
+    lb = coldgen.make_batch(sch, range(4 * 10**7, 4 * 10**7 + args.serve_requests), n, seed=args.seed + 7)
+    hb = Batch(lb.ad_offsets, lb.ids, lb.offs)
+    srv = Server(ctx, max_batch_requests=B, max_batch_ads=B * n, top_k=K)
+    srv.submit(hb)                        # warm-up (sizes the pinned staging and the library's buffers)
+    srv.drain()
+    t0 = time.monotonic_ns()
+    _, _, done = srv.submit(hb)           # closed loop: everything queued at once
+    calls, reqs = srv.drain()
+    cap_s = (done.max() - t0) / 1e9
+    capacity_rps = args.serve_requests / cap_s
+    rates = [capacity_rps * f for f in (0.1, 0.25, 0.5, 0.7, 0.85, 0.95)]
+    rows = serve_rates(srv, hb, n, rates)
+    usable = {}
+    for lim in (1.0, 10.0):
+        ok = [r["offered_rps"] for r in rows if r["p99_ms"] <= lim and not r["failed"]]
+        usable[f"usable_rps_p99_le_{int(lim)}ms"] = max(ok) if ok else 0.0
+        usable[f"usable_ads_per_s_p99_le_{int(lim)}ms"] = (max(ok) if ok else 0.0) * n
+    srv.close()
+    ctx.close()
+    line = {"metric": METRIC, "value": capacity_rps * n, "unit": "ads/s", "n_gpus": 1, "dtype": args.precision,
+            "data": "synthetic (seeded ids, tables, weights)",
+            "config": {"workload": f"serving: {args.serve_requests} requests x {n} ads (BASELINE configs[1] shape), "
+                                   f"S-paper, top-{K}; request-coalescing server, <= {B} requests per call; "
+                                   f"open-loop Poisson arrivals from the host, end-to-end latency"},
+            "closed_loop": {"ads_per_s": capacity_rps * n, "requests_per_s": capacity_rps, "calls": calls,
+                            "requests_per_call": reqs / max(calls, 1)},
+            "open_loop": rows, **usable,
+            "timing": "host CLOCK_MONOTONIC: arrival = the submit time the C replay loop waited for; completion = "
+                      "when the dispatcher published the request's top-K to host memory"}
+    print(json.dumps(line), flush=True)
+
+
 def run_latency_sweep(args):
     """SURVEY §8(d) C2 measurements on one B200 (S-paper schema, LL on, K = 500):
     (1) per-request latency vs N (one stream, requests back to back, device events);
@@ -844,6 +918,9 @@ def main():
         return
     if args.latency_sweep:
         run_latency_sweep(args)
+        return
+    if args.serve:
+        run_serve(args)
         return
     if args.vps:
         run_vps(args)

@@ -313,6 +313,39 @@ cold_status cold_debug_features(cold_ctx* ctx, const cold_batch* batch, float* o
 cold_status cold_debug_rows(cold_ctx* ctx, const cold_batch* batch, int32_t group, int64_t* rows_out,
                             int32_t max_rows, void* stream);
 
+/* ---- request-coalescing server (serving path; §3.3 and P:690-692: after Float16 each query was
+ * too small to fill the GPU and the paper added MPS; here requests that arrive while the GPU is busy are
+ * concatenated into one cold_score_batch + cold_topk call, with a dispatcher thread owning the ctx) ---- */
+
+typedef struct cold_server cold_server;   /* opaque */
+
+typedef struct {
+  int32_t max_batch_requests;    /* requests coalesced into one call, 1 .. ctx max_requests_per_call */
+  int64_t max_batch_ads;         /* ads in one call, 1 .. ctx max_ads_per_call (also the largest request) */
+  int32_t top_k;                 /* K of every request (each request needs >= K ads) */
+  int32_t max_wait_us;           /* an idle GPU waits up to this long for a fuller batch (0: dispatch at once) */
+} cold_server_config;
+
+/* Starts the dispatcher thread. The ctx must be loaded and must not be used by anyone else until
+ * cold_server_destroy. Errors: COLD_ERR_CAPACITY (limits above the ctx's), COLD_ERR_K_RANGE, COLD_ERR_OOM. */
+cold_status cold_server_create(cold_ctx* ctx, const cold_server_config* config, cold_server** out);
+/* Completes queued requests, then stops the thread and frees the server (not the ctx). */
+void cold_server_destroy(cold_server* server);
+/* Enqueue the R requests of a HOST batch (cold_batch layout, offs_host required for bag groups). With
+ * arrival_ns ([R], CLOCK_MONOTONIC nanoseconds) the call enqueues request r at arrival_ns[r] (spinning
+ * until then: an open-loop replay); NULL enqueues all now. Request r's top-K (positions within the
+ * request, keys; as cold_topk) is written to idx_out / key_out [r * K .. r * K + K) (host), after which
+ * done_ns[r] receives the completion time (CLOCK_MONOTONIC ns; -1 if its call failed), stored with
+ * release semantics; done_ns[r] is 0 until then. The batch arrays and the outputs must stay valid until
+ * cold_server_drain returns. Errors (nothing enqueued): COLD_ERR_INVALID_ARG, COLD_ERR_K_RANGE (a request
+ * with fewer than K ads), COLD_ERR_CAPACITY (a request larger than max_batch_ads). */
+cold_status cold_server_submit(cold_server* server, const cold_batch* requests, const int64_t* arrival_ns,
+                               int32_t* idx_out, float* key_out, int64_t* done_ns);
+/* Waits until every submitted request is complete; returns the first error a coalesced call hit (its
+ * requests got done_ns = -1; cold_last_error of the dispatcher thread is not visible here) or COLD_OK.
+ * batches_out / requests_out (nullable): calls issued and requests they carried so far. */
+cold_status cold_server_drain(cold_server* server, int64_t* batches_out, int64_t* requests_out);
+
 const char* cold_status_string(cold_status s);
 const char* cold_last_error(void);
 

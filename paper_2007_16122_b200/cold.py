@@ -28,7 +28,8 @@ STATUS = {0: "COLD_OK", 1: "COLD_ERR_INVALID_ARG", 2: "COLD_ERR_SHAPE", 3: "COLD
 EXPORTS = ["cold_create", "cold_destroy", "cold_load_params", "cold_score_batch", "cold_score_request",
            "cold_topk", "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
            "cold_status_string", "cold_last_error", "cold_profile", "cold_profile_read", "cold_se_stats",
-           "cold_select_groups", "cold_merge_topk", "cold_vps_score", "cold_ctx_clone"]
+           "cold_select_groups", "cold_merge_topk", "cold_vps_score", "cold_ctx_clone", "cold_server_create",
+           "cold_server_destroy", "cold_server_submit", "cold_server_drain"]
 PROF_KINDS = 23
 PROF_USER, PROF_GATHER, PROF_TOPK, PROF_FC, PROF_SE_DENSE = 0, 1, 2, 3, 3 + 16
 PROF_CHAIN, PROF_TAIL, PROF_MLP_F32 = 20, 21, 22
@@ -67,6 +68,11 @@ class cold_params(C.Structure):
                 ("in_scale", C.c_void_p), ("in_shift", C.c_void_p),
                 ("se_w_dense", C.c_void_p), ("se_b_dense", C.c_void_p),
                 ("act_slope", C.POINTER(C.c_void_p))]
+
+
+class cold_server_config(C.Structure):
+    _fields_ = [("max_batch_requests", C.c_int32), ("max_batch_ads", C.c_int64), ("top_k", C.c_int32),
+                ("max_wait_us", C.c_int32)]
 
 
 class cold_batch(C.Structure):
@@ -112,6 +118,12 @@ def lib() -> C.CDLL:
         L.cold_vps_score.argtypes = [C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]
         L.cold_ctx_clone.argtypes = [C.c_void_p, C.POINTER(C.c_void_p)]
+        L.cold_server_create.argtypes = [C.c_void_p, C.POINTER(cold_server_config), C.POINTER(C.c_void_p)]
+        L.cold_server_destroy.argtypes = [C.c_void_p]
+        L.cold_server_destroy.restype = None
+        L.cold_server_submit.argtypes = [C.c_void_p, C.POINTER(cold_batch), C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p]
+        L.cold_server_drain.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.cold_profile.argtypes = [C.c_void_p, C.c_int32]
         L.cold_profile_read.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.cold_status_string.restype = C.c_char_p
@@ -120,7 +132,8 @@ def lib() -> C.CDLL:
         for f in ["cold_create", "cold_load_params", "cold_score_batch", "cold_score_request", "cold_topk",
                   "cold_get_info", "cold_debug_pooled", "cold_debug_features", "cold_debug_rows",
                   "cold_profile", "cold_profile_read", "cold_se_stats", "cold_select_groups",
-                  "cold_merge_topk", "cold_vps_score", "cold_ctx_clone"]:
+                  "cold_merge_topk", "cold_vps_score", "cold_ctx_clone", "cold_server_create",
+                  "cold_server_submit", "cold_server_drain"]:
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -344,3 +357,49 @@ def vps_score(ad_vecs, vec_dtype: str, user_vecs, ad_ids, ad_offsets, ad_offsets
     _check(lib().cold_vps_score(_addr(ad_vecs), PRECISION[vec_dtype], int(ad_vecs.shape[0]), d, _addr(user_vecs),
                                 _addr(ad_ids), _addr(ad_offsets), aoh.ctypes.data, len(aoh) - 1, _addr(scores),
                                 _stream_handle(stream)))
+
+
+class Server:
+    """cold_server: a dispatcher thread that coalesces the requests submitted while the GPU is busy into
+    one cold_score_batch + cold_topk call (include/cold.h). Owns the ctx while it lives."""
+
+    def __init__(self, ctx: Context, max_batch_requests: int, max_batch_ads: int, top_k: int, max_wait_us: int = 0):
+        cfg = cold_server_config(max_batch_requests, max_batch_ads, top_k, max_wait_us)
+        self.srv = C.c_void_p()
+        self.top_k = top_k
+        self._ctx = ctx
+        self._keep = []
+        _check(lib().cold_server_create(ctx.ctx, C.byref(cfg), C.byref(self.srv)))
+
+    def submit(self, batch: "Batch", arrival_ns=None):
+        """Enqueue the R requests of a host batch (Batch.from_numpy(..., device=None) / pin=True), at
+        arrival_ns[r] (CLOCK_MONOTONIC, time.monotonic_ns()) when given. Returns numpy (idx [R, K],
+        key [R, K], done_ns [R]) filled asynchronously; valid after drain()."""
+        R = len(batch.ad_offsets_host) - 1
+        K = self.top_k
+        idx = np.zeros((R, K), np.int32)
+        key = np.zeros((R, K), np.float32)
+        done = np.zeros(R, np.int64)
+        arr = None if arrival_ns is None else np.ascontiguousarray(arrival_ns, np.int64)
+        self._keep.append((batch, idx, key, done, arr))
+        _check(lib().cold_server_submit(self.srv, C.byref(batch.c), None if arr is None else arr.ctypes.data,
+                                        idx.ctypes.data, key.ctypes.data, done.ctypes.data))
+        return idx, key, done
+
+    def drain(self):
+        """Wait for every submitted request; returns (coalesced calls, requests they carried)."""
+        b, r = C.c_int64(), C.c_int64()
+        _check(lib().cold_server_drain(self.srv, C.byref(b), C.byref(r)))
+        self._keep.clear()
+        return b.value, r.value
+
+    def close(self):
+        if self.srv:
+            lib().cold_server_destroy(self.srv)
+            self.srv = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

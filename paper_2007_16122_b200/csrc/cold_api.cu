@@ -1707,6 +1707,15 @@ extern "C" cold_status cold_profile_read(cold_ctx* c, double* total_ms, int64_t*
   return COLD_OK;
 }
 
+extern "C" void cold_ctx_describe(const cold_ctx* c, int* num_groups, const cold_group** groups, int* max_requests,
+                                  int64_t* max_ads, int* device) {
+  *num_groups = c->M;
+  *groups = c->groups.data();
+  *max_requests = c->max_req;
+  *max_ads = c->max_ads;
+  *device = c->device;
+}
+
 extern "C" cold_status cold_get_info(const cold_ctx* c, cold_info* out) {
   if (!c || !out) return fail(COLD_ERR_INVALID_ARG, "null");
   out->version = c->version;

@@ -29,8 +29,11 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
                                                int tile_row0, int q, int h, int lane, int dbg = 0,
                                                unsigned long long* tacc = nullptr, void* gout = nullptr,
                                                int ldo = 0, int M = 0, uint64_t store_policy = 0,
-                                               const float* __restrict__ slope = nullptr) {
-  const uint32_t sbuf = smem_u32(group_buf) + (uint32_t)q * EPI_WIDE_BOX;
+                                               const float* __restrict__ slope = nullptr,
+                                               uint8_t* group_buf2 = nullptr, int* box_ctr = nullptr) {
+  // group_buf2 / box_ctr (optional): a second staging box; consecutive 64-column chunks alternate between
+  // the two so the math of chunk c + 1 overlaps the TMA store of chunk c (box_ctr: running chunk count of
+  // the group, identical in its four warps)
   const bool elected = (q == 0) && (lane == 0);
   // debug timing (tacc != null, lane 0): cycles in [0] TMEM load+wait, [1] math+pack, [2] wait for the
   // staging buffer, [3] smem writes + fence, [4] store issue
@@ -113,9 +116,17 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
       tick(4);
       continue;
     }
-    if (elected) bulk_wait_read<0>();     // the group's previous box has left shared memory
+    uint8_t* gbuf = group_buf;
+    if (group_buf2) {
+      gbuf = (*box_ctr & 1) ? group_buf2 : group_buf;
+      ++*box_ctr;
+      if (elected) bulk_wait_read<1>();   // the store issued two chunks ago (same box) has left smem
+    } else {
+      if (elected) bulk_wait_read<0>();   // the group's previous box has left shared memory
+    }
     named_bar_sync(1 + h, 128);
     tick(2);
+    const uint32_t sbuf = smem_u32(gbuf) + (uint32_t)q * EPI_WIDE_BOX;
     const uint32_t rowp = sbuf + (uint32_t)lane * 128u;
 #pragma unroll
     for (int j = 0; j < 8; j++)
@@ -125,8 +136,8 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
     tick(3);
     if (elected && dbg != 4) {
       // dbg 6 (timing experiment): every box to the same L2-resident location (no DRAM write traffic)
-      if (store_policy) tma_store_2d_hint(tmC, group_buf, col0, tile_row0, store_policy);
-      else tma_store_2d(tmC, group_buf, dbg == 6 ? 0 : col0, dbg == 6 ? 0 : tile_row0);
+      if (store_policy) tma_store_2d_hint(tmC, gbuf, col0, tile_row0, store_policy);
+      else tma_store_2d(tmC, gbuf, dbg == 6 ? 0 : col0, dbg == 6 ? 0 : tile_row0);
       bulk_commit();
     }
     tick(4);

@@ -35,7 +35,12 @@ constexpr int C_THREADS = 64 + 32 * C_EPI_WARPS;
 constexpr int C_A_BYTES = BM * BK * 2;                 // 16 KB: own 128 rows x 64 K
 constexpr int C_B_BYTES = (C_BN / 2) * BK * 2;         // 16 KB: own half of the 256-row weight tile
 constexpr int C_STAGE_BYTES = C_A_BYTES + C_B_BYTES;
-constexpr int C_OUT_BYTES = 2 * EPI_GROUP_BOX;          // two 4-warp groups x 16 KB
+#ifdef COLD_CHAIN_EPI_DB
+constexpr int C_OUT_BOXES = 4;   // A/B build: two 16 KB boxes per group (one pipeline stage fewer): measured neutral
+#else
+constexpr int C_OUT_BOXES = 2;   // one 16 KB staging box per 4-warp group
+#endif
+constexpr int C_OUT_BYTES = C_OUT_BOXES * EPI_GROUP_BOX;
 constexpr int C_UXA = BM * 32, C_UXB = (C_BN / 2) * 16 * 4, C_UX_BUF = C_UXA + C_UXB, C_NUX = 2;
 constexpr int C_BIASF = 1024;                          // FC2 + FC3 biases staged in smem (n2 + n3 <= 1024)
 constexpr int C_BIAS_BYTES = C_BIASF * 4;
@@ -243,7 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     const bool elected = (q == 0) && (lane == 0);
     const bool ins = cp.instr != nullptr && lane == 0;
     unsigned long long w_tfull = 0;
-    int lt = 0;
+    int lt = 0, box_ctr = 0;
     for_tasks([&](int l, int j, int nb) {
       const int pm = pair + j * npairs;
       const int acc = lt & 1;
@@ -293,7 +298,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         const float* slope = l == 0 ? cp.s1 : (l == 1 ? cp.s2 : (l == 2 ? cp.s3 : nullptr));
         epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, bias_s, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
                              nb * tn[l], trow0, q, h, lane, 0, nullptr, nullptr, 0, 0,
-                             0ull, slope);
+                             0ull, slope, C_OUT_BOXES == 4 ? sOut + (2 + h) * EPI_GROUP_BOX : nullptr, &box_ctr);
       }
       tc_fence_before();
       __syncwarp();

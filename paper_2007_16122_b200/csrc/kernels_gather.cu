@@ -437,6 +437,10 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
   // is halved for twice the resident warps)
   constexpr int GATHER_RB = (NV <= 2 ? 8 : (NV == 4 ? 4 : 2)) / (MINB >= 12 ? 4 : (MINB >= 8 ? 2 : 1));
   __shared__ uint64_t s_hx[2][HX_HALF];
+#ifdef COLD_GATHER_PAD_SMEM   // A/B: the static shared footprint of the round-1 build (5376 B)
+  __shared__ uint8_t s_pad[1280];
+  if (a.n < 0) s_pad[threadIdx.x] = 1;
+#endif
   const int j = a.order[blockIdx.y];
   const int g = a.ac_g[j];
 #ifdef COLD_GATHER_SW_SMEM   // A/B build: the group's SE weights staged in shared memory (a barrier at CTA start)
@@ -683,7 +687,15 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
       else if (sizeof(T) == 2 && a.ring == 5) gather_kernel<T, 16, FAST, 8, 4, 5><<<grid, 128, 5 * 4096, s>>>(a);
       else if (sizeof(T) == 2 && a.ring == 8) gather_kernel<T, 16, FAST, 6, 4, 8><<<grid, 128, 8 * 4096, s>>>(a);
       else if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
-      else gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
+      else {
+#ifdef COLD_GATHER_CARVEOUT   // A/B: explicit shared-memory carveout preference for the main build
+        static DevOnce co;
+        if (co.first())
+          cudaFuncSetAttribute(gather_kernel<T, 16, FAST, 8>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               COLD_GATHER_CARVEOUT);
+#endif
+        gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
+      }
       break;
     }
     case 32: gather_kernel<T, 32, FAST><<<grid, 128, 0, s>>>(a); break;

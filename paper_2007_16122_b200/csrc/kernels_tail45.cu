@@ -34,7 +34,7 @@ constexpr int Q_H4_BYTES = (Q_N4 / BK) * Q_H4_ATOM;     // 32 KB per buffer
 constexpr int Q_SMEM = Q_W4_BYTES + Q_W5_BYTES + Q_STAGES * Q_A_BYTES + 2 * Q_H4_BYTES + 1024 + 256;
 static_assert(Q_SMEM <= 232448, "tail45 shared memory");
 
-template <bool BF16>
+template <bool BF16, bool PRELU>
 __global__ void __launch_bounds__(Q_THREADS, 1)
     tail45_kernel(const __grid_constant__ CUtensorMap tmA4, const __grid_constant__ CUtensorMap tmB4,
                   const __grid_constant__ CUtensorMap tmB5, int M, TailParams tp) {
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
         const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + 8 * j));
         const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + 8 * j + 4));
         uint4 w;
-        if (tp.s4) {   // PReLU (F2)
+        if constexpr (PRELU) {   // PReLU (F2)
           const float4 a0 = __ldg(reinterpret_cast<const float4*>(tp.s4 + 64 * h + 8 * j));
           const float4 a1 = __ldg(reinterpret_cast<const float4*>(tp.s4 + 64 * h + 8 * j + 4));
           w.x = Pack<BF16>::two(prelu(__uint_as_float(v[o + 0]) + b0.x, a0.x), prelu(__uint_as_float(v[o + 1]) + b0.y, a0.y));
@@ -211,7 +211,9 @@ __global__ void __launch_bounds__(Q_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 64; i++) {
           const float x5 = __uint_as_float(i < 32 ? v0[i] : v1[i - 32]) + __ldg(tp.b5 + i);
-          const float a = tp.s5 ? prelu(x5, __ldg(tp.s5 + i)) : fmaxf(x5, 0.0f);
+          float a;
+          if constexpr (PRELU) a = prelu(x5, __ldg(tp.s5 + i));
+          else a = fmaxf(x5, 0.0f);
           z0 = fmaf(__ldg(tp.head_w + i), a, z0);
           if (tp.head_n == 2) z1 = fmaf(__ldg(tp.head_w + Q_N5 + i), a, z1);
         }
@@ -247,9 +249,11 @@ bool tail45_supported(int n4, int n5, int k4) { return n4 == Q_N4 && n5 == Q_N5 
 cudaError_t launch_tail45(const CUtensorMap* tmA4, const CUtensorMap* tmB4, const CUtensorMap* tmB5, int M, int bf16,
                           const TailParams& tp, int num_sms, bool pdl, cudaStream_t s) {
   if (M <= 0) return cudaSuccess;
-  auto kern = bf16 ? tail45_kernel<true> : tail45_kernel<false>;
-  static DevOnce attr[2];
-  if (attr[bf16 ? 1 : 0].first()) {
+  const bool pr = tp.s4 != nullptr;
+  auto kern = bf16 ? (pr ? tail45_kernel<true, true> : tail45_kernel<true, false>)
+                   : (pr ? tail45_kernel<false, true> : tail45_kernel<false, false>);
+  static DevOnce attr[4];
+  if (attr[(bf16 ? 2 : 0) + (pr ? 1 : 0)].first()) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q_SMEM);
   }
   const int tiles = (M + BM - 1) / BM;

@@ -772,3 +772,38 @@ def test_gather_ring_equals_register_path(ring):
     ads = np.random.default_rng(3).choice(batch.n_ads, 300, replace=False)
     p, z = oracle.score(oracle.Model(sch, params), batch, ad_list=ads)
     _check_scores(got[ads], p, z, "f16", f"ring {ring}")
+
+
+# ---- serving: the request-coalescing server (cold_server_*) ----------------------------------
+
+def test_server_coalesced_results_equal_direct_calls():
+    """Requests submitted together are coalesced into calls of <= 4 requests; each request's top-K equals
+    the oracle's sort of the scores a direct call gives (requests are independent), including
+    with paced (open-loop) arrivals; errors are reported before anything is enqueued."""
+    import time
+    from paper_2007_16122_b200 import Batch, ColdError, Server
+    sizes = [700, 1500, 3000, 650, 2222, 901, 1000, 1777, 2500, 612, 800, 999]
+    sch, params, batch = small_case("paper", R=len(sizes), n_ads=tuple(sizes), precision="f16", cap=20000, seed=121)
+    K = 100
+    ref = gpu_scores(make_ctx(sch, params), batch)
+    ctx = make_ctx(sch, params, max_ads=8192, max_requests=8)
+    srv = Server(ctx, max_batch_requests=4, max_batch_ads=8192, top_k=K)
+    hb = Batch(batch.ad_offsets, batch.ids, batch.offs)
+    idx, key, done = srv.submit(hb)
+    calls, reqs = srv.drain()
+    assert reqs == len(sizes) and 3 <= calls <= len(sizes)
+    assert np.all(done > 0)
+    oidx, okey = oracle.topk_batch(ref.astype(np.float64), batch.ad_offsets, K)
+    np.testing.assert_array_equal(idx, oidx)
+    np.testing.assert_array_equal(key.astype(np.float64), okey)
+    t0 = time.monotonic_ns() + 2_000_000
+    arrival = t0 + np.arange(len(sizes), dtype=np.int64) * 200_000        # one request every 0.2 ms
+    idx2, key2, done2 = srv.submit(hb, arrival_ns=arrival)
+    srv.drain()
+    np.testing.assert_array_equal(idx2, oidx)
+    assert np.all(done2 >= arrival)
+    small = coldgen.make_batch(sch, 1, [50], seed=3)                       # fewer ads than K
+    with pytest.raises(ColdError) as e:
+        srv.submit(Batch(small.ad_offsets, small.ids, small.offs))
+    assert e.value.name == "COLD_ERR_K_RANGE"
+    srv.close()
