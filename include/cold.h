@@ -130,8 +130,9 @@ typedef struct {
   int64_t chain_min_ads;         /* chunks of fewer ads run FC1..FC3 layer by layer (the chain needs >= 2
                                     256-row blocks per CTA pair to fill the GPU); 0 = default (256 x SMs),
                                     1 = the chain for every chunk */
-  int32_t gather_ring;           /* cross-bag gather columns through a cp.async ring of this depth (4, 5 or
-                                    8 rows per thread); 0 = default, -1 = register-held row bursts */
+  int32_t gather_ring;           /* cross-bag gather columns (user bag x single ad id): 0 = default, their own
+                                    launch with register-held row bursts; -1 = one launch for every column;
+                                    4, 5 or 8 = their own launch through a cp.async ring of that depth */
 } cold_config;
 
 enum { COLD_SE_GROUP = 0, COLD_SE_DENSE = 1 };

@@ -403,8 +403,10 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
   c->cfg_chain_min = cfg->chain_min_ads;
   c->cfg_span = cfg->gather_span_chunks;
   c->cfg_ring = cfg->gather_ring;
-  c->gather_ring = cfg->gather_ring == 0 ? COLD_DEFAULT_GATHER_RING : cfg->gather_ring;
-  if (c->gather_ring != 4 && c->gather_ring != 5 && c->gather_ring != 8) c->gather_ring = 0;
+  // 0 (default): cross-bag columns in their own register-burst launch; -1: one launch for all columns;
+  // 4 / 5 / 8: cross-bag columns through a cp.async ring of that depth (measured slower: DESIGN.md §9)
+  c->gather_ring = cfg->gather_ring;
+  if (c->gather_ring != -1 && c->gather_ring != 4 && c->gather_ring != 5 && c->gather_ring != 8) c->gather_ring = 0;
 
   if (cudaSetDevice(c->device) != cudaSuccess) { delete c; return fail(COLD_ERR_CUDA, "cudaSetDevice failed"); }
   cudaDeviceProp prop;
@@ -1308,13 +1310,13 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
       ga.adoff = d_adoff;
       ga.R = pl.R;
     }
-    if (c->gather_ring && c->tensor && c->k * c->elem() == 32 && !dbg.pooled && !dbg.feat &&
-               s1 - s0 >= 148 * 128 * 4) {
-      // cross-bag columns (user bag x single ad id) through the cp.async-ring build, then the rest
+    if (c->gather_ring != -1 && c->tensor && c->k * c->elem() == 32 && !dbg.pooled && !dbg.feat &&
+        s1 - s0 >= 148 * 128 * 4) {
+      // cross-bag columns (user bag x single ad id) in the bag-only build, then the rest
       GatherArgs gb = ga, gr = ga;
       gb.n_ac = gr.n_ac = 0;
       gb.ohot = nullptr;
-      gb.ring = c->gather_ring;
+      gb.ring = c->gather_ring > 0 ? c->gather_ring : -1;
       for (int j = 0; j < ga.n_ac; j++) {
         const int g = ga.ac_g[ga.order[j]];
         const cold_group& G = c->groups[g];

@@ -4,8 +4,6 @@
 #include <cuda.h>
 #include "common.cuh"
 
-// default cp.async-ring depth of the cross-bag gather columns (cold_config.gather_ring = 0)
-#define COLD_DEFAULT_GATHER_RING 0
 
 namespace cold {
 
@@ -86,8 +84,8 @@ struct GatherArgs {
   float* E;                        // dense SE (nullable): [n][lde] fp32 pre-SE ê (after linear_log) at
   int lde;                         //   column sel_pos * k; the gate runs in se_dense_kernel
   DevGroup gp[COLD_MAX_GROUPS];    // copy of groups[0..M) in the parameters (read via the constant bank)
-  int ring;                        // > 0: every column is a cross-bag column (user bag x single ad id),
-                                   // gathered through a `ring`-deep cp.async ring (kernels_gather.cu)
+  int ring;                        // != 0: every column is a cross-bag column (user bag x single ad id), for
+                                   // the bag-only build: -1 register bursts, > 0 a `ring`-deep cp.async ring
   int search_req;                  // 1: request of an ad by binary search of adoff (req_of_ad not yet written)
   const int32_t* adoff; int R;     // call-global ad offsets [R+1]
 };

@@ -420,8 +420,10 @@ __device__ __forceinline__ void cross_bag_ring(const GatherArgs& a, const DevGro
 }
 
 // APT: ads per thread (4 for large spans; 1 for small batches, where per-thread serial work is the latency)
-// RING > 0: cross-bag columns stream their rows through a RING-deep cp.async ring (dynamic smem
-// RING * 4 KB); 0: register-held bursts of GATHER_RB rows
+// RING == 0: every column kind (one launch per span). RING != 0: a build launched over the cross-bag
+// columns only (no AD-group / single-row code in it, so the register allocation serves the bag loop):
+// RING == -1 holds GATHER_RB rows per burst in registers, RING > 0 streams them through a RING-deep
+// cp.async ring (dynamic smem RING * 4 KB)
 template <typename T, int K, bool FAST, int MINB = 4, int GATHER_APT = 4, int RING = 0>
 __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
   if ((int)blockIdx.y == a.n_ac) {          // FC1's one-hot u1 operand rows
@@ -683,7 +685,8 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
     case 16: {
       // 8 CTAs of 128 threads per SM at <= 64 registers (12-16 CTAs spill; 6-7 CTAs with 8 rows in flight
       // per thread measured slower: DESIGN.md §9)
-      if (sizeof(T) == 2 && a.ring == 4) gather_kernel<T, 16, FAST, 8, 4, 4><<<grid, 128, 4 * 4096, s>>>(a);
+      if (a.ring == -1) gather_kernel<T, 16, FAST, 8, 4, -1><<<grid, 128, 0, s>>>(a);
+      else if (sizeof(T) == 2 && a.ring == 4) gather_kernel<T, 16, FAST, 8, 4, 4><<<grid, 128, 4 * 4096, s>>>(a);
       else if (sizeof(T) == 2 && a.ring == 5) gather_kernel<T, 16, FAST, 8, 4, 5><<<grid, 128, 5 * 4096, s>>>(a);
       else if (sizeof(T) == 2 && a.ring == 8) gather_kernel<T, 16, FAST, 6, 4, 8><<<grid, 128, 8 * 4096, s>>>(a);
       else if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path

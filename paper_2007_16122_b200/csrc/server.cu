@@ -66,17 +66,18 @@ struct Pinned {
 
 struct Slot {
   std::vector<ReqRec> recs;
-  std::vector<Pinned> ids, offs;           // per group
-  Pinned ao;                               // [B + 1] ad offsets
-  std::vector<const int32_t*> ids_ptr, offs_ptr, offs_host;
+  Pinned h_in;                             // one contiguous pinned image of the batch: ao | per group offs, ids
+  void* d_in = nullptr;                    // its device copy (one H2D per call)
+  size_t d_in_cap = 0;
+  std::vector<const int32_t*> ids_dev, offs_dev, offs_host;
+  const int32_t* ao_host = nullptr;
+  const int32_t* ao_dev = nullptr;
   float* d_scores = nullptr;
-  int32_t* d_ao = nullptr;
   int32_t* d_idx = nullptr;
   float* d_key = nullptr;
   Pinned h_res;                            // [B * K] idx then [B * K] key
   cudaEvent_t done = nullptr;
   bool inflight = false;
-  cold_status status = COLD_OK;
 };
 
 }  // namespace
@@ -91,6 +92,8 @@ struct cold_server {
   std::mutex m;
   std::condition_variable cv, cv_drain;
   std::deque<ReqRec> q;
+  std::atomic<int64_t> queued{0};          // q.size(), readable without the lock (the idle spin)
+  std::atomic<bool> stopping{false};
   int64_t submitted = 0, completed = 0;
   bool stop = false;
   cold_status first_error = COLD_OK;
@@ -103,64 +106,91 @@ struct cold_server {
   void run();
 };
 
-// concatenate the slot's requests into one host batch (pinned), columnar per group as cold_batch expects
+// concatenate the slot's requests into one batch: a single pinned image [ad offsets | per group: offsets,
+// ids] (16 B aligned segments), copied to the device with ONE cudaMemcpyAsync; the call then takes the
+// device-batch path (no per-group staging copies inside the library), with host copies of the offsets
+// from the pinned image
 cold_status cold_server::assemble(Slot& s) {
   const int B = (int)s.recs.size();
   const int M = (int)groups.size();
-  if (!s.ao.reserve(sizeof(int32_t) * (B + 1))) return COLD_ERR_OOM;
-  int32_t* ao = (int32_t*)s.ao.p;
-  ao[0] = 0;
-  for (int i = 0; i < B; i++) ao[i + 1] = ao[i] + s.recs[i].n;
-  s.ids.resize(M);
-  s.offs.resize(M);
-  s.ids_ptr.assign(M, nullptr);
-  s.offs_ptr.assign(M, nullptr);
-  s.offs_host.assign(M, nullptr);
+  auto al = [](size_t x) { return (x + 15) / 16 * 16; };
+  // sizes
+  int64_t n_ads = 0;
+  for (const ReqRec& q : s.recs) n_ads += q.n;
+  std::vector<size_t> off_bytes(M, 0), id_bytes(M, 0);
+  size_t total = al(sizeof(int32_t) * (B + 1));
   for (int g = 0; g < M; g++) {
     const cold_group& G = groups[g];
-    if (G.side == COLD_CROSS) continue;
-    if (!s.recs[0].b->ids[g]) continue;          // a group no request carries (unselected, not crossed)
+    if (G.side == COLD_CROSS || !s.recs[0].b->ids[g]) continue;
     if (G.side == COLD_USER || G.pooled) {
-      // CSR bags: offsets over requests (USER) or ads (AD pooled), ids concatenated in order
-      const int rows = G.side == COLD_USER ? B : ao[B];
+      const int64_t rows = G.side == COLD_USER ? B : n_ads;
       size_t nid = 0;
       for (const ReqRec& q : s.recs) {
-        const int32_t* o = q.b->offs_host ? q.b->offs_host[g] : nullptr;
-        if (!o) return COLD_ERR_INVALID_ARG;
+        const int32_t* o = q.b->offs_host[g];
         const int32_t* aoq = q.b->ad_offsets_host;
         const int lo = G.side == COLD_USER ? q.r : aoq[q.r], hi = G.side == COLD_USER ? q.r + 1 : aoq[q.r + 1];
         nid += (size_t)(o[hi] - o[lo]);
       }
-      if (!s.offs[g].reserve(sizeof(int32_t) * (rows + 1)) || !s.ids[g].reserve(sizeof(int32_t) * (nid + 1)))
-        return COLD_ERR_OOM;
-      int32_t* oo = (int32_t*)s.offs[g].p;
-      int32_t* ii = (int32_t*)s.ids[g].p;
-      int row = 0;
+      off_bytes[g] = al(sizeof(int32_t) * (rows + 1));
+      id_bytes[g] = al(sizeof(int32_t) * std::max<size_t>(nid, 1));
+    } else {
+      id_bytes[g] = al(sizeof(int32_t) * (size_t)n_ads);
+    }
+    total += off_bytes[g] + id_bytes[g];
+  }
+  if (!s.h_in.reserve(total)) return COLD_ERR_OOM;
+  if (total > s.d_in_cap) {
+    if (s.d_in) cudaFree(s.d_in);
+    s.d_in = nullptr;
+    s.d_in_cap = 0;
+    if (cudaMalloc(&s.d_in, total * 3 / 2) != cudaSuccess) { cudaGetLastError(); return COLD_ERR_OOM; }
+    s.d_in_cap = total * 3 / 2;
+  }
+  uint8_t* hbase = (uint8_t*)s.h_in.p;
+  uint8_t* dbase = (uint8_t*)s.d_in;
+  size_t pos = 0;
+  int32_t* ao = (int32_t*)hbase;
+  ao[0] = 0;
+  for (int i = 0; i < B; i++) ao[i + 1] = ao[i] + s.recs[i].n;
+  s.ao_host = ao;
+  s.ao_dev = (const int32_t*)dbase;
+  pos += al(sizeof(int32_t) * (B + 1));
+  s.ids_dev.assign(M, nullptr);
+  s.offs_dev.assign(M, nullptr);
+  s.offs_host.assign(M, nullptr);
+  for (int g = 0; g < M; g++) {
+    const cold_group& G = groups[g];
+    if (G.side == COLD_CROSS || !s.recs[0].b->ids[g]) continue;
+    if (G.side == COLD_USER || G.pooled) {
+      // CSR bags: offsets over requests (USER) or ads (AD pooled), ids concatenated in order
+      int32_t* oo = (int32_t*)(hbase + pos);
+      int32_t* ii = (int32_t*)(hbase + pos + off_bytes[g]);
+      s.offs_host[g] = oo;
+      s.offs_dev[g] = (const int32_t*)(dbase + pos);
+      s.ids_dev[g] = (const int32_t*)(dbase + pos + off_bytes[g]);
+      int64_t row = 0;
       oo[0] = 0;
       for (const ReqRec& q : s.recs) {
         const int32_t* o = q.b->offs_host[g];
         const int32_t* aoq = q.b->ad_offsets_host;
         const int lo = G.side == COLD_USER ? q.r : aoq[q.r], hi = G.side == COLD_USER ? q.r + 1 : aoq[q.r + 1];
         const int32_t* src = q.b->ids[g];
-        for (int j = lo; j < hi; j++, row++) {
-          const int32_t len = o[j + 1] - o[j];
-          memcpy(ii + oo[row], src + o[j], sizeof(int32_t) * (size_t)len);
-          oo[row + 1] = oo[row] + len;
-        }
+        const int32_t len_all = o[hi] - o[lo];
+        memcpy(ii + oo[row], src + o[lo], sizeof(int32_t) * (size_t)len_all);   // the rows' bags are contiguous
+        const int32_t shift = oo[row] - o[lo];
+        for (int j = lo; j < hi; j++, row++) oo[row + 1] = o[j + 1] + shift;
       }
-      s.offs_ptr[g] = oo;
-      s.offs_host[g] = oo;
-      s.ids_ptr[g] = ii;
     } else {   // single-valued AD group: the request's ad slice
-      if (!s.ids[g].reserve(sizeof(int32_t) * (size_t)(ao[B] + 1))) return COLD_ERR_OOM;
-      int32_t* ii = (int32_t*)s.ids[g].p;
+      int32_t* ii = (int32_t*)(hbase + pos);
+      s.ids_dev[g] = (const int32_t*)(dbase + pos);
       for (int i = 0; i < B; i++) {
         const ReqRec& q = s.recs[i];
         memcpy(ii + ao[i], q.b->ids[g] + q.b->ad_offsets_host[q.r], sizeof(int32_t) * (size_t)q.n);
       }
-      s.ids_ptr[g] = ii;
     }
+    pos += off_bytes[g] + id_bytes[g];
   }
+  if (cudaMemcpyAsync(s.d_in, s.h_in.p, total, cudaMemcpyHostToDevice, stream) != cudaSuccess) return COLD_ERR_CUDA;
   return COLD_OK;
 }
 
@@ -182,6 +212,14 @@ void cold_server::run() {
     {
       std::unique_lock<std::mutex> lk(m);
       if (!o.inflight) {
+        if (q.empty() && !stop) {   // idle: spin up to 200 us for the next request (no wake-up latency), then block
+          lk.unlock();
+          const int64_t t_end = now_ns() + 200000;
+          while (queued.load(std::memory_order_acquire) == 0 && !stopping.load(std::memory_order_relaxed) &&
+                 now_ns() < t_end) {
+          }
+          lk.lock();
+        }
         cv.wait(lk, [&] { return stop || !q.empty(); });
         if (q.empty() && stop) break;
         // optional short wait for a fuller batch when the GPU is idle
@@ -194,25 +232,23 @@ void cold_server::run() {
         ads += q.front().n;
         s.recs.push_back(q.front());
         q.pop_front();
+        queued.fetch_sub(1, std::memory_order_relaxed);
       }
     }
     if (!s.recs.empty()) {
       const int B = (int)s.recs.size();
       cold_status st = assemble(s);
       if (st == COLD_OK) {
-        cold_batch hb;
-        memset(&hb, 0, sizeof(hb));
-        hb.num_requests = B;
-        hb.ad_offsets = (const int32_t*)s.ao.p;
-        hb.ad_offsets_host = (const int32_t*)s.ao.p;
-        hb.ids = s.ids_ptr.data();
-        hb.offs = s.offs_ptr.data();
-        hb.offs_host = s.offs_host.data();
-        const int32_t* ao = (const int32_t*)s.ao.p;
-        st = cold_score_batch(ctx, &hb, s.d_scores, stream);
-        if (st == COLD_OK && cudaMemcpyAsync(s.d_ao, ao, sizeof(int32_t) * (B + 1), cudaMemcpyHostToDevice, stream))
-          st = COLD_ERR_CUDA;
-        if (st == COLD_OK) st = cold_topk(ctx, s.d_scores, s.d_ao, ao, B, K, nullptr, s.d_idx, s.d_key, stream);
+        cold_batch db;
+        memset(&db, 0, sizeof(db));
+        db.num_requests = B;
+        db.ad_offsets = s.ao_dev;
+        db.ad_offsets_host = s.ao_host;
+        db.ids = s.ids_dev.data();
+        db.offs = s.offs_dev.data();
+        db.offs_host = s.offs_host.data();
+        st = cold_score_batch(ctx, &db, s.d_scores, stream);
+        if (st == COLD_OK) st = cold_topk(ctx, s.d_scores, s.ao_dev, s.ao_host, B, K, nullptr, s.d_idx, s.d_key, stream);
         int32_t* hi = (int32_t*)s.h_res.p;
         float* hk = (float*)(hi + (size_t)cfg.max_batch_requests * K);
         if (st == COLD_OK &&
@@ -274,7 +310,6 @@ extern "C" cold_status cold_server_create(cold_ctx* ctx, const cold_server_confi
   const size_t K = (size_t)cfg->top_k, B = (size_t)cfg->max_batch_requests;
   for (Slot& sl : s->slot) {
     ok = ok && cudaMalloc(&sl.d_scores, sizeof(float) * (size_t)cfg->max_batch_ads) == cudaSuccess;
-    ok = ok && cudaMalloc(&sl.d_ao, sizeof(int32_t) * (B + 1)) == cudaSuccess;
     ok = ok && cudaMalloc(&sl.d_idx, sizeof(int32_t) * B * K) == cudaSuccess;
     ok = ok && cudaMalloc(&sl.d_key, sizeof(float) * B * K) == cudaSuccess;
     ok = ok && sl.h_res.reserve(8 * B * K);
@@ -296,6 +331,7 @@ extern "C" void cold_server_destroy(cold_server* s) {
     {
       std::lock_guard<std::mutex> lk(s->m);
       s->stop = true;
+      s->stopping.store(true);
     }
     s->cv.notify_all();
     s->worker.join();
@@ -303,7 +339,7 @@ extern "C" void cold_server_destroy(cold_server* s) {
   cudaSetDevice(s->device);
   for (Slot& sl : s->slot) {
     if (sl.d_scores) cudaFree(sl.d_scores);
-    if (sl.d_ao) cudaFree(sl.d_ao);
+    if (sl.d_in) cudaFree(sl.d_in);
     if (sl.d_idx) cudaFree(sl.d_idx);
     if (sl.d_key) cudaFree(sl.d_key);
     if (sl.done) cudaEventDestroy(sl.done);
@@ -342,6 +378,7 @@ extern "C" cold_status cold_server_submit(cold_server* s, const cold_batch* reqs
       std::lock_guard<std::mutex> lk(s->m);
       s->q.push_back(ReqRec{reqs, r, ao[r + 1] - ao[r], idx_out + (size_t)r * K, key_out + (size_t)r * K, done_ns + r});
       s->submitted++;
+      s->queued.fetch_add(1, std::memory_order_release);
     }
     s->cv.notify_one();
   }

@@ -759,11 +759,12 @@ def test_prelu_variant(prec, chain_min):
     assert e.value.name == "COLD_ERR_PARAMS"
 
 
-@pytest.mark.parametrize("ring", [4, 5, 8])
+@pytest.mark.parametrize("ring", [0, 4, 5, 8])
 def test_gather_ring_equals_register_path(ring):
-    """The cp.async-ring build of the cross-bag columns (cold_config.gather_ring) sums the same rows in the same
-    bag order as the register path, so whole-span scores are bit-identical; a sample is checked against
-    the oracle. Spans of >= 75,776 ads take the ring; requests of mixed sizes put 1-3 requests in a CTA."""
+    """The bag-only gather builds of the cross-bag columns (cold_config.gather_ring: 0 default register
+    bursts in their own launch, 4/5/8 cp.async ring) sum the same rows in the same bag order as the one-launch
+    path (-1), so whole-span scores are bit-identical; a sample is checked against the oracle. Spans of
+    >= 75,776 ads take the split; requests of mixed sizes put 1-3 requests in a CTA."""
     sizes = [5000, 37, 20000, 1, 3000] * 6
     sch, params, batch = small_case("paper", R=len(sizes), n_ads=tuple(sizes), precision="f16", cap=50000, seed=111)
     ref = gpu_scores(make_ctx(sch, params, max_ads=batch.n_ads, max_requests=64, gather_ring=-1), batch)
@@ -794,8 +795,10 @@ def test_server_coalesced_results_equal_direct_calls():
     assert reqs == len(sizes) and 3 <= calls <= len(sizes)
     assert np.all(done > 0)
     oidx, okey = oracle.topk_batch(ref.astype(np.float64), batch.ad_offsets, K)
+    # the same ads sit in other FC tiles in a coalesced call, so a tile may add u1 in the epilogue instead of
+    # the MMA (D-4): keys agree to fp32 rounding (here bit-equal but for a few ULPs), positions exactly
     np.testing.assert_array_equal(idx, oidx)
-    np.testing.assert_array_equal(key.astype(np.float64), okey)
+    np.testing.assert_allclose(key.astype(np.float64), okey, rtol=1e-5)
     t0 = time.monotonic_ns() + 2_000_000
     arrival = t0 + np.arange(len(sizes), dtype=np.int64) * 200_000        # one request every 0.2 ms
     idx2, key2, done2 = srv.submit(hb, arrival_ns=arrival)
