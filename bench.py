@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--kernel-flags", type=int, default=0, help="cold_config.kernel_flags (A/B runs)")
     ap.add_argument("--gather-ring", type=int, default=0, help="cold_config.gather_ring (A/B runs)")
     ap.add_argument("--gather-span", type=int, default=0, help="cold_config.gather_span_chunks (A/B runs)")
+    ap.add_argument("--chain-min", type=int, default=0, help="cold_config.chain_min_ads (A/B runs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-latency", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -949,7 +950,8 @@ def main():
     N = batch.n_ads
     ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, device=local, max_ads=N,
                   max_requests=max(batch.R, 1), chunk_ads=args.chunk, se_mode="dense" if args.se_dense else "group",
-                  kernel_flags=args.kernel_flags, gather_ring=args.gather_ring, gather_span_chunks=args.gather_span)
+                  kernel_flags=args.kernel_flags, gather_ring=args.gather_ring, gather_span_chunks=args.gather_span,
+                  chain_min_ads=args.chain_min)
     load_ctx_params(ctx, params, dense_se_params(sch, args.seed + 17) if args.se_dense else None)
     K = args.topk
     step = RankStep(ctx, batch, K, world, r_pad, dev)
