@@ -76,6 +76,7 @@ struct cold_ctx {
   DevGroup* d_groups = nullptr;
   std::vector<DevGroup> h_groups;    // host copy (gather kernel parameters)
   float* d_se_w = nullptr;
+  std::vector<float> h_se_w, h_se_b;   // host copies (the gather passes its columns' SE weights as parameters)
   float* d_se_b = nullptr;
   float* d_w1u_t = nullptr;
   float* d_b1 = nullptr;
@@ -608,6 +609,8 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
   c->d_groups = src->d_groups;
   c->h_groups = src->h_groups;
   c->d_se_w = src->d_se_w;
+  c->h_se_w = src->h_se_w;
+  c->h_se_b = src->h_se_b;
   c->d_se_b = src->d_se_b;
   c->d_w1u_t = src->d_w1u_t;
   c->d_b1 = src->d_b1;
@@ -733,6 +736,8 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
   if (s) return s;
   s = upload(c, (void**)&c->d_se_b, sizeof(float) * c->M, [&](uint8_t* h) { memcpy(h, p->se_b, sizeof(float) * c->M); });
   if (s) return s;
+  c->h_se_w.assign(p->se_w, p->se_w + (size_t)c->M * k);
+  c->h_se_b.assign(p->se_b, p->se_b + c->M);
   if ((p->in_scale == nullptr) != (p->in_shift == nullptr))
     return fail(COLD_ERR_PARAMS, "in_scale and in_shift must both be set or both be NULL");
   if (p->in_scale) {
@@ -1028,6 +1033,19 @@ static UserArgs make_user_args(cold_ctx* c, const CallPlan& pl, const int32_t* d
   return ua;
 }
 
+// the SE weights of the launch's columns into its parameters (read through the constant bank: the
+// per-thread global loads of w_g were a quarter of the gather's LSU instructions)
+static void fill_se_params(const cold_ctx* c, GatherArgs& ga) {
+  ga.sew_in_params = 0;
+  if ((size_t)ga.n_ac * c->k > sizeof(ga.sew_c) / sizeof(float) || c->h_se_w.empty()) return;
+  for (int j = 0; j < ga.n_ac; j++) {
+    const int g = ga.ac_g[j];
+    memcpy(&ga.sew_c[(size_t)j * c->k], &c->h_se_w[(size_t)g * c->k], sizeof(float) * c->k);
+    ga.seb_c[j] = c->h_se_b[g];
+  }
+  ga.sew_in_params = 1;
+}
+
 static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0, int64_t n, const DebugOut& dbg) {
   GatherArgs ga;
   memset(&ga, 0, sizeof(ga));
@@ -1065,6 +1083,7 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
     ga.E = c->d_E;
     ga.lde = c->d_in;
   }
+  fill_se_params(c, ga);
   return ga;
 }
 
@@ -1326,6 +1345,8 @@ static cold_status run(cold_ctx* c, const cold_batch* b, float* scores, cudaStre
         d.order[d.n_ac] = d.n_ac;
         d.n_ac++;
       }
+      fill_se_params(c, gb);
+      fill_se_params(c, gr);
       c->mark_begin(st);
       if (gb.n_ac) launch_gather(gb, c->precision, st);
       launch_gather(gr, c->precision, st);
@@ -1491,6 +1512,7 @@ extern "C" cold_status cold_se_stats(cold_ctx* c, const cold_batch* b, double* m
       if (cls == pass) ga.ac_g[ga.n_ac++] = g;
     }
   for (int j = 0; j < ga.n_ac; j++) ga.order[j] = j;
+  fill_se_params(c, ga);
   ga.X = nullptr;
   ga.ohot = nullptr;
   ga.stats = d_stats;

@@ -84,6 +84,11 @@ struct GatherArgs {
   float* E;                        // dense SE (nullable): [n][lde] fp32 pre-SE ê (after linear_log) at
   int lde;                         //   column sel_pos * k; the gate runs in se_dense_kernel
   DevGroup gp[COLD_MAX_GROUPS];    // copy of groups[0..M) in the parameters (read via the constant bank)
+  // SE weights of the launch's columns in the parameters (constant bank): column j's w at
+  // sew_c[j * k .. j * k + k), b at seb_c[j]; set when n_ac * k <= GATHER_SEW_MAX (else read from se_w / se_b)
+  int sew_in_params;
+  float sew_c[512];
+  float seb_c[COLD_MAX_GROUPS];
   int ring;                        // != 0: every column is a cross-bag column (user bag x single ad id), for
                                    // the bag-only build: -1 register bursts, > 0 a `ring`-deep cp.async ring
   int search_req;                  // 1: request of an ad by binary search of adoff (req_of_ad not yet written)

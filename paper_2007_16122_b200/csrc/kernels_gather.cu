@@ -229,10 +229,11 @@ struct RawRow {
 #endif
 
 // pooled e -> [debug] -> linear_log -> SE gate -> v = s ê -> RNE cast -> X_ac[local][slot]
-// sew / seb: the group's SE weights (staged in shared memory by the one-group-per-CTA columns)
+// sew / seb: the group's SE weights in global memory; jcol >= 0 with a.sew_in_params: read them from the
+// kernel parameters instead (a.sew_c[jcol * K + d], a.seb_c[jcol]: uniform constant-bank loads, no LSU)
 template <typename T, int K, bool FAST>
 __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G, int g, int64_t local, float* e,
-                                          const float* sew, float seb) {
+                                          const float* sew, float seb, int jcol) {
   const int64_t ad = a.a0 + local;
   if (a.dbg_pooled) {
 #pragma unroll
@@ -254,12 +255,14 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
     return;
   }
   float z = 0.0f;
+  if (a.sew_in_params && jcol >= 0) {
 #pragma unroll
-#ifdef COLD_GATHER_SW_SMEM
-  for (int d = 0; d < K; d++) z = fmaf(sew[d], e[d], z);
-#else
-  for (int d = 0; d < K; d++) z = fmaf(__ldg(sew + d), e[d], z);
-#endif
+    for (int d = 0; d < K; d++) z = fmaf(a.sew_c[jcol * K + d], e[d], z);
+    seb = a.seb_c[jcol];
+  } else {
+#pragma unroll
+    for (int d = 0; d < K; d++) z = fmaf(__ldg(sew + d), e[d], z);
+  }
   const float s = sigmoid_t<FAST>(z + seb);
   if (a.stats) {                            // SE statistics mode (cold_se_stats)
     atomicAdd(a.stats + g, (double)s);
@@ -354,7 +357,8 @@ template <typename T, int K, bool FAST, int APT, int RING>
 __device__ __forceinline__ void cross_bag_ring(const GatherArgs& a, const DevGroup& G, int g, const T* __restrict__ tab,
                                                uint64_t card, const uint64_t (*s_hx)[HX_HALF], const int64_t* ul,
                                                int rfirst, const BatchGroup& BA, const DevGroup& A,
-                                               const float* sew, float seb, const int64_t* loc, const bool* ok) {
+                                               const float* sew, float seb, int j, const int64_t* loc,
+                                               const bool* ok) {
   static_assert(K * (int)sizeof(T) == 32, "ring rows are 32 B");
   extern __shared__ __align__(16) uint8_t ring_smem[];
   const uint32_t my = smem_addr(ring_smem) + threadIdx.x * 32u;
@@ -414,7 +418,7 @@ __device__ __forceinline__ void cross_bag_ring(const GatherArgs& a, const DevGro
 #pragma unroll
       for (int d = 0; d < 8; d++) e[8 + d] = Store<T>::add(e[8 + d], t1[d]);
     }
-    if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb);
+    if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb, j);
   }
   cp_async_wait<0>();
 }
@@ -445,16 +449,8 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
 #endif
   const int j = a.order[blockIdx.y];
   const int g = a.ac_g[j];
-#ifdef COLD_GATHER_SW_SMEM   // A/B build: the group's SE weights staged in shared memory (a barrier at CTA start)
-  __shared__ float s_w[K + 1];
-  if (threadIdx.x <= K) s_w[threadIdx.x] = threadIdx.x < K ? a.se_w[g * K + threadIdx.x] : a.se_b[g];
-  __syncthreads();
-  const float* sew = s_w;
-  const float seb = s_w[K];
-#else
   const float* sew = a.se_w + g * K;
-  const float seb = __ldg(a.se_b + g);
-#endif
+  const float seb = a.sew_in_params ? 0.0f : __ldg(a.se_b + g);
   const DevGroup G = GGROUP(a, g);
   const T* tab = reinterpret_cast<const T*>(G.table);
   const int64_t base = (int64_t)blockIdx.x * (128 * GATHER_APT);
@@ -483,7 +479,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
 #pragma unroll
         for (int d = 0; d < K; d++) e[d] = 0.0f;
         raw[i].add_to(e);
-        if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb);
+        if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb, j);
       }
     } else {
       for (int i = 0; i < GATHER_APT; i++) {
@@ -500,7 +496,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
           const int64_t o1 = (int64_t)B.offs[ad + 1 - B.offs_shift] - B.val_shift;
           for (int64_t q = o0; q < o1; q++) add_row<T, K>(tab, checked(B.ids[q], G.card, a.validate, a.err), e);
         }
-        finish_ad<T, K, FAST>(a, G, g, li, e, sew, seb);
+        finish_ad<T, K, FAST>(a, G, g, li, e, sew, seb, j);
       }
     }
     return;
@@ -549,14 +545,14 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
 #pragma unroll
       for (int d = 0; d < K; d++) e[d] = 0.0f;
       raw[i].add_to(e);
-      if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb);
+      if (ok[i]) finish_ad<T, K, FAST>(a, G, g, loc[i], e, sew, seb, j);
     }
     return;
   }
 
   if constexpr (RING > 0 && K * (int)sizeof(T) == 32) {
     if (shared_hx && !A.pooled) {
-      cross_bag_ring<T, K, FAST, GATHER_APT, RING>(a, G, g, tab, card, s_hx, ul, rfirst, BA, A, sew, seb, loc, ok);
+      cross_bag_ring<T, K, FAST, GATHER_APT, RING>(a, G, g, tab, card, s_hx, ul, rfirst, BA, A, sew, seb, j, loc, ok);
       return;
     }
   }
@@ -605,7 +601,7 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
         }
       }
     }
-    finish_ad<T, K, FAST>(a, G, g, li, e, sew, seb);
+    finish_ad<T, K, FAST>(a, G, g, li, e, sew, seb, j);
   }
 }
 
