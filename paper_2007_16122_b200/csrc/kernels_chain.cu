@@ -30,6 +30,11 @@
 namespace cold {
 
 constexpr int C_BN = 256;
+#ifdef COLD_CHAIN_H1_BLOCK   // A/B: FC2 waits for the whole H1 block (round-1 behaviour)
+constexpr bool H1_TILES = false;
+#else
+constexpr bool H1_TILES = true;
+#endif
 constexpr int C_EPI_WARPS = 8;
 constexpr int C_THREADS = 64 + 32 * C_EPI_WARPS;
 constexpr int C_A_BYTES = BM * BK * 2;                 // 16 KB: own 128 rows x 64 K
@@ -83,7 +88,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   uint64_t* uxfull = tempty + 2;                  // leader: u1 operand landed [C_NUX]
   uint64_t* uxempty = uxfull + C_NUX;             // both: u1 MMA of the buffer's last FC1 tile done [C_NUX]
   uint64_t* hready = uxempty + C_NUX;             // local: [l] block of layer l's output stored (H1..H4)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hready + 4);
+  uint64_t* h1t = hready + 4;                     // local: [nb] FC1 n-tile nb of the block stored (H1_TILES)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h1t + 4);
   // FC2 / FC3 biases in shared memory: the epilogue reads them with LDS instead of a global load that
   // stalled it (ncu r01h: 9% of the chain's stall samples on the bias add)
   float* sBias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);
@@ -127,6 +133,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     for (int s = 0; s < 2; s++) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * C_EPI_WARPS); }
     for (int s = 0; s < C_NUX; s++) { mbar_init(&uxfull[s], 1); mbar_init(&uxempty[s], 1); }
     for (int i = 0; i < 4; i++) mbar_init(&hready[i], C_EPI_WARPS);
+    for (int i = 0; i < 4; i++) mbar_init(&h1t[i], C_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const CUtensorMap* maps[12] = {&tmX, &tmW1, &tmW2, &tmW3, &tmH1, &tmH2, &tmH3, &tmOH, &tmU1T, &tmW4, &tmW5, &tmH4};
     for (int i = 0; i < (TAIL ? 12 : 9); i++) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)maps[i]) : "memory");
@@ -164,9 +171,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       for_tasks([&](int l, int j, int nb) {
         const int pm = pair + j * npairs;
         const int mrow = pm * 2 * BM + (int)rank * BM;
-        if (l > 0 && nb == 0) cwait(&hready[l - 1], (uint32_t)(j & 1), w_hready, ins);   // own rows of the input
+        if (l > 1 || (l == 1 && !H1_TILES)) {
+          if (nb == 0) cwait(&hready[l - 1], (uint32_t)(j & 1), w_hready, ins);   // own rows of the input
+        }
         const int bhalf = tn[l] / 2;                  // weight rows this CTA stages (half the tile N)
         for (int kb = 0; kb < kbs[l]; kb++) {
+          // FC2 reads H1 one FC1 n-tile (C_BN columns) at a time: wait for that tile's stores only, so FC2(j)
+          // starts on the first tiles of H1(j) while the last FC1 tile is still draining
+          if (H1_TILES && l == 1 && (kb * BK) % C_BN == 0)
+            cwait(&h1t[(kb * BK) / C_BN], (uint32_t)(j & 1), w_hready, ins);
           cwait(&empty[s], ph ^ 1, w_empty, ins);
           if (leader) mbar_expect_tx(&full[s], 2 * (C_A_BYTES + bhalf * BK * 2));
           tma_load_2d_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb * BK, mrow, l == 0 ? pol_x : pol_a);
@@ -305,7 +318,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
       lt++;
       const bool last_of_layer = nb == ntile[l] - 1;
-      if ((l < 2 || (TAIL && l < 4)) && last_of_layer) {
+      if (H1_TILES && l == 0) {
+        // per-tile H1 readiness: tile nb - 1's stores are complete once at most this tile's two group stores
+        // are pending (lazy: no wait on the tile just issued); the block's last tile waits for everything
+        if (nb > 0) {
+          if (elected) {
+            bulk_wait_group<2>();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+          named_bar_sync(1 + h, 128);
+          if (lane == 0) mbar_arrive(&h1t[nb - 1]);
+        }
+        if (last_of_layer) {
+          if (elected) {
+            bulk_wait_all();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+          named_bar_sync(1 + h, 128);
+          if (lane == 0) mbar_arrive(&h1t[nb]);
+        }
+      } else if ((l < 2 || (TAIL && l < 4)) && last_of_layer) {
         // the block's rows of this layer are stored once this group's bulk stores completed
         if (elected) {
           bulk_wait_all();
