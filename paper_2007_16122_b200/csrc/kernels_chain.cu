@@ -35,15 +35,16 @@ constexpr bool H1_TILES = false;
 #else
 constexpr bool H1_TILES = true;
 #endif
-constexpr int C_EPI_WARPS = 8;
+constexpr int C_EPI_WARPS = 8;                         // 2 per TMEM lane quadrant, 128 columns each
+constexpr int C_GROUPS = C_EPI_WARPS / 4;              // 4-warp store groups (one 16 KB staging box each)
 constexpr int C_THREADS = 64 + 32 * C_EPI_WARPS;
 constexpr int C_A_BYTES = BM * BK * 2;                 // 16 KB: own 128 rows x 64 K
 constexpr int C_B_BYTES = (C_BN / 2) * BK * 2;         // 16 KB: own half of the 256-row weight tile
 constexpr int C_STAGE_BYTES = C_A_BYTES + C_B_BYTES;
 #ifdef COLD_CHAIN_EPI_DB
-constexpr int C_OUT_BOXES = 4;   // A/B build: two 16 KB boxes per group (one pipeline stage fewer): measured neutral
+constexpr int C_OUT_BOXES = 2 * C_GROUPS;   // A/B: two 16 KB boxes per group (one pipeline stage fewer): neutral
 #else
-constexpr int C_OUT_BOXES = 2;   // one 16 KB staging box per 4-warp group
+constexpr int C_OUT_BOXES = C_GROUPS;   // one 16 KB staging box per 4-warp group
 #endif
 constexpr int C_OUT_BYTES = C_OUT_BOXES * EPI_GROUP_BOX;
 constexpr int C_UXA = BM * 32, C_UXB = (C_BN / 2) * 16 * 4, C_UX_BUF = C_UXA + C_UXB, C_NUX = 2;
@@ -301,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       } else {
         // H3 (no TAIL) leaves for the tail kernel: stream it past L2 (evict_first) so it does not push out
         // live H1 / H2
-        const int half = tn[l] / 2;
+        const int half = tn[l] / C_GROUPS;      // this group's columns of the tile
         const float* bias = l == 1 ? cp.b2 : (l == 2 ? cp.b3 : (l == 3 ? cp.b4 : nullptr));
         uint32_t bias_s = 0u;   // smem address of this tile's bias columns (added like a u1 row)
         if (sbias && (l == 1 || l == 2)) {
@@ -311,7 +312,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         const float* slope = l == 0 ? cp.s1 : (l == 1 ? cp.s2 : (l == 2 ? cp.s3 : nullptr));
         epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, bias_s, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
                              nb * tn[l], trow0, q, h, lane, 0, nullptr, nullptr, 0, 0,
-                             0ull, slope, C_OUT_BOXES == 4 ? sOut + (2 + h) * EPI_GROUP_BOX : nullptr, &box_ctr);
+                             0ull, slope, C_OUT_BOXES == 2 * C_GROUPS ? sOut + (C_GROUPS + h) * EPI_GROUP_BOX : nullptr,
+                             &box_ctr);
       }
       tc_fence_before();
       __syncwarp();
