@@ -23,7 +23,7 @@ namespace cold {
 constexpr int Q_EPI_WARPS = 8;
 constexpr int Q_THREADS = 64 + 32 * Q_EPI_WARPS;
 constexpr int Q_K4 = 256, Q_N4 = 128, Q_N5 = 64;
-constexpr int Q_STAGES = 4;
+constexpr int Q_STAGES = 4;   // (5 measured neutral: profiles/r02/ab_t5_*.jsonl)
 constexpr int Q_A_BYTES = BM * BK * 2;                  // 16 KB: 128 rows x 64 cols of H3
 constexpr int Q_W4_ATOM = Q_N4 * 128;                   // 16 KB: 128 rows x 64 K
 constexpr int Q_W4_BYTES = (Q_K4 / BK) * Q_W4_ATOM;     // 64 KB

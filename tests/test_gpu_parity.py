@@ -246,14 +246,16 @@ def test_topk_exact_on_same_keys():
         idx, key = gpu_topk(ctx, keys, ao, K)
         oidx, _ = oracle.topk_batch(keys.astype(np.float64), ao, K)
         np.testing.assert_array_equal(idx, oidx)
-    ao2 = np.asarray([0, 4000, 14000], np.int32)
-    keys2 = keys[105:105 + 14000]
-    bids2 = bids[105:105 + 14000]
-    for K in (500, 1000):
-        idx, key = gpu_topk(ctx, keys2, ao2, K, bids=bids2)
-        ecpm = (keys2 * bids2).astype(np.float32).astype(np.float64)
-        oidx, _ = oracle.topk_batch(ecpm, ao2, K)
-        np.testing.assert_array_equal(idx, oidx)
+    # a 10,000-ad segment (radix-select path) and segments of <= 4096 ads (whole-segment bitonic sort path)
+    for ao2 in (np.asarray([0, 4000, 14000], np.int32), np.asarray([0, 4000, 8096, 9097], np.int32)):
+        keys2 = keys[105:105 + int(ao2[-1])]
+        bids2 = bids[105:105 + int(ao2[-1])]
+        for K in (500, 1000):
+            idx, key = gpu_topk(ctx, keys2, ao2, K, bids=bids2)
+            ecpm = (keys2 * bids2).astype(np.float32).astype(np.float64)
+            oidx, okey = oracle.topk_batch(ecpm, ao2, K)
+            np.testing.assert_array_equal(idx, oidx)
+            np.testing.assert_array_equal(key.astype(np.float64), okey.astype(np.float32).astype(np.float64))
 
 
 def test_topk_vs_oracle_scores_within_tolerance():

@@ -16,7 +16,7 @@ timeout 400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 REPS=""
 for k in $KERNELS; do
   case $k in
-    gather) RX="regex:gather_kernel"; S=1; NM=gather;;
+    gather) RX="regex:gather_kernel"; S=2; C=2; NM=gather;;   # the span's two launches (cross-bag columns, the rest)
     chain) RX="regex:chain_kernel"; S=1; NM=chain;;
     fc1) RX="regex:gemm_pair_kernel"; S=3; NM=fc1;;      # pair launches per chunk: FC1, FC2, FC3
     fc2) RX="regex:gemm_pair_kernel"; S=4; NM=fc2;;
@@ -24,9 +24,11 @@ for k in $KERNELS; do
     tail45) RX="regex:tail45_kernel"; S=1; NM=tail;;
     *) RX="regex:$k"; S=1; NM=$k;;
   esac
-  timeout 400 ncu --set full --clock-control none --import-source on -k $RX -s $S -c 1 \
+  C=${C:-1}
+  timeout 400 ncu --set full --clock-control none --import-source on -k $RX -s $S -c $C \
     -o $OUT/prof_${k}_$TAG python bench.py $ARGS > $OUT/ncu_${k}_$TAG.log 2>&1
   REPS="$REPS $NM=$OUT/prof_${k}_$TAG.ncu-rep"
+  unset C
 done
 for f in $OUT/prof_*_$TAG.ncu-rep; do python tools/ncu_summary.py $f; done > $OUT/ncu_summary_$TAG.txt 2>&1
 python tools/ncu_traffic.py --commit "${GIT_SHA:-unknown}" --source "ncu --set full, bench.py $ARGS, tag $TAG" \

@@ -37,14 +37,22 @@ def main():
     out = {"commit": a.commit, "source": a.source, "kernels": {}}
     for item in a.reps:
         name, rep = item.split("=", 1)
-        d = summary(rep)[0]
-        rd, wr = num(d["dram__bytes_read.sum"]), num(d["dram__bytes_write.sum"])
-        k = {"kernel_name": d.get("Kernel Name", "").replace("void ", "").split("(")[0], "dram_read_bytes": rd, "dram_write_bytes": wr,
-             "dram_bytes_per_launch": rd + wr, "duration": d.get("gpu__time_duration.sum"),
-             "tensor_active_pct": num(d.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "0")),
-             "dram_throughput_pct": num(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "0")),
-             "l2_throughput_pct": num(d.get("lts__throughput.avg.pct_of_peak_sustained_elapsed", "0")),
-             "warps_active_pct": num(d.get("sm__warps_active.avg.pct_of_peak_sustained_active", "0"))}
+        launches = summary(rep)   # one or more consecutive launches of the kernel class (e.g. the two gather
+        #                           launches of one span: the cross-bag columns, then the rest), summed
+        rd = sum(num(d["dram__bytes_read.sum"]) for d in launches)
+        wr = sum(num(d["dram__bytes_write.sum"]) for d in launches)
+        durs = [num(d.get("gpu__time_duration.sum", "0")) for d in launches]
+        tot = sum(durs) or 1.0
+
+        def wavg(key):
+            return sum(num(d.get(key, "0")) * w for d, w in zip(launches, durs)) / tot
+        k = {"kernel_name": " + ".join(d.get("Kernel Name", "").replace("void ", "").split("(")[0] for d in launches),
+             "launches": len(launches), "dram_read_bytes": rd, "dram_write_bytes": wr,
+             "dram_bytes_per_launch": rd + wr, "duration": " + ".join(d.get("gpu__time_duration.sum") for d in launches),
+             "tensor_active_pct": wavg("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+             "dram_throughput_pct": wavg("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+             "l2_throughput_pct": wavg("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+             "warps_active_pct": wavg("sm__warps_active.avg.pct_of_peak_sustained_active")}
         if name in ads:
             k["ads_per_launch"] = ads[name]
             k["dram_bytes_per_ad"] = (rd + wr) / ads[name]
