@@ -171,58 +171,7 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
   }
 }
 
-// Short segments (n <= TOPK_SORT_MAX, the single-request latency path): one bitonic sort of the whole
-// segment's 64-bit composites (key << 32 | ~position, descending = key desc, position asc; NaN keys are 0,
-// padding is 0 and sorts below every real key) in shared memory, then the first K. No radix passes: CTR-like
-// keys share their top bytes, so the radix histograms serialised on one or two bins.
-constexpr int TOPK_SORT_MAX = 4096;
-
-__global__ void __launch_bounds__(TOPK_THREADS) topk_sort_kernel(TopkArgs a) {
-  extern __shared__ unsigned long long cs[];   // [P]
-  const int r = blockIdx.x;
-  const int64_t base = a.ad_offsets[r];
-  const int n = (int)(a.ad_offsets[r + 1] - base);
-  int P = 1;
-  while (P < n) P <<= 1;
-  for (int i = threadIdx.x; i < P; i += blockDim.x) {
-    unsigned long long c = 0ull;
-    if (i < n) {
-      float v = a.scores[base + i];
-      if (a.bids) v *= a.bids[base + i];
-      c = ((unsigned long long)orderable(v) << 32) | (0xffffffffu - (uint32_t)i);
-    }
-    cs[i] = c;
-  }
-  __syncthreads();
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        const int j = i ^ stride;
-        if (j > i) {
-          const bool desc = ((i & size) == 0);
-          const unsigned long long x = cs[i], y = cs[j];
-          if (desc ? (x < y) : (x > y)) { cs[i] = y; cs[j] = x; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < a.K; i += blockDim.x) {
-    const unsigned long long c = cs[i];
-    a.idx[(int64_t)r * a.K + i] = (int32_t)(0xffffffffu - (uint32_t)(c & 0xffffffffu));
-    a.key[(int64_t)r * a.K + i] = from_orderable((uint32_t)(c >> 32));
-  }
-}
-
 void launch_topk(const TopkArgs& a0, cudaStream_t s) {
-#ifndef COLD_TOPK_NO_SORT
-  if (a0.G == 0 && a0.max_n > 0 && a0.max_n <= TOPK_SORT_MAX) {
-    int P = 1;
-    while (P < a0.max_n) P <<= 1;
-    topk_sort_kernel<<<a0.R, TOPK_THREADS, (size_t)P * sizeof(unsigned long long), s>>>(a0);
-    return;
-  }
-#endif
   TopkArgs a = a0;
   int P = 1;
   while (P < a.K) P <<= 1;
