@@ -937,10 +937,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # COLD_BENCH_ONE_GPU=1 (path check only, never a bench number): every rank on cuda:0 over gloo, so the
+    # N > 1 code path (partition, RankStep, gather, e2e D2H, SplitRequest, per-rank timing) runs on a 1-GPU box
+    one_gpu = os.environ.get("COLD_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    cdev = torch.device("cpu") if one_gpu else dev     # bookkeeping collectives (gloo: host tensors)
 
     sch = schema_for(args)
     t_setup = time.perf_counter()
@@ -959,7 +968,7 @@ def main():
     setup_s = time.perf_counter() - t_setup
     n_all = [N]
     if world > 1:
-        t = torch.tensor([N], device=dev, dtype=torch.int64)
+        t = torch.tensor([N], device=cdev, dtype=torch.int64)
         gl = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(gl, t)
         n_all = [int(x.item()) for x in gl]
@@ -967,7 +976,7 @@ def main():
     def max_over_ranks(ms):
         if world == 1:
             return ms, [ms]
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device=cdev, dtype=torch.float64)
         gl = [torch.empty_like(t) for _ in range(world)]
         dist.all_gather(gl, t)
         per = [float(x.item()) for x in gl]
@@ -1152,7 +1161,7 @@ def main():
                 split(mine[i])
                 evs[i][1].record(stream)
             torch.cuda.synchronize()
-            lat = torch.tensor([a.elapsed_time(b) for a, b in evs], dtype=torch.float64, device=dev)
+            lat = torch.tensor([a.elapsed_time(b) for a, b in evs], dtype=torch.float64, device=cdev)
             dist.all_reduce(lat, op=dist.ReduceOp.MAX)
             lat = lat.cpu().numpy()
             latency_split = {"n_ads": args.ads, "requests": nl, "gpus": world, "p50_ms": float(np.percentile(lat, 50)),
