@@ -84,6 +84,7 @@ enum { COLD_RELU = 0, COLD_PRELU = 1 };
 #define COLD_K_CHAIN_TAIL 128u   /* FC4/FC5/head inside the chain kernel (measured 4% slower; ReLU only) */
 #define COLD_K_SERIAL_USER 256u  /* calls of <= 4 requests: user kernel before the gather, one stream */
 #define COLD_K_NO_PDL     512u   /* no programmatic dependent launch between the kernels */
+#define COLD_K_X_ROWS    1024u   /* X_ac row-major (512 B rows) instead of the half-slab layout */
 
 /* A feature group ("the embedding of the i-th feature group e_i"). */
 typedef struct {

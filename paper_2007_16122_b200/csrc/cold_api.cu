@@ -101,6 +101,7 @@ struct cold_ctx {
   void* d_H[COLD_MAX_LAYERS] = {nullptr};
   CUtensorMap tmA[COLD_MAX_LAYERS];
   std::vector<CUtensorMap> tmAX;     // layer-0 A maps, one per chunk slot of the gather span
+  bool x_slab = false;               // X_ac in the half-slab layout [2 slot + h][span rows][8]
   bool u1mma = false;                // FC1 adds u1[request(row)] on the tensor core (kernels_gemm2.cu)
   bool chain = false;                // FC1 -> FC3 in one persistent kernel over 256-row blocks
   int64_t chain_min = 0;             // chunks smaller than this use the layer-by-layer kernels
@@ -303,6 +304,23 @@ static cold_status make_tmap(CUtensorMap* tm, void* ptr, int precision, uint64_t
   return COLD_OK;
 }
 
+// X_ac half-slab planes [planes][rows_total][8] 16-bit, viewed from chunk row offset `ptr`: 3-D map
+// {8 columns, rows, planes}, box {8, 128, 8} (one 64-column k-block = 8 half-slabs), no swizzle
+static cold_status make_tmap_slab(CUtensorMap* tm, void* ptr, int precision, uint64_t rows, uint64_t rows_total,
+                                  uint64_t planes) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[3] = {8, rows, planes};
+  cuuint64_t strides[2] = {16, rows_total * 16};
+  cuuint32_t box[3] = {8, 128, 8};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(tm, precision == COLD_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   3, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled (slab) failed: " + std::to_string((int)r));
+  return COLD_OK;
+}
+
 // 2-D 16-bit tensor, no swizzle: box rows of box_cols * 2 bytes land contiguously (the FC1 u1 operand)
 static cold_status make_tmap_plain(CUtensorMap* tm, void* ptr, int precision, uint64_t inner, uint64_t rows,
                                    uint32_t box_rows, uint32_t box_cols) {
@@ -487,10 +505,17 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       cold_status s = make_tmap(&c->tmA[l], in, c->precision, K, c->chunk, 128);
       if (s) { delete c; return s; }
       if (l == 0) {
+        // X_ac half-slabs (coalesced gather stores) when FC1 runs as a GEMM / the chain with per-group SE
+        // (not when layer 0 sits inside a fused tail kernel, nor for the dense-SE gate's row-major X)
+        c->x_slab = !c->dense_se && c->k % 8 == 0 && (c->L - 1 - c->n_tail) >= 1 && !(c->kflags & COLD_K_X_ROWS);
         c->tmAX.resize(c->gspan);
         for (int j = 0; j < c->gspan; j++) {
-          s = make_tmap(&c->tmAX[j], (uint8_t*)c->d_X + (size_t)j * c->chunk * c->d_ac_pad * 2, c->precision, K,
-                        c->chunk, 128);
+          if (c->x_slab)
+            s = make_tmap_slab(&c->tmAX[j], (uint8_t*)c->d_X + (size_t)j * c->chunk * 16, c->precision, c->chunk,
+                               (uint64_t)c->gspan * c->chunk, (uint64_t)c->d_ac_pad / 8);
+          else
+            s = make_tmap(&c->tmAX[j], (uint8_t*)c->d_X + (size_t)j * c->chunk * c->d_ac_pad * 2, c->precision, K,
+                          c->chunk, 128);
           if (s) { delete c; return s; }
         }
       }
@@ -1067,6 +1092,8 @@ static GatherArgs make_gather_args(cold_ctx* c, const BatchView& bv, int64_t a0,
   ga.n = n;
   ga.X = c->d_X;
   ga.ldx = c->d_ac_pad;
+  ga.x_slab = c->x_slab ? 1 : 0;
+  ga.x_rows = (int64_t)c->gspan * c->chunk;
   ga.validate = (c->flags & COLD_VALIDATE_IDS) ? 1 : 0;
   ga.err = c->d_err;
   ga.dbg_pooled = dbg.pooled;
@@ -1125,6 +1152,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     memset(&cp, 0, sizeof(cp));
     cp.b2 = c->d_b[1];
     cp.b3 = c->d_b[2];
+    cp.x_slab = c->x_slab ? 1 : 0;
     cp.s1 = c->d_slope[0];
     cp.s2 = c->d_slope[1];
     cp.s3 = c->d_slope[2];
@@ -1182,6 +1210,7 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     memset(&ep, 0, sizeof(ep));
     ep.relu = 1;
     ep.slope = c->d_slope[l];
+    ep.a_slab = (l == 0 && c->x_slab) ? 1 : 0;
     if (l == 0) {
       ep.u1 = c->d_u1;
       ep.ld_u1 = c->widths[0];

@@ -89,6 +89,8 @@ struct GatherArgs {
   int sew_in_params;
   float sew_c[512];
   float seb_c[COLD_MAX_GROUPS];
+  int x_slab;                      // X_ac in the half-slab layout: column block `slot` of ad a at
+  int64_t x_rows;                  //   [(2 slot + h) * x_rows + a][8], h = 0 / 1 for columns 0-7 / 8-15
   int ring;                        // != 0: every column is a cross-bag column (user bag x single ad id), for
                                    // the bag-only build: -1 register bursts, > 0 a `ring`-deep cp.async ring
   int search_req;                  // 1: request of an ad by binary search of adoff (req_of_ad not yet written)
@@ -155,6 +157,7 @@ struct EpiParams {
   int head_n;                      // 0: no head; 1 or 2: fused last layer + sigmoid
   float* scores;                   // chunk-local [M]
   int relu;
+  int a_slab;                      // A (layer 0: X_ac) in the half-slab layout via a 3-D map
   const float* slope;              // PReLU slopes [N] (F2; null: ReLU when relu)
   unsigned long long* instr;       // debug: per-role wait-cycle counters [8] (null = off)
   int dbg_mode;                    // timing experiments only (results invalid): 1 = epilogue only drains
@@ -195,6 +198,7 @@ cudaError_t launch_tail(const CUtensorMap* tmA3, const CUtensorMap* tmB3, const 
 struct ChainParams {
   const float* b2; const float* b3;      // FC2 / FC3 biases (FC1's bias is inside u1)
   const float* s1; const float* s2; const float* s3;   // PReLU slopes of FC1..FC3 (F2; null: ReLU)
+  int x_slab;                            // FC1's A (X_ac) in the half-slab layout (3-D map)
   const float* u1; int ld_u1;            // FC1 fallback for blocks spanning > U1_NSLOT requests
   const int32_t* req_of_ad; int64_t a0;
   int n1, n2, n3, k1;                    // widths of FC1..FC3 and FC1's K (D_ac_pad)

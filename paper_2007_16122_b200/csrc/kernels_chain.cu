@@ -183,7 +183,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
             cwait(&h1t[(kb * BK) / C_BN], (uint32_t)(j & 1), w_hready, ins);
           cwait(&empty[s], ph ^ 1, w_empty, ins);
           if (leader) mbar_expect_tx(&full[s], 2 * (C_A_BYTES + bhalf * BK * 2));
-          tma_load_2d_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb * BK, mrow, l == 0 ? pol_x : pol_a);
+          tma_load_a_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb, mrow, l == 0 ? pol_x : pol_a, l == 0 && cp.x_slab);
           tma_load_2d_pair(sB + s * C_B_BYTES, tB[l], &full[s], kb * BK, nb * tn[l] + (int)rank * bhalf, pol_b);
           if (++s == C_STAGES) { s = 0; ph ^= 1; }
         }
@@ -228,8 +228,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           const uint64_t ad = sdesc_sw128(smem_u32(sA + s * C_A_BYTES));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + s * C_B_BYTES));
 #pragma unroll
-          for (int kk = 0; kk < BK / UMMA_K; kk++)
-            umma_f16_pair(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+          for (int kk = 0; kk < BK / UMMA_K; kk++) {
+            const uint64_t a_kk = (l == 0 && cp.x_slab) ? sdesc_k16_plain(smem_u32(sA + s * C_A_BYTES) + kk * BM * 32)
+                                                         : ad + (uint64_t)(kk * 2);
+            umma_f16_pair(d, a_kk, bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+          }
           umma_commit_pair(&empty[s]);
           if (++s == C_STAGES) { s = 0; ph ^= 1; }
         }

@@ -277,8 +277,23 @@ __device__ __forceinline__ void finish_ad(const GatherArgs& a, const DevGroup& G
 #pragma unroll
     for (int d = 0; d < K; d++) out[d] = Store<T>::from_f(s * e[d]);
   }
-  T* dst = reinterpret_cast<T*>(a.X) + local * a.ldx + G.sel_slot * K;
   constexpr int BYTES = K * (int)sizeof(T);
+  if constexpr (sizeof(T) == 2 && K % 8 == 0) {
+    if (a.x_slab) {   // half-slab layout: 8 columns (16 B) per plane, consecutive ads contiguous in a plane, so a
+      //               warp's stores are 512 B runs (4 full lines) instead of 32 scattered 32 B sectors
+      T* xb = reinterpret_cast<T*>(a.X);
+#pragma unroll
+      for (int v = 0; v < K / 8; v++)
+        reinterpret_cast<uint4*>(xb + ((int64_t)(G.sel_slot * (K / 8) + v) * a.x_rows + local) * 8)[0] =
+            reinterpret_cast<const uint4*>(out)[v];
+      if (a.dbg_feat) {
+#pragma unroll
+        for (int d = 0; d < K; d++) a.dbg_feat[ad * a.d_in + G.sel_pos * K + d] = Store<T>::to_f(out[d]);
+      }
+      return;
+    }
+  }
+  T* dst = reinterpret_cast<T*>(a.X) + local * a.ldx + G.sel_slot * K;
   if constexpr (BYTES % 32 == 0) {
 #pragma unroll
     for (int v = 0; v < BYTES / 16; v += 2)

@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = 0; kb < kb_count; kb++) {
           mbar_wait_t(&empty[s], ph ^ 1, w_empty, ins);
           mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
-          tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK, mb * BM, pol_a);
+          tma_load_a(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb, mb * BM, pol_a, ep.a_slab != 0);
           if (!RESB) {
             uint8_t* dstB = sB + s * Cfg::B_BYTES + crank * B_SLICE_BYTES;
             if (CS > 1)
@@ -214,8 +214,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint64_t bd = sdesc_sw128(smem_u32(RESB ? sRes + kb * Cfg::B_BYTES : sB + s * Cfg::B_BYTES));
           if (ep.dbg_mode != 2) {
 #pragma unroll
-            for (int kk = 0; kk < BK / UMMA_K; kk++)   // +32 B along K inside the swizzle atom
-              umma_f16(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / UMMA_K; kk++) {   // +32 B along K inside the swizzle atom (slab: +4 KB)
+              const uint64_t a_kk = ep.a_slab ? sdesc_k16_plain(smem_u32(sA + s * Cfg::A_BYTES) + kk * BM * 32)
+                                              : ad + (uint64_t)(kk * 2);
+              umma_f16(d, a_kk, bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            }
           }
           if (CS > 1) umma_commit_mc(&empty[s], (uint16_t)((1u << CS) - 1u));
           else umma_commit(&empty[s]);

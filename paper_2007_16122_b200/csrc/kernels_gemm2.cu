@@ -171,7 +171,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>
         for (int kb = 0; kb < kb_count; kb++) {
           mbar_wait(&empty[s], ph ^ 1);
           if (leader) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
-          tma_load_2d_pair(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * BK, mrow, pol_a);
+          tma_load_a_pair(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb, mrow, pol_a, ep.a_slab != 0);
           if (!RES)
             tma_load_2d_pair(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * BK, nb * BN + (int)rank * (BN / 2), pol_b);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
@@ -210,8 +210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>
           const uint64_t bd = sdesc_sw128(smem_u32(RES ? sRes + kb * Cfg::B_ATOM : sB + s * Cfg::B_BYTES));
           if (ep.dbg_mode != 2) {
 #pragma unroll
-            for (int kk = 0; kk < BK / UMMA_K; kk++)
-              umma_f16_pair(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            for (int kk = 0; kk < BK / UMMA_K; kk++) {
+              const uint64_t a_kk = ep.a_slab ? sdesc_k16_plain(smem_u32(sA + s * Cfg::A_BYTES) + kk * BM * 32)
+                                              : ad + (uint64_t)(kk * 2);
+              umma_f16_pair(d, a_kk, bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            }
           }
           umma_commit_pair(&empty[s]);
           if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }

@@ -1,6 +1,6 @@
 // pair.cuh — PTX wrappers for CTA-pair (cta_group::2) tcgen05 kernels (sm_100a): pair TMA loads that
 // signal the leader's barrier, pair MMA / commit, remote mbarrier arrive, the pair instruction
-// descriptor, and the no-swizzle K-major descriptor of FC1's u1 operand.
+// descriptor (the no-swizzle K-major descriptor of FC1's u1 operand is sdesc_k16_plain in ptx.cuh).
 #pragma once
 #include "ptx.cuh"
 
@@ -8,17 +8,6 @@ namespace cold {
 
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;        // shared::cluster address of the leader's copy
 
-// SMEM descriptor, K-major, no swizzle (the u1 operand): core matrices of 8 rows x 16 B; rows are
-// 16 B apart (one TMA box of 8 x 128), 8-row groups 128 B apart (SBO), K chunks 2 KB apart (LBO).
-// (probe: tools/probes/umma_k16_probe.cu checks the LBO / SBO roles.)
-__device__ __forceinline__ uint64_t sdesc_k16_plain(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)(2048 >> 4) << 16;
-  d |= (uint64_t)(128 >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  return d;                                    // layout type 0 = SWIZZLE_NONE
-}
 
 __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                  uint64_t policy) {
@@ -27,6 +16,19 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar) & PEER_MASK), "l"(policy)
       : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                 int c2, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar) & PEER_MASK), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_a_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int kb, int row,
+                                                uint64_t policy, bool slab) {
+  if (slab) tma_load_3d_pair(dst, map, bar, 0, row, kb * 8, policy);
+  else tma_load_2d_pair(dst, map, bar, kb * 64, row, policy);
 }
 __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                               uint32_t accumulate) {

@@ -64,6 +64,22 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+// X_ac in the half-slab layout ([2 * slab + k half][rows][8 columns]) through a 3-D map: the A
+// tile of k-block kb (64 columns = 8 half-slabs) lands as [8][BM rows][8] = four K = 16 no-swizzle
+// K-major operands (sdesc_k16_plain at +kk * BM * 32)
+__device__ __forceinline__ void tma_load_a(void* dst, const CUtensorMap* map, uint64_t* bar, int kb, int row,
+                                           uint64_t policy, bool slab) {
+  if (slab) tma_load_3d(dst, map, bar, 0, row, kb * 8, policy);
+  else tma_load_2d(dst, map, bar, kb * 64, row, policy);
+}
 // Same box delivered (data + complete_tx) to the same smem offsets of every CTA in `mask`.
 __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                                uint16_t mask, uint64_t policy) {
@@ -127,6 +143,18 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)2 << 61;
   return d;
+}
+
+// K-major, no swizzle, K = 16: core matrices of 8 rows x 16 B; the two 8-column halves 2 KB apart (LBO),
+// consecutive 8-row groups 128 B apart (SBO) — a [2][128 rows][8] tile (the u1 operand, X_ac half-slabs;
+// tools/probes/umma_k16_probe.cu checks the LBO / SBO roles)
+__device__ __forceinline__ uint64_t sdesc_k16_plain(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(2048 >> 4) << 16;
+  d |= (uint64_t)(128 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;                                    // layout type 0 = SWIZZLE_NONE
 }
 
 // Instruction descriptor, kind::f16: D fp32 [4,6)=1, A/B format [7,10)/[10,13) (0 f16, 1 bf16),

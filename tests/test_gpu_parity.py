@@ -125,7 +125,8 @@ _KV = {"tail45": {}, "tail3": {"kernel_flags": 64}, "no_tail": {"kernel_flags": 
        "single_cta_stream_b": {"kernel_flags": 4 | 16}, "span1": {"gather_span_chunks": 1},
        "span3": {"gather_span_chunks": 3}, "layerwise": {"kernel_flags": 1}, "chain_always": {"chain_min_ads": 1},
        "chain_tail": {"kernel_flags": 128, "chain_min_ads": 1}, "layerwise_pair_stream": {"kernel_flags": 1 | 8},
-       "layerwise_no_u1mma": {"kernel_flags": 1 | 2}, "serial_user_no_pdl": {"kernel_flags": 256 | 512}}
+       "layerwise_no_u1mma": {"kernel_flags": 1 | 2}, "serial_user_no_pdl": {"kernel_flags": 256 | 512},
+       "x_rows": {"kernel_flags": 1024}, "x_rows_layerwise": {"kernel_flags": 1024 | 1}}
 
 
 @pytest.mark.parametrize("variant", sorted(_KV))
