@@ -304,15 +304,17 @@ static cold_status make_tmap(CUtensorMap* tm, void* ptr, int precision, uint64_t
   return COLD_OK;
 }
 
-// X_ac half-slab planes [planes][rows_total][8] 16-bit, viewed from chunk row offset `ptr`: 3-D map
-// {8 columns, rows, planes}, box {8, 128, 8} (one 64-column k-block = 8 half-slabs), no swizzle
+// X_ac half-slab planes [planes][rows_total][8] 16-bit, viewed from chunk row offset `ptr`: a 3-D map
+// {256 elements = 32 rows x 8 columns (contiguous in a plane), row group of 32, plane}, box {256, 4, 8} =
+// one 64-column k-block of 128 rows in 512 B lines, landing as [8 planes][128 rows][8] = four no-swizzle
+// K-major K = 16 operands (sdesc_k16_plain at +kk * BM * 32)
 static cold_status make_tmap_slab(CUtensorMap* tm, void* ptr, int precision, uint64_t rows, uint64_t rows_total,
                                   uint64_t planes) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return fail(COLD_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  cuuint64_t dims[3] = {8, rows, planes};
-  cuuint64_t strides[2] = {16, rows_total * 16};
-  cuuint32_t box[3] = {8, 128, 8};
+  cuuint64_t dims[3] = {256, rows / 32, planes};
+  cuuint64_t strides[2] = {512, rows_total * 16};
+  cuuint32_t box[3] = {256, 4, 8};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(tm, precision == COLD_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    3, ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

@@ -27,7 +27,7 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
 }
 __device__ __forceinline__ void tma_load_a_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int kb, int row,
                                                 uint64_t policy, bool slab) {
-  if (slab) tma_load_3d_pair(dst, map, bar, 0, row, kb * 8, policy);
+  if (slab) tma_load_3d_pair(dst, map, bar, 0, row / 32, kb * 8, policy);
   else tma_load_2d_pair(dst, map, bar, kb * 64, row, policy);
 }
 __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,

@@ -72,12 +72,12 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-// X_ac in the half-slab layout ([2 * slab + k half][rows][8 columns]) through a 3-D map: the A
-// tile of k-block kb (64 columns = 8 half-slabs) lands as [8][BM rows][8] = four K = 16 no-swizzle
-// K-major operands (sdesc_k16_plain at +kk * BM * 32)
+// X_ac in the half-slab layout ([2 * slab + k half][rows][8 columns]) through a 3-D map
+// {32 rows x 8 columns, row group, plane}: the A tile of k-block kb (64 columns = planes 8 kb .. 8 kb + 7)
+// lands as [8][BM rows][8] = four no-swizzle K-major K = 16 operands (sdesc_k16_plain at +kk * BM * 32)
 __device__ __forceinline__ void tma_load_a(void* dst, const CUtensorMap* map, uint64_t* bar, int kb, int row,
                                            uint64_t policy, bool slab) {
-  if (slab) tma_load_3d(dst, map, bar, 0, row, kb * 8, policy);
+  if (slab) tma_load_3d(dst, map, bar, 0, row / 32, kb * 8, policy);
   else tma_load_2d(dst, map, bar, kb * 64, row, policy);
 }
 // Same box delivered (data + complete_tx) to the same smem offsets of every CTA in `mask`.
