@@ -36,8 +36,8 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
   // the group, identical in its four warps)
   const bool elected = (q == 0) && (lane == 0);
   // debug timing (tacc != null, lane 0): cycles in [0] TMEM load+wait, [1] math+pack, [2] wait for the
-  // staging buffer, [3] smem writes + fence, [4] store issue
-  long long tc0 = 0, tsum[5] = {0, 0, 0, 0, 0};
+  // staging buffer, [3] smem writes, [4] store issue, [5] proxy fence, [6] group barrier after the writes
+  long long tc0 = 0, tsum[7] = {0, 0, 0, 0, 0, 0, 0};
   auto tick = [&](int k) {
     if (tacc) { const long long t = clock64(); if (k >= 0) tsum[k] += t - tc0; tc0 = t; }
   };
@@ -131,9 +131,11 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
 #pragma unroll
     for (int j = 0; j < 8; j++)
       sts128(rowp + (uint32_t)((j ^ (lane & 7)) << 4), make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]));
-    fence_async_smem();
-    named_bar_sync(1 + h, 128);           // all 128 rows of the box written
     tick(3);
+    fence_async_smem();
+    tick(5);
+    named_bar_sync(1 + h, 128);           // all 128 rows of the box written
+    tick(6);
     if (elected && dbg != 4) {
       // dbg 6 (timing experiment): every box to the same L2-resident location (no DRAM write traffic)
       if (store_policy) tma_store_2d_hint(tmC, gbuf, col0, tile_row0, store_policy);
@@ -143,7 +145,7 @@ __device__ __forceinline__ void epi_store_wide(uint32_t taddr, int c_begin, int 
     tick(4);
   }
   if (tacc && lane == 0)
-    for (int k = 0; k < 5; k++) atomicAdd(tacc + k, (unsigned long long)tsum[k]);
+    for (int k = 0; k < 7; k++) atomicAdd(tacc + k, (unsigned long long)tsum[k]);
 }
 
 }  // namespace cold

@@ -35,6 +35,7 @@ constexpr bool H1_TILES = false;
 #else
 constexpr bool H1_TILES = true;
 #endif
+constexpr bool FC1_DIRECT = false;   // (direct st.global H1 stores from registers: 294 vs 273 us, not adopted)
 constexpr int C_EPI_WARPS = 8;                         // 2 per TMEM lane quadrant, 128 columns each
 constexpr int C_GROUPS = C_EPI_WARPS / 4;              // 4-warp store groups (one 16 KB staging box each)
 constexpr int C_THREADS = 64 + 32 * C_EPI_WARPS;
@@ -314,8 +315,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         }
         const float* slope = l == 0 ? cp.s1 : (l == 1 ? cp.s2 : (l == 2 ? cp.s3 : nullptr));
         epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, bias_s, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
-                             nb * tn[l], trow0, q, h, lane, 0, nullptr, nullptr, 0, 0,
-                             0ull, slope, C_OUT_BOXES == 2 * C_GROUPS ? sOut + (C_GROUPS + h) * EPI_GROUP_BOX : nullptr,
+                             nb * tn[l], trow0, q, h, lane, 0, cp.instr ? cp.instr + 16 + 8 * (l < 3 ? l : 0) : nullptr,
+                             (FC1_DIRECT && l == 0) ? const_cast<void*>(cp.h1) : nullptr, cp.n1, M, 0ull, slope, C_OUT_BOXES == 2 * C_GROUPS ? sOut + (C_GROUPS + h) * EPI_GROUP_BOX : nullptr,
                              &box_ctr);
       }
       tc_fence_before();
@@ -323,7 +324,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
       lt++;
       const bool last_of_layer = nb == ntile[l] - 1;
-      if (H1_TILES && l == 0) {
+      if (FC1_DIRECT && l == 0) {
+        // direct stores: this tile's H1 rows are written once every lane's stores are ordered before the
+        // async-proxy (TMA) reads of FC2
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        named_bar_sync(1 + h, 128);
+        if (lane == 0) mbar_arrive(&h1t[nb]);
+      } else if (H1_TILES && l == 0) {
         // per-tile H1 readiness: tile nb - 1's stores are complete once at most this tile's two group stores
         // are pending (lazy: no wait on the tile just issued); the block's last tile waits for everything
         if (nb > 0) {

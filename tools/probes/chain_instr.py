@@ -43,3 +43,10 @@ for i, n in enumerate(names):
         continue
     div = 74.0 if i in (2, 3, 4) or i >= 6 else ctas
     print(f"  {n}: {v[i] / div / 1e3:.1f} kcycles")
+
+# epilogue sections per layer (sum over the 8 epilogue warps' lane 0, per CTA): TMEM load + wait, math + pack,
+# wait for the staging box, smem writes, store issue, proxy fence, group barrier after the writes
+sec = ["tmem_ld", "math", "box_wait", "sts", "store", "fence", "group_bar"]
+for l in range(3):
+    v = buf[48 + 8 * l:48 + 8 * l + 7].astype(np.float64) / ctas / 8 / 1e3
+    print(f"  epilogue fc{l + 1} per warp (kcycles): " + ", ".join(f"{n} {x:.1f}" for n, x in zip(sec, v)))
