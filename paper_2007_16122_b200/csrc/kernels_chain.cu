@@ -36,11 +36,7 @@ constexpr bool H1_TILES = false;
 constexpr bool H1_TILES = true;
 #endif
 constexpr bool FC1_DIRECT = false;
-#ifdef COLD_CHAIN_FC3_LAST   // A/B: the round-1 order FC1(s) x4 | FC3(s-1) | FC2(s) x2
-constexpr bool FC3_MID = false;
-#else
-constexpr bool FC3_MID = true;
-#endif   // (direct st.global H1 stores from registers: 294 vs 273 us, not adopted)
+constexpr bool FC3_MID = false;   // (FC3 between the FC1 halves: 277.4 vs 272.0 us per chunk, not adopted)   // (direct st.global H1 stores from registers: 294 vs 273 us, not adopted)
 constexpr int C_EPI_WARPS = 8;                         // 2 per TMEM lane quadrant, 128 columns each
 constexpr int C_GROUPS = C_EPI_WARPS / 4;              // 4-warp store groups (one 16 KB staging box each)
 constexpr int C_THREADS = 64 + 32 * C_EPI_WARPS;
@@ -125,9 +121,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   // TAIL: step s = FC1(s) | FC5(s-3) | FC4(s-2) | FC3(s-1) | FC2(s). Every consumer sits several tiles
   // after its producer, and the producer's wait on hready[l](j) always precedes the loads of the task
   // that would complete the barrier's next phase (no parity aliasing).
-  // FC3_MID: FC3(s-1) sits between the first and the second half of FC1(s)'s n-tiles, so FC1's short
-  // (K = 256), epilogue-heavy tiles are not all back to back (their staging-box stores contend for shared
-  // memory with the operand traffic); FC2(s) then starts on H1's first tiles (per-tile readiness)
+  // (FC3_MID would put FC3(s-1) between the two halves of FC1(s)'s n-tiles to spread FC1's epilogue-heavy
+  // tiles: measured slower, off)
   auto for_tasks = [&](auto&& f) {
     for (int s = 0; s <= nrb + (TAIL ? 2 : 0); s++) {
       const int fc1_split = (FC3_MID && !TAIL && s >= 1 && s <= nrb) ? ntile[0] / 2 : ntile[0];
