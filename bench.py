@@ -72,7 +72,8 @@ def parse():
                     help="serving path: the request-coalescing server (cold_server_*) under open-loop Poisson "
                          "arrivals of configs[1]-shaped requests; p50/p99 end-to-end latency and usable rate")
     ap.add_argument("--serve-requests", type=int, default=6000)
-    ap.add_argument("--serve-batch", type=int, default=16, help="max requests coalesced into one call")
+    ap.add_argument("--serve-batch", type=int, default=32, help="max requests coalesced into one call")
+    ap.add_argument("--no-serve", action="store_true", help="skip the serving section of the default line")
     ap.add_argument("--latency-sweep", action="store_true",
                     help="SURVEY §8(d) C2: p50/p95/p99 vs N, multi-stream serving (S contexts sharing one "
                          "parameter copy), fp32 / fp16 / bf16 ads/s (the analogue of Table tab:qps_cuda)")
@@ -592,6 +593,36 @@ def serve_rates(srv, hb, n_ads, rates, seed=11):
     return rows
 
 
+def serve_sweep(ctx, sch, args, n_requests, B, fractions=(0.1, 0.25, 0.5, 0.7, 0.85, 0.95)):
+    """The coalescing server on `ctx` (which it owns until it returns): closed-loop capacity, then open-loop
+    Poisson arrivals at fractions of it; usable rate at p99 <= 1 ms / 10 ms."""
+    from paper_2007_16122_b200 import Batch, Server
+    n = 4000
+    K = args.topk
+    lb = coldgen.make_batch(sch, range(4 * 10**7, 4 * 10**7 + n_requests), n, seed=args.seed + 7)
+    hb = Batch(lb.ad_offsets, lb.ids, lb.offs)
+    srv = Server(ctx, max_batch_requests=B, max_batch_ads=B * n, top_k=K)
+    srv.submit(hb)                        # warm-up (sizes the pinned staging and the library's buffers)
+    srv.drain()
+    t0 = time.monotonic_ns()
+    _, _, done = srv.submit(hb)           # closed loop: everything queued at once
+    calls, reqs = srv.drain()
+    capacity_rps = n_requests / ((done.max() - t0) / 1e9)
+    rows = serve_rates(srv, hb, n, [capacity_rps * f for f in fractions])
+    srv.close()
+    out = {"requests_per_call_max": B, "requests": n_requests, "ads_per_request": n, "top_k": K,
+           "closed_loop": {"ads_per_s": capacity_rps * n, "requests_per_s": capacity_rps, "calls": calls,
+                           "requests_per_call": reqs / max(calls, 1)},
+           "open_loop": rows,
+           "timing": "host CLOCK_MONOTONIC: arrival = the submit time the C replay loop waited for; completion = "
+                     "when the dispatcher published the request's top-K to host memory (ids from host memory, one "
+                     "H2D and one D2H per coalesced call)"}
+    for lim in (1.0, 10.0):
+        ok = [r["offered_rps"] for r in rows if r["p99_ms"] <= lim and not r["failed"]]
+        out[f"usable_ads_per_s_p99_le_{int(lim)}ms"] = (max(ok) if ok else 0.0) * n
+    return out
+
+
 def run_serve(args):
     """Serving path (P:298 / P:690-692: the paper's GPU was idle between small queries until MPS let them
     share it; "usable QPS"): configs[1]-shaped requests (1 user x 4000 ads, S-paper, fp16, top-500)
@@ -600,44 +631,21 @@ def run_serve(args):
     (host ids in, top-K back in host memory). Reports the closed-loop capacity, p50/p99 per offered rate,
     and the usable rate at p99 <= 1 ms / 10 ms."""
     import torch
-    from paper_2007_16122_b200 import Batch, Context, Server
+    from paper_2007_16122_b200 import Context
     torch.cuda.set_device(0)
     sch = schema_for(args)
-    n = 4000
-    K = args.topk
     params = coldgen.make_params(sch, seed=args.seed, precision=args.precision)
     B = args.serve_batch
-    ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, max_ads=B * n, max_requests=B)
+    ctx = Context(sch.groups, sch.k, sch.widths, precision=args.precision, max_ads=B * 4000, max_requests=B)
     load_ctx_params(ctx, params)
-    lb = coldgen.make_batch(sch, range(4 * 10**7, 4 * 10**7 + args.serve_requests), n, seed=args.seed + 7)
-    hb = Batch(lb.ad_offsets, lb.ids, lb.offs)
-    srv = Server(ctx, max_batch_requests=B, max_batch_ads=B * n, top_k=K)
-    srv.submit(hb)                        # warm-up (sizes the pinned staging and the library's buffers)
-    srv.drain()
-    t0 = time.monotonic_ns()
-    _, _, done = srv.submit(hb)           # closed loop: everything queued at once
-    calls, reqs = srv.drain()
-    cap_s = (done.max() - t0) / 1e9
-    capacity_rps = args.serve_requests / cap_s
-    rates = [capacity_rps * f for f in (0.1, 0.25, 0.5, 0.7, 0.85, 0.95)]
-    rows = serve_rates(srv, hb, n, rates)
-    usable = {}
-    for lim in (1.0, 10.0):
-        ok = [r["offered_rps"] for r in rows if r["p99_ms"] <= lim and not r["failed"]]
-        usable[f"usable_rps_p99_le_{int(lim)}ms"] = max(ok) if ok else 0.0
-        usable[f"usable_ads_per_s_p99_le_{int(lim)}ms"] = (max(ok) if ok else 0.0) * n
-    srv.close()
+    sv = serve_sweep(ctx, sch, args, args.serve_requests, B)
     ctx.close()
-    line = {"metric": METRIC, "value": capacity_rps * n, "unit": "ads/s", "n_gpus": 1, "dtype": args.precision,
-            "data": "synthetic (seeded ids, tables, weights)",
-            "config": {"workload": f"serving: {args.serve_requests} requests x {n} ads (BASELINE configs[1] shape), "
-                                   f"S-paper, top-{K}; request-coalescing server, <= {B} requests per call; "
+    line = {"metric": METRIC, "value": sv["closed_loop"]["ads_per_s"], "unit": "ads/s", "n_gpus": 1,
+            "dtype": args.precision, "data": "synthetic (seeded ids, tables, weights)",
+            "config": {"workload": f"serving: {args.serve_requests} requests x 4000 ads (BASELINE configs[1] shape), "
+                                   f"S-paper, top-{args.topk}; request-coalescing server, <= {B} requests per call; "
                                    f"open-loop Poisson arrivals from the host, end-to-end latency"},
-            "closed_loop": {"ads_per_s": capacity_rps * n, "requests_per_s": capacity_rps, "calls": calls,
-                            "requests_per_call": reqs / max(calls, 1)},
-            "open_loop": rows, **usable,
-            "timing": "host CLOCK_MONOTONIC: arrival = the submit time the C replay loop waited for; completion = "
-                      "when the dispatcher published the request's top-K to host memory"}
+            **sv}
     print(json.dumps(line), flush=True)
 
 
@@ -1172,6 +1180,14 @@ def main():
         except Exception as exc:   # optional section: report, keep the headline line
             latency_split = {"error": f"{type(exc).__name__}: {exc}"}
 
+    # ---- serving: the coalescing server (D-13) on this context, configs[1]-shaped requests, open loop ----
+    serve = None
+    if rank == 0 and world == 1 and not args.no_latency and not args.no_serve:
+        try:
+            serve = serve_sweep(ctx, sch, args, 2000, args.serve_batch, fractions=(0.25, 0.5, 0.75, 0.9))
+        except Exception as exc:   # optional section: report, keep the headline line
+            serve = {"error": f"{type(exc).__name__}: {exc}"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_oracle_sample(sch, params, batch)
@@ -1184,7 +1200,7 @@ def main():
             "config": config_dict(args, sch, world),
             "roofline": roofline, "roofline_gather": roofline_gather, "fc_stack": fc_stack,
             "kernels": classes, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
-            "clocks": clocks, "latency": latency, "latency_split": latency_split, "setup_s": setup_s,
+            "clocks": clocks, "latency": latency, "latency_split": latency_split, "serve": serve, "setup_s": setup_s,
             "compressed_activations": bool(info.get("compressed_activations", 0)),
             "profiled_region": {"ms_per_step": ms_prof / args.steps,
                                 "note": "per-kernel CUDA events (kernels, roofline) come from this second timed "
