@@ -339,7 +339,8 @@ void cold_server_destroy(cold_server* server);
  * request, keys; as cold_topk) is written to idx_out / key_out [r * K .. r * K + K) (host), after which
  * done_ns[r] receives the completion time (CLOCK_MONOTONIC ns; -1 if its call failed), stored with
  * release semantics; done_ns[r] is 0 until then. The batch arrays and the outputs must stay valid until
- * cold_server_drain returns. Errors (nothing enqueued): COLD_ERR_INVALID_ARG, COLD_ERR_K_RANGE (a request
+ * cold_server_drain returns. Errors (nothing enqueued): COLD_ERR_INVALID_ARG (also for device-memory arrays:
+ * the dispatcher copies request slices on the CPU), COLD_ERR_K_RANGE (a request
  * with fewer than K ads), COLD_ERR_CAPACITY (a request larger than max_batch_ads). */
 cold_status cold_server_submit(cold_server* server, const cold_batch* requests, const int64_t* arrival_ns,
                                int32_t* idx_out, float* key_out, int64_t* done_ns);

@@ -363,6 +363,15 @@ extern "C" cold_status cold_server_submit(cold_server* s, const cold_batch* reqs
     if (n < K) return COLD_ERR_K_RANGE;
     if (n > s->cfg.max_batch_ads) return COLD_ERR_CAPACITY;
   }
+  {   // the dispatcher copies the requests' slices on the CPU: every array must be host memory
+    auto on_device = [](const void* p) {
+      cudaPointerAttributes at;
+      if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+      return at.type == cudaMemoryTypeDevice;
+    };
+    for (size_t g = 0; g < s->groups.size(); g++)
+      if (on_device(reqs->ids[g]) || on_device(reqs->offs[g])) return COLD_ERR_INVALID_ARG;
+  }
   for (size_t g = 0; g < s->groups.size(); g++) {   // bag groups need host offsets (the server copies slices)
     const cold_group& G = s->groups[g];
     if (reqs->ids[g] && (G.side == COLD_USER || (G.side == COLD_AD && G.pooled)) &&

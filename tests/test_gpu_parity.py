@@ -812,4 +812,7 @@ def test_server_coalesced_results_equal_direct_calls():
     with pytest.raises(ColdError) as e:
         srv.submit(Batch(small.ad_offsets, small.ids, small.offs))
     assert e.value.name == "COLD_ERR_K_RANGE"
+    with pytest.raises(ColdError) as e:                                    # device arrays: refused
+        srv.submit(device_batch(coldgen.sub_batch(batch, [0])))
+    assert e.value.name == "COLD_ERR_INVALID_ARG"
     srv.close()
