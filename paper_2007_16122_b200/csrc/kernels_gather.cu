@@ -701,11 +701,7 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
       else if (sizeof(T) == 2 && a.ring == 5) gather_kernel<T, 16, FAST, 8, 4, 5><<<grid, 128, 5 * 4096, s>>>(a);
       else if (sizeof(T) == 2 && a.ring == 8) gather_kernel<T, 16, FAST, 6, 4, 8><<<grid, 128, 8 * 4096, s>>>(a);
       else if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
-#ifdef COLD_REST_APT8   // A/B: the non-bag columns with 8 ads (8 rows in flight) per thread at 6 CTAs/SM
-      else gather_kernel<T, 16, FAST, 6, 8><<<grid_for(8), 128, 0, s>>>(a);
-#else
-      else gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);
-#endif
+      else gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);   // (8 ads per thread at 6 CTAs/SM: 14% slower)
       break;
     }
     case 32: gather_kernel<T, 32, FAST><<<grid, 128, 0, s>>>(a); break;
