@@ -111,6 +111,10 @@ struct cold_ctx {
   CUtensorMap tmU1T;
   bool chain_tail = false;           // FC4 -> FC5 -> head inside the chain kernel too
   CUtensorMap tmW4h, tmW5h;          // W4 / W5 with half-N boxes (CTA-pair tiles)
+  // small calls (below chain_min: one request) run FC3 -> FC4 -> FC5 -> head in the one-CTA tail kernel
+  // instead of the FC3 pair GEMM + tail45 (one launch fewer and 32 CTAs instead of 16 pairs for FC3)
+  bool lat_tail3 = false;
+  CUtensorMap tmW3full;              // W3 with whole-N boxes for that kernel
   std::vector<CUtensorMap> tmOH;     // per chunk slot of the span
   int gspan = 1;                     // chunks per column-wise gather pass (X_ac holds gspan * chunk rows)
   int gather_ring = 0;               // > 0: cross-bag columns through a cp.async ring of this depth
@@ -570,6 +574,8 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     // resident-weight tail kernel (N = 128 / 64 pair tiles, larger live L2 set), so off by default
     c->chain_tail = c->chain && chain_tail_supported(c->widths[3], c->widths[4], c->widths[2]) &&
                     c->widths[5] <= 2 && (c->kflags & COLD_K_CHAIN_TAIL) && !c->prelu;
+    c->lat_tail3 = !c->chain_tail && !c->prelu && !(c->kflags & COLD_K_LAT_TAIL45) &&
+                   tail_supported(c->widths[2], c->widths[3], c->widths[4], c->widths[1]);
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       [&] {   // the user kernel is on the latency path's critical chain: highest stream priority
@@ -656,6 +662,7 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
   }
   c->tmW4h = src->tmW4h;
   c->tmW5h = src->tmW5h;
+  c->tmW3full = src->tmW3full;
   *out = c;
   return COLD_OK;
 }
@@ -838,6 +845,10 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
       s = make_tmap(&c->tmB[l], c->d_w[l], c->precision, Kp, out,
                     c->pair[l] ? c->bn[l] / 2 : c->bn[l] / c->cs[l]);
       if (s) return s;
+      if (c->lat_tail3 && l == 2) {   // whole-N boxes for the small-call FC3-FC5 tail kernel
+        s = make_tmap(&c->tmW3full, c->d_w[l], c->precision, Kp, out, c->bn[l]);
+        if (s) return s;
+      }
       if (c->chain_tail && (l == 3 || l == 4)) {   // half-N boxes for the chain's pair tiles
         s = make_tmap(l == 3 ? &c->tmW4h : &c->tmW5h, c->d_w[l], c->precision, Kp, out, out / 2);
         if (s) return s;
@@ -1207,6 +1218,9 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
 #else
   const bool instr_on = false;
 #endif
+  // small calls: FC1, FC2 as pair GEMMs, then FC3 -> FC4 -> FC5 -> head in the one-CTA tail kernel
+  const bool lat3 = c->lat_tail3 && n_gemm == c->L - 1 - c->n_tail && n < c->chain_min;
+  if (lat3) n_gemm = c->L - 4;
   for (int l = 0; l < n_gemm; l++) {
     EpiParams ep;
     memset(&ep, 0, sizeof(ep));
@@ -1244,6 +1258,23 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
       launch_gemm(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
                   c->precision == COLD_BF16 ? 1 : 0, c->cs[l], c->resb[l], ep, c->num_sms, c->pdl && !c->prof, st);
     c->mark_end(COLD_PROF_FC + l, st, c->layer_flop(l, head ? c->L : l + 1, n));
+  }
+  if (lat3) {
+    const int l3 = c->L - 4;
+    TailParams tp;
+    memset(&tp, 0, sizeof(tp));
+    tp.b3 = c->d_b[l3];
+    tp.b4 = c->d_b[l3 + 1];
+    tp.b5 = c->d_b[l3 + 2];
+    tp.head_w = c->d_head_w;
+    tp.head_b = c->d_head_b;
+    tp.head_n = c->widths[c->L - 1];
+    tp.scores = scores_out;
+    c->mark_begin(st);
+    launch_tail(tmA_of(l3), &c->tmW3full, &c->tmB[l3 + 1], &c->tmB[l3 + 2], (int)n, c->widths[l3 - 1],
+                c->precision == COLD_BF16 ? 1 : 0, tp, c->num_sms, c->pdl && !c->prof, st);
+    c->mark_end(COLD_PROF_TAIL, st, c->layer_flop(l3, c->L, n));
+    return;
   }
   if (c->tail_mode == 2) {
     const int l4 = c->L - 3;

@@ -18,6 +18,7 @@ constexpr int TOPK_STAGE = 12288;   // keys of a segment staged in shared memory
 __device__ __forceinline__ uint32_t orderable(float f) {
   uint32_t u = __float_as_uint(f);
   if ((u & 0x7fffffffu) > 0x7f800000u) return 0u;       // NaN ranks last
+  if ((u & 0x7fffffffu) == 0u) u = 0u;                  // -0 == +0 (a tie, resolved by position)
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 __device__ __forceinline__ float from_orderable(uint32_t o) {
@@ -171,8 +172,211 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Register-resident top-K for segments of <= 512 * KPT keys and K <= 512 (the latency path: one
+// 4,000-ad request). The radix kernel above is issue-bound on its single SM there (~20 us: one CTA,
+// 1024 threads; ncu r03d). Same result, bit for bit, in a fifth of the instructions:
+//   * 512 threads; thread t owns positions t*KPT .. t*KPT+KPT-1 (blocked: thread order = position order);
+//   * radix select with 4-bit digits and no atomics: each thread counts its keys per digit in 4-bit
+//     fields of a 64-bit word (one shift-add per key, <= 8 keys per word), widens them to 16-bit
+//     fields, a warp sums them with __reduce_add_sync, lane 0 publishes 8 words; after a barrier warp 0
+//     sums the 16 warps' counts per bin (lane = bin), finds the digit with a 16-lane scan + ballot and
+//     publishes it (second barrier; the per-round buffers alternate); stops as soon as every key that
+//     matches the prefix is needed;
+//   * launched as a programmatic dependent of the scoring kernels (PDL): its launch overlaps their tail;
+//   * collect: keys above the prefix in any order, keys equal to it by ascending position (one
+//     block-wide exclusive scan of the packed (gt, eq) counts);
+//   * bitonic sort of the <= 512 composites (key << 32 | ~position), descending, one per thread:
+//     strides < 32 by warp shuffles, larger strides through shared memory (double-buffered).
+constexpr int TOPK_SMALL_THREADS = 512;
+constexpr int TOPK_SMALL_MAX_K = TOPK_SMALL_THREADS;
+
+template <int KPT>
+__global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs a) {
+  constexpr int NW = TOPK_SMALL_THREADS / 32;
+  constexpr int NC = (KPT + 7) / 8;                   // 64-bit nibble counters (<= 8 keys each: no carry)
+  __shared__ __align__(16) uint32_t wcnt[2][NW][8];   // per-warp digit counts (bin b: word b/2, half b%2)
+  __shared__ uint32_t wtot[NW];                       // per-warp packed (gt << 16 | eq) totals
+  __shared__ uint4 sres[2];                           // per round: digit, its count, count above it
+  __shared__ unsigned long long sbuf[2][TOPK_SMALL_THREADS];
+  const int r = blockIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: the scores of the previous kernel
+  const int64_t base = a.ad_offsets[r];
+  const int n = (int)(a.ad_offsets[r + 1] - base);
+  const int K = a.K;
+  constexpr unsigned FULL = 0xffffffffu;
+
+  uint32_t u[KPT];
+  uint32_t valid = 0;
+  {
+    float v[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      const int p = t * KPT + j;
+      v[j] = p < n ? a.scores[base + p] : 0.0f;
+    }
+    if (a.bids) {
+#pragma unroll
+      for (int j = 0; j < KPT; j++) {
+        const int p = t * KPT + j;
+        if (p < n) v[j] *= a.bids[base + p];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KPT; j++) {
+      u[j] = orderable(v[j]);
+      if (t * KPT + j < n) valid |= 1u << j;
+    }
+  }
+
+  // ---- radix select (4-bit digits, MSB first) ----
+  uint32_t P = 0, mask = 0, need = (uint32_t)K;
+  int round = 0;
+  for (int shift = 28; shift >= 0; shift -= 4, round++) {
+    unsigned long long nib[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) nib[c] = 0ull;
+#pragma unroll
+    for (int j = 0; j < KPT; j++)
+      if (((valid >> j) & 1u) && (u[j] & mask) == P) nib[j / 8] += 1ull << (((u[j] >> shift) & 15u) << 2);
+    uint32_t pk[8];   // word w: bins 2w (low half) and 2w + 1 (high half)
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int c = 0; c < NC; c++) {
+        const uint32_t byte = (uint32_t)(nib[c] >> (8 * w)) & 0xffu;
+        x += (byte & 15u) | ((byte >> 4) << 16);
+      }
+      pk[w] = __reduce_add_sync(FULL, x);
+    }
+    uint32_t (*buf)[8] = wcnt[round & 1];
+    if (lane == 0) {
+      reinterpret_cast<uint4*>(buf[warp])[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      reinterpret_cast<uint4*>(buf[warp])[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      // lane l < 16 sums bin 15 - l over the warps; inclusive scan from the top bin; the first lane whose
+      // running count reaches `need` holds the digit
+      const int b = 15 - (lane & 15);
+      uint32_t cb = 0;
+      if (lane < 16) {
+#pragma unroll
+        for (int w = 0; w < NW; w++) cb += (buf[w][b >> 1] >> ((b & 1) << 4)) & 0xffffu;
+      }
+      uint32_t cum = cb;
+#pragma unroll
+      for (int off = 1; off < 16; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, cum, off);
+        if ((lane & 15) >= off) cum += y;
+      }
+      const unsigned hit = __ballot_sync(FULL, lane < 16 && cum >= need);
+      const int ls = __ffs(hit) - 1;
+      if (lane == ls) sres[round & 1] = make_uint4((uint32_t)(15 - ls), cb, cum - cb, 0u);
+    }
+    __syncthreads();
+    const uint4 res = sres[round & 1];
+    const uint32_t csel = res.y;
+    need -= res.z;
+    P |= res.x << shift;
+    mask |= 15u << shift;
+    if (csel == need) break;   // every key matching the prefix is a winner: no need to resolve further
+  }
+
+  // ---- collect: keys above the prefix (any order), then the first `need` keys on it by position ----
+  const uint32_t n_gt = (uint32_t)K - need;
+  uint32_t cnt = 0;   // packed (gt << 16) | eq for this thread
+#pragma unroll
+  for (int j = 0; j < KPT; j++) {
+    if ((valid >> j) & 1u) {
+      const uint32_t m = u[j] & mask;
+      cnt += m > P ? (1u << 16) : (m == P ? 1u : 0u);
+    }
+  }
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(FULL, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  uint32_t wbase;
+  {
+    const uint32_t c = lane < NW ? wtot[lane] : 0u;
+    uint32_t wi = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, wi, off);
+      if (lane >= off) wi += y;
+    }
+    wbase = __shfl_sync(FULL, wi - c, warp);
+  }
+  const uint32_t excl = wbase + incl - cnt;
+  uint32_t gslot = excl >> 16, erank = excl & 0xffffu;
+  unsigned long long* cand = sbuf[0];
+#pragma unroll
+  for (int j = 0; j < KPT; j++) {
+    if ((valid >> j) & 1u) {
+      const uint32_t m = u[j] & mask;
+      const unsigned long long comp = ((unsigned long long)u[j] << 32) | (0xffffffffu - (uint32_t)(t * KPT + j));
+      if (m > P) cand[gslot++] = comp;
+      else if (m == P) {
+        if (erank < need) cand[n_gt + erank] = comp;
+        erank++;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- bitonic sort of the P2 = pow2 >= K composites, descending (threads >= P2 sort padding) ----
+  int P2 = 1;
+  while (P2 < K) P2 <<= 1;
+  unsigned long long x = t < K ? cand[t] : 0ull;
+  int cur = 1;   // sbuf[0] holds the candidates; the first exchange writes sbuf[1]
+  for (int size = 2; size <= P2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      unsigned long long y;
+      if (stride >= 32) {
+        sbuf[cur][t] = x;
+        __syncthreads();
+        y = sbuf[cur][t ^ stride];
+        cur ^= 1;
+      } else {
+        y = __shfl_xor_sync(FULL, x, stride);
+      }
+      // keep the larger of the pair where the lower index of a descending block (or the upper index
+      // of an ascending one) sits
+      const bool keep_hi = ((t & stride) == 0) == ((t & size) == 0);
+      x = (keep_hi == (x > y)) ? x : y;
+    }
+  }
+  if (t < K) {
+    a.idx[(int64_t)r * K + t] = (int32_t)(0xffffffffu - (uint32_t)(x & 0xffffffffu));
+    a.key[(int64_t)r * K + t] = from_orderable((uint32_t)(x >> 32));
+  }
+}
+
 void launch_topk(const TopkArgs& a0, cudaStream_t s) {
   TopkArgs a = a0;
+  if (a.G == 0 && a.K <= TOPK_SMALL_MAX_K && a.max_n > 0 && a.max_n <= 24 * TOPK_SMALL_THREADS) {
+    auto kern = a.max_n <= 8 * TOPK_SMALL_THREADS    ? topk_small_kernel<8>
+                : a.max_n <= 16 * TOPK_SMALL_THREADS ? topk_small_kernel<16>
+                                                     : topk_small_kernel<24>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.R);
+    cfg.blockDim = dim3(TOPK_SMALL_THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, a);
+    return;
+  }
   int P = 1;
   while (P < a.K) P <<= 1;
   a.stage = (a.max_n > 0 && a.max_n <= TOPK_STAGE) ? a.max_n : 0;

@@ -126,7 +126,8 @@ _KV = {"tail45": {}, "tail3": {"kernel_flags": 64}, "no_tail": {"kernel_flags": 
        "span3": {"gather_span_chunks": 3}, "layerwise": {"kernel_flags": 1}, "chain_always": {"chain_min_ads": 1},
        "chain_tail": {"kernel_flags": 128, "chain_min_ads": 1}, "layerwise_pair_stream": {"kernel_flags": 1 | 8},
        "layerwise_no_u1mma": {"kernel_flags": 1 | 2}, "serial_user_no_pdl": {"kernel_flags": 256 | 512},
-       "x_rows": {"kernel_flags": 1024}, "x_rows_layerwise": {"kernel_flags": 1024 | 1}}
+       "x_rows": {"kernel_flags": 1024}, "x_rows_layerwise": {"kernel_flags": 1024 | 1},
+       "lat_tail45": {"kernel_flags": 2048}}
 
 
 @pytest.mark.parametrize("variant", sorted(_KV))
@@ -257,6 +258,43 @@ def test_topk_exact_on_same_keys():
             oidx, okey = oracle.topk_batch(ecpm, ao2, K)
             np.testing.assert_array_equal(idx, oidx)
             np.testing.assert_array_equal(key.astype(np.float64), okey.astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("n_list", [
+    [1, 31, 32, 33, 1024, 1025, 4095, 4096],        # register-resident kernel, 8 keys per thread (<= 4096)
+    [4097, 8192, 33],                               # 16 keys per thread
+    [8193, 12288, 2],                               # 24 keys per thread
+    [12289, 600],                                   # radix kernel (longest segment > 12,288)
+])
+def test_topk_size_classes_and_degenerate_keys(n_list):
+    """The register-resident top-K (segments <= 12,288 ads, K <= 512) and the radix kernel agree with
+    the oracle's full sort at every size-class boundary, for K from 1 to 1025, with
+    all-equal keys, all-NaN segments, negative and signed-zero keys (ties by position, AMB-13)."""
+    rng = np.random.default_rng(sum(n_list))
+    ao = np.zeros(len(n_list) + 1, np.int32)
+    ao[1:] = np.cumsum(n_list)
+    N = int(ao[-1])
+    base = rng.standard_normal(N).astype(np.float32)
+    variants = {
+        "normal": base,
+        "ties": np.round(rng.random(N), 2).astype(np.float32),
+        "equal": np.full(N, 0.25, np.float32),
+        "nan": np.where(rng.random(N) < 0.5, np.float32(np.nan), base).astype(np.float32),
+        "zeros": np.where(rng.random(N) < 0.5, np.float32(-0.0), np.float32(0.0)).astype(np.float32),
+    }
+    variants["nan"][ao[0]:ao[1]] = np.nan          # one all-NaN segment
+    sch, params, _ = small_case("tiny", precision="f32")
+    ctx = make_ctx(sch, params, max_requests=64, max_ads=1 << 15)
+    min_n = min(n_list)
+    for name, keys in variants.items():
+        for K in sorted({min(k, min_n) for k in (1, 2, 7, 64, 500, 512, 513, 1024, 1025)}):
+            idx, key = gpu_topk(ctx, keys, ao, K)
+            oidx, okey = oracle.topk_batch(keys.astype(np.float64), ao, K)
+            np.testing.assert_array_equal(idx, oidx, err_msg=f"{name} K={K}")
+            np.testing.assert_array_equal(np.isnan(key), np.isnan(okey), err_msg=f"{name} K={K}")
+            ok = ~np.isnan(okey)
+            np.testing.assert_array_equal(key[ok].astype(np.float64), okey[ok], err_msg=f"{name} K={K}")
+    ctx.close()
 
 
 def test_topk_vs_oracle_scores_within_tolerance():
