@@ -86,6 +86,7 @@ enum { COLD_RELU = 0, COLD_PRELU = 1 };
 #define COLD_K_NO_PDL     512u   /* no programmatic dependent launch between the kernels */
 #define COLD_K_X_ROWS    1024u   /* X_ac row-major (512 B rows) instead of the half-slab layout */
 #define COLD_K_LAT_TAIL45 2048u  /* small calls (below chain_min_ads): FC3 pair GEMM + tail45 instead of the FC3-FC5 tail kernel */
+#define COLD_K_LAT_FC2_256 4096u /* small calls: FC2 as 256-wide pair tiles instead of 128-wide ones */
 
 /* A feature group ("the embedding of the i-th feature group e_i"). */
 typedef struct {

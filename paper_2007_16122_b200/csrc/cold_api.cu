@@ -115,6 +115,9 @@ struct cold_ctx {
   // instead of the FC3 pair GEMM + tail45 (one launch fewer and 32 CTAs instead of 16 pairs for FC3)
   bool lat_tail3 = false;
   CUtensorMap tmW3full;              // W3 with whole-N boxes for that kernel
+  // small calls also run FC2 as 128-wide pair tiles (twice the CTA pairs of the 256-wide tiles)
+  bool lat_fc2_128 = false;
+  CUtensorMap tmW2q;                 // W2 with 64-row boxes (half of a 128-wide pair tile)
   std::vector<CUtensorMap> tmOH;     // per chunk slot of the span
   int gspan = 1;                     // chunks per column-wise gather pass (X_ac holds gspan * chunk rows)
   int gather_ring = 0;               // > 0: cross-bag columns through a cp.async ring of this depth
@@ -576,6 +579,7 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
                     c->widths[5] <= 2 && (c->kflags & COLD_K_CHAIN_TAIL) && !c->prelu;
     c->lat_tail3 = !c->chain_tail && !c->prelu && !(c->kflags & COLD_K_LAT_TAIL45) &&
                    tail_supported(c->widths[2], c->widths[3], c->widths[4], c->widths[1]);
+    c->lat_fc2_128 = c->lat_tail3 && c->widths[1] % 128 == 0 && !(c->kflags & COLD_K_LAT_FC2_256);
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       [&] {   // the user kernel is on the latency path's critical chain: highest stream priority
@@ -663,6 +667,7 @@ extern "C" cold_status cold_ctx_clone(cold_ctx* src, cold_ctx** out) {
   c->tmW4h = src->tmW4h;
   c->tmW5h = src->tmW5h;
   c->tmW3full = src->tmW3full;
+  c->tmW2q = src->tmW2q;
   *out = c;
   return COLD_OK;
 }
@@ -847,6 +852,10 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
       if (s) return s;
       if (c->lat_tail3 && l == 2) {   // whole-N boxes for the small-call FC3-FC5 tail kernel
         s = make_tmap(&c->tmW3full, c->d_w[l], c->precision, Kp, out, c->bn[l]);
+        if (s) return s;
+      }
+      if (c->lat_fc2_128 && l == 1) {   // 64-row boxes for the small-call 128-wide FC2 pair tiles
+        s = make_tmap(&c->tmW2q, c->d_w[l], c->precision, Kp, out, 64);
         if (s) return s;
       }
       if (c->chain_tail && (l == 3 || l == 4)) {   // half-N boxes for the chain's pair tiles
@@ -1249,8 +1258,9 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
     const int K = (l == 0) ? c->d_ac_pad : c->widths[l - 1];
     ep.instr = instr_on ? g_instr + 8 * l : nullptr;
     c->mark_begin(st);
+    const bool q128 = lat3 && l == 1 && c->lat_fc2_128 && c->pair[l];
     if (c->pair[l])
-      launch_gemm_pair(tmA_of(l), &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, c->bn[l],
+      launch_gemm_pair(tmA_of(l), q128 ? &c->tmW2q : &c->tmB[l], &c->tmC[l], (int)n, c->widths[l], K, q128 ? 128 : c->bn[l],
                        c->precision == COLD_BF16 ? 1 : 0, ep, c->num_sms, c->pdl && !c->prof, st,
                        (l == 0 && c->u1mma) ? &c->tmOH[xslot] : nullptr, (l == 0 && c->u1mma) ? &c->tmU1T : nullptr,
                        c->pair_res[l]);

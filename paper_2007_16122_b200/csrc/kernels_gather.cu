@@ -65,7 +65,8 @@ __device__ __forceinline__ int64_t checked(int64_t id, int64_t card, int validat
 // user side: grid = (R requests, S output slices), block = 256 threads. Every CTA of a request pools
 // the request's user groups (cheap: ~84 rows); the CTA with blockIdx.y == 0 also writes x_u, the
 // ad -> request map, statistics and debug outputs. The hoisted GEMV u1 = b1 + W1_u x_u is split over
-// the S CTAs (S > 1 when few requests are in flight: the single-request latency path).
+// the S CTAs in 64-output passes (S > 1, up to 16, when few requests are in flight: the single-request
+// latency path).
 // Bag pooling: the warp loads up to 32 rows of a bag in parallel (one row per lane, 256-bit), stages
 // them in shared memory and lane d sums dimension d sequentially in bag order (the fp32 order the
 // oracle's fp32-ordered mode defines), instead of a dependent id -> row chain per bag element.
@@ -143,39 +144,59 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
   }
   __syncthreads();
   // u1[r][o] = b1[o] + sum_i W1u[o][i] x_u[i]   (W1u stored transposed: coalesced over o)
-  const int ostep = blockDim.x * gridDim.y;
-  for (int o = blockIdx.y * blockDim.x + threadIdx.x; o < a.H && !a.stats; o += ostep) {
-    float acc = a.b1[o];
-    if (!a.dense) {   // dense SE: W1's user columns run inside FC1 with the gated per-ad x (u1 = b1)
-      // 16 independent weight loads in flight per step (the loop was latency-bound: one L2 round trip
-      // per few FMAs); the accumulation order is unchanged
-      int i = 0;
-      for (; i + 16 <= d_u; i += 16) {
-        float w[16];
+  // 64 outputs per pass, 4 threads per output: thread part q sums inputs [q*P, q*P + P) (up to 32 weight
+  // loads in flight, one L2 round trip instead of d_u / 16 dependent ones), then the four partial sums
+  // are added in part order through shared memory. The order is fixed, so u1 does not depend on the
+  // slice count or on the other requests of the call.
+  float* part = stage;   // [4][64] partial sums (reuses the pooling stage)
+  const int q = threadIdx.x >> 6, ol = threadIdx.x & 63;
+  const int P = (d_u + 3) / 4;
+  const int i0 = min(q * P, d_u), i1 = min(i0 + P, d_u);
+  const int npass = (a.H + 63) / 64;
+  for (int pass = blockIdx.y; pass < npass && !a.stats; pass += gridDim.y) {
+    const int o = pass * 64 + ol;
+    float acc = 0.0f;
+    if (!a.dense && o < a.H) {   // dense SE: W1's user columns run inside FC1 with the gated per-ad x (u1 = b1)
+      int i = i0;
+      for (; i + 32 <= i1; i += 32) {
+        float w[32];
 #pragma unroll
-        for (int j = 0; j < 16; j++) w[j] = __ldg(a.w1u_t + (int64_t)(i + j) * a.H + o);
+        for (int j = 0; j < 32; j++) w[j] = __ldg(a.w1u_t + (int64_t)(i + j) * a.H + o);
 #pragma unroll
-        for (int j = 0; j < 16; j++) acc = fmaf(w[j], xs[i + j], acc);
+        for (int j = 0; j < 32; j++) acc = fmaf(w[j], xs[i + j], acc);
       }
-      for (; i < d_u; i++) acc = fmaf(a.w1u_t[(int64_t)i * a.H + o], xs[i], acc);
+      for (; i + 8 <= i1; i += 8) {
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) w[j] = __ldg(a.w1u_t + (int64_t)(i + j) * a.H + o);
+#pragma unroll
+        for (int j = 0; j < 8; j++) acc = fmaf(w[j], xs[i + j], acc);
+      }
+      for (; i < i1; i++) acc = fmaf(__ldg(a.w1u_t + (int64_t)i * a.H + o), xs[i], acc);
     }
-    a.u1[(int64_t)r * a.H + o] = acc;
-    if (a.u1t) {   // u1 = term_0 + term_1 (+ term_2), each RNE in 16 bits: the FC1 tensor-core operand
-      float u = acc;
-      for (int t = 0; t < a.u1_terms; t++) {
-        uint16_t bits;
-        if (a.bf16) {
-          const __nv_bfloat16 q = __float2bfloat16_rn(u);
-          bits = __bfloat16_as_ushort(q);
-          u -= __bfloat162float(q);
-        } else {
-          const __half q = __float2half_rn(u);
-          bits = __half_as_ushort(q);
-          u -= __half2float(q);
+    part[q * 64 + ol] = acc;
+    __syncthreads();
+    if (q == 0 && o < a.H) {
+      acc = a.b1[o] + part[ol] + part[64 + ol] + part[128 + ol] + part[192 + ol];
+      a.u1[(int64_t)r * a.H + o] = acc;
+      if (a.u1t) {   // u1 = term_0 + term_1 (+ term_2), each RNE in 16 bits: the FC1 tensor-core operand
+        float u = acc;
+        for (int t = 0; t < a.u1_terms; t++) {
+          uint16_t bits;
+          if (a.bf16) {
+            const __nv_bfloat16 qq = __float2bfloat16_rn(u);
+            bits = __bfloat16_as_ushort(qq);
+            u -= __bfloat162float(qq);
+          } else {
+            const __half qq = __float2half_rn(u);
+            bits = __half_as_ushort(qq);
+            u -= __half2float(qq);
+          }
+          a.u1t[((int64_t)t * a.H + o) * a.u1t_ld + r] = bits;
         }
-        a.u1t[((int64_t)t * a.H + o) * a.u1t_ld + r] = bits;
       }
     }
+    __syncthreads();
   }
   if (main_cta) {   // bounds in registers: the stores may alias ad_offsets, which would reload it per step
     const int64_t e0 = a.ad_offsets[r], e1 = a.ad_offsets[r + 1];
@@ -456,7 +477,9 @@ __global__ void __launch_bounds__(128, MINB) gather_kernel(GatherArgs a) {
   constexpr int NV = K * (int)sizeof(T) / 16;
   // bag rows in flight per thread (<= 16 vectors of raw registers; halved when the register budget
   // is halved for twice the resident warps)
-  constexpr int GATHER_RB = (NV <= 2 ? 8 : (NV == 4 ? 4 : 2)) / (MINB >= 12 ? 4 : (MINB >= 8 ? 2 : 1));
+  // (MINB <= 2, the single-request latency build: a whole 16-row bag in flight per thread)
+  constexpr int GATHER_RB = MINB <= 2 && NV <= 2 ? 16
+                          : (NV <= 2 ? 8 : (NV == 4 ? 4 : 2)) / (MINB >= 12 ? 4 : (MINB >= 8 ? 2 : 1));
   __shared__ uint64_t s_hx[2][HX_HALF];
 #ifdef COLD_GATHER_PAD_SMEM   // A/B: the static shared footprint of the round-1 build (5376 B)
   __shared__ uint8_t s_pad[1280];
@@ -660,7 +683,7 @@ template <typename T>
 static void user_dispatch(const UserArgs& a, int R, cudaStream_t s) {
   const size_t smem = ((size_t)a.n_user * a.k + 4) * sizeof(float) + (size_t)8 * 32 * a.k * sizeof(float);
   // few requests (the latency path): split the u1 GEMV over up to 4 CTAs per request
-  const int slices = R >= 64 ? 1 : std::min(4, std::max(1, (a.H + 255) / 256));
+  const int slices = R >= 64 ? 1 : std::min(16, std::max(1, (a.H + 63) / 64));
   const dim3 grid((unsigned)R, (unsigned)slices);
   switch (a.k) {
     case 2: user_kernel<T, 2><<<grid, 256, smem, s>>>(a); break;
@@ -700,7 +723,17 @@ static void gather_dispatch(const GatherArgs& a, cudaStream_t s) {
       else if (sizeof(T) == 2 && a.ring == 4) gather_kernel<T, 16, FAST, 8, 4, 4><<<grid, 128, 4 * 4096, s>>>(a);
       else if (sizeof(T) == 2 && a.ring == 5) gather_kernel<T, 16, FAST, 8, 4, 5><<<grid, 128, 5 * 4096, s>>>(a);
       else if (sizeof(T) == 2 && a.ring == 8) gather_kernel<T, 16, FAST, 6, 4, 8><<<grid, 128, 8 * 4096, s>>>(a);
-      else if (a.n < 148 * 128 * 4) gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);   // latency path
+      else if (a.n < 148 * 128 * 4) {   // latency path: one ad per thread
+        // 8 bag rows in flight per thread at 4 CTAs per SM: p50 63.0 us at 4000 ads, vs 4 rows at 8 CTAs/SM
+        // 67.9 and a whole 16-row bag at 2 CTAs/SM 64.8 (profiles/r03/lat_ab_r03g_*.jsonl)
+#if defined(COLD_GATHER_LAT_RB4)   // A/B: 4 bag rows in flight per thread (round-2 latency build)
+        gather_kernel<T, 16, FAST, 8, 1><<<grid_for(1), 128, 0, s>>>(a);
+#elif defined(COLD_GATHER_LAT_RB16)   // A/B: 16 rows in flight, 2 CTAs per SM
+        gather_kernel<T, 16, FAST, 2, 1><<<grid_for(1), 128, 0, s>>>(a);
+#else
+        gather_kernel<T, 16, FAST, 4, 1><<<grid_for(1), 128, 0, s>>>(a);
+#endif
+      }
       else gather_kernel<T, 16, FAST, 8><<<grid, 128, 0, s>>>(a);   // (8 ads per thread at 6 CTAs/SM: 14% slower)
       break;
     }
