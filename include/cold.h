@@ -81,7 +81,7 @@ enum { COLD_RELU = 0, COLD_PRELU = 1 };
 #define COLD_K_STREAM_B    16u   /* single-CTA GEMMs stream the weight tile instead of keeping it resident */
 #define COLD_K_TAIL_NONE   32u   /* no fused tail kernel: every hidden layer a GEMM (head fused into the last) */
 #define COLD_K_TAIL3       64u   /* the FC(L-3)..head fused tail instead of FC(L-2)..head (tail45) */
-#define COLD_K_CHAIN_TAIL 128u   /* FC4/FC5/head inside the chain kernel (measured 4% slower; ReLU only) */
+#define COLD_K_CHAIN_TAIL 128u   /* FC4/FC5/head inside the chain kernel, in TMEM (H3/H4 as A operands; measured 1.5% slower; ReLU only) */
 #define COLD_K_SERIAL_USER 256u  /* calls of <= 4 requests: user kernel before the gather, one stream */
 #define COLD_K_NO_PDL     512u   /* no programmatic dependent launch between the kernels */
 #define COLD_K_X_ROWS    1024u   /* X_ac row-major (512 B rows) instead of the half-slab layout */

@@ -573,8 +573,11 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
       chain_supported(c->widths[0], c->widths[1], c->widths[2], c->d_ac_pad)) {
     c->chain = !(c->kflags & COLD_K_LAYERWISE);
     c->chain_min = cfg->chain_min_ads > 0 ? cfg->chain_min_ads : (int64_t)c->num_sms * 256;
-    // COLD_K_CHAIN_TAIL also folds FC4 / FC5 / head into the chain: measured slower than the separate
-    // resident-weight tail kernel (N = 128 / 64 pair tiles, larger live L2 set), so off by default
+    // COLD_K_CHAIN_TAIL also folds FC4 / FC5 / head into the chain, in TMEM (FC3's epilogue writes H3 back
+    // into its accumulator buffer as FC4's A operand, H4 likewise for FC5): no H3 round trip and no tail
+    // launch, but the in-place tail holds one of the two 256-column accumulator buffers from FC3 to the
+    // head, so FC2's two n-tiles share the other one and wait for each other's drain: 304.9 us per chunk
+    // vs 275.6 + 24.8 for chain + tail45 (profiles/r03/ab_tt_*.jsonl), off by default
     c->chain_tail = c->chain && chain_tail_supported(c->widths[3], c->widths[4], c->widths[2]) &&
                     c->widths[5] <= 2 && (c->kflags & COLD_K_CHAIN_TAIL) && !c->prelu;
     c->lat_tail3 = !c->chain_tail && !c->prelu && !(c->kflags & COLD_K_LAT_TAIL45) &&

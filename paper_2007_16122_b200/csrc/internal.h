@@ -33,6 +33,7 @@ struct UserArgs {
   const float* w1u_t;              // [D_u][H] fp32 (W1 user columns, transposed)
   const float* b1;                 // [H]
   int H;                           // FC1 width
+  int part_off;                    // set by launch_user: shared-memory float offset of the [4][H] partial sums
   float* u1;                       // [R][H] out: b1 + W1_u x_u
   float* xu;                       // [R][D_u] out: x_u
   const int32_t* ad_offsets;       // [R+1] device

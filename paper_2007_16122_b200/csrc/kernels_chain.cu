@@ -15,7 +15,9 @@
 // FC3(j-1) sits between FC1(j) and FC2(j) so the tensor pipe has work while H1(j) drains.
 // After FC2(j) (resp. FC3(j-1)) has consumed H1(j) (H2(j-1)), the epilogue issues
 // discard.global.L2 on the CTA's rows of that block: the lines are dead, so L2 drops them without a
-// write-back. H3 is written for the tail kernel (FC4 / FC5 / head).
+// write-back. H3 is written for the tail kernel (FC4 / FC5 / head), or, with TAIL, never leaves the SM:
+// FC4 and FC5 run as CTA-pair MMAs whose A operand (H3, H4) the epilogue writes back into TMEM
+// (tcgen05.st) and whose weights stream through the same stage ring (see for_tasks).
 //
 // Per tile the machinery is gemm_pair_kernel's: TMA producer (warp 0), leader MMA issuer (warp 1),
 // 8 epilogue warps (2..9) with double-buffered TMEM accumulators and group TMA stores (epi.cuh), and
@@ -106,11 +108,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   const int pair = (int)cluster_id_x(), npairs = (int)num_clusters_x();
   const int num_pm = (M + 2 * BM - 1) / (2 * BM);
   const int nrb = pair < num_pm ? (num_pm - 1 - pair) / npairs + 1 : 0;   // this pair's row blocks
-  // layers 0..2 = FC1..FC3 (N = 256 per tile), TAIL: 3 = FC4 (N = n4 <= 256), 4 = FC5 (N = n5) + head
+  // layers 0..2 = FC1..FC3 (N = 256 per tile), TAIL: 3 = FC4 (N = n4 = 128), 4 = FC5 (N = n5 = 64) + head
   const int kbs[5] = {cp.k1 / BK, cp.n1 / BK, cp.n2 / BK, cp.n3 / BK, cp.n4 / BK};
-  const CUtensorMap* tA[5] = {&tmX, &tmH1, &tmH2, &tmH3, &tmH4};
+  const CUtensorMap* tA[3] = {&tmX, &tmH1, &tmH2};
   const CUtensorMap* tB[5] = {&tmW1, &tmW2, &tmW3, &tmW4, &tmW5};
-  const CUtensorMap* tC[4] = {&tmH1, &tmH2, &tmH3, &tmH4};
+  const CUtensorMap* tC[3] = {&tmH1, &tmH2, &tmH3};
   const int ntile[5] = {cp.n1 / C_BN, cp.n2 / C_BN, cp.n3 / C_BN, 1, 1};
   const int tn[5] = {C_BN, C_BN, C_BN, cp.n4, cp.n5};          // tile N per layer
 
@@ -118,20 +120,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   //   FC1(s) n-tiles | FC3(s-1) | FC2(s) n-tiles
   // (measured: interleaving FC1(j) with FC2(j-1) to spread the epilogue load doubles the L2 working set
   // of live activations and ran 14% slower)
-  // TAIL: step s = FC1(s) | FC5(s-3) | FC4(s-2) | FC3(s-1) | FC2(s). Every consumer sits several tiles
-  // after its producer, and the producer's wait on hready[l](j) always precedes the loads of the task
-  // that would complete the barrier's next phase (no parity aliasing).
   // (FC3_MID would put FC3(s-1) between the two halves of FC1(s)'s n-tiles to spread FC1's epilogue-heavy
   // tiles: measured slower, off)
+  // Each task names its TMEM accumulator buffer (0 / 1, C_BN columns each); MMA issuer and epilogue count
+  // the uses of each buffer for the barrier phases. Without TAIL the buffers alternate in task order.
+  // TAIL (FC4 / FC5 / head in TMEM, no H3 round trip): step s =
+  //   FC1(s) n-tiles (buffers alternate by n-tile) | FC3(s-1) [buffer 0] | FC2(s) tile 0 [buffer 1] |
+  //   FC4(s-1) [buffer 0] | FC2(s) tiles 1.. [buffer 1] | FC5(s-1) [buffer 0]
+  // FC3 -> FC4 -> FC5 of a block run IN PLACE in buffer 0: the FC3 epilogue writes H3 (16-bit, packed two
+  // per column) into columns [0, 128) as FC4's A operand, acc4 lands in [128, 256), H4 goes to [0, 64) and
+  // acc5 to [64, 128); the FC5 epilogue applies the head and the sigmoid.
   auto for_tasks = [&](auto&& f) {
-    for (int s = 0; s <= nrb + (TAIL ? 2 : 0); s++) {
-      const int fc1_split = (FC3_MID && !TAIL && s >= 1 && s <= nrb) ? ntile[0] / 2 : ntile[0];
-      if (s < nrb) for (int nb = 0; nb < fc1_split; nb++) f(0, s, nb);
-      if (TAIL && s >= 3) f(4, s - 3, 0);
-      if (TAIL && s >= 2 && s <= nrb + 1) f(3, s - 2, 0);
-      if (s >= 1 && s <= nrb) for (int nb = 0; nb < ntile[2]; nb++) f(2, s - 1, nb);
-      if (s < nrb) for (int nb = fc1_split; nb < ntile[0]; nb++) f(0, s, nb);
-      if (s < nrb) for (int nb = 0; nb < ntile[1]; nb++) f(1, s, nb);
+    int t = 0;
+    auto go = [&](int l, int j, int nb, int tbuf) { f(l, j, nb, TAIL ? tbuf : (t & 1)); t++; };
+    for (int s = 0; s <= nrb; s++) {
+      if (!TAIL) {
+        const int fc1_split = (FC3_MID && s >= 1 && s <= nrb) ? ntile[0] / 2 : ntile[0];
+        if (s < nrb) for (int nb = 0; nb < fc1_split; nb++) go(0, s, nb, 0);
+        if (s >= 1) for (int nb = 0; nb < ntile[2]; nb++) go(2, s - 1, nb, 0);
+        if (s < nrb) for (int nb = fc1_split; nb < ntile[0]; nb++) go(0, s, nb, 0);
+        if (s < nrb) for (int nb = 0; nb < ntile[1]; nb++) go(1, s, nb, 0);
+      } else {
+        if (s < nrb) for (int nb = 0; nb < ntile[0]; nb++) go(0, s, nb, nb & 1);
+        if (s >= 1) go(2, s - 1, 0, 0);
+        if (s < nrb) go(1, s, 0, 1);
+        if (s >= 1) go(3, s - 1, 0, 0);
+        if (s < nrb) for (int nb = 1; nb < ntile[1]; nb++) go(1, s, nb, 1);
+        if (s >= 1) go(4, s - 1, 0, 0);
+      }
     }
   };
 
@@ -175,10 +191,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       uint32_t ph = 0;
       const bool ins = cp.instr != nullptr;
       unsigned long long w_empty = 0, w_hready = 0;
-      for_tasks([&](int l, int j, int nb) {
+      for_tasks([&](int l, int j, int nb, int) {
         const int pm = pair + j * npairs;
         const int mrow = pm * 2 * BM + (int)rank * BM;
-        if (l > 1 || (l == 1 && !H1_TILES)) {
+        if (l == 2 || (l == 1 && !H1_TILES)) {
           if (nb == 0) cwait(&hready[l - 1], (uint32_t)(j & 1), w_hready, ins);   // own rows of the input
         }
         const int bhalf = tn[l] / 2;                  // weight rows this CTA stages (half the tile N)
@@ -188,8 +204,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           if (H1_TILES && l == 1 && (kb * BK) % C_BN == 0)
             cwait(&h1t[(kb * BK) / C_BN], (uint32_t)(j & 1), w_hready, ins);
           cwait(&empty[s], ph ^ 1, w_empty, ins);
-          if (leader) mbar_expect_tx(&full[s], 2 * (C_A_BYTES + bhalf * BK * 2));
-          tma_load_a_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb, mrow, l == 0 ? pol_x : pol_a, l == 0 && cp.x_slab);
+          if (TAIL && l >= 3) {   // FC4 / FC5: A is in TMEM, only the weight half streams
+            if (leader) mbar_expect_tx(&full[s], 2 * (bhalf * BK * 2));
+          } else {
+            if (leader) mbar_expect_tx(&full[s], 2 * (C_A_BYTES + bhalf * BK * 2));
+            tma_load_a_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb, mrow, l == 0 ? pol_x : pol_a, l == 0 && cp.x_slab);
+          }
           tma_load_2d_pair(sB + s * C_B_BYTES, tB[l], &full[s], kb * BK, nb * tn[l] + (int)rank * bhalf, pol_b);
           if (++s == C_STAGES) { s = 0; ph ^= 1; }
         }
@@ -216,18 +236,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       constexpr uint32_t id256 = idesc_pair<C_BN, BF16>();
       const uint32_t id_tail[2] = {cp.n4 == 128 ? idesc_pair<128, BF16>() : idesc_pair<64, BF16>(),
                                    cp.n5 == 64 ? idesc_pair<64, BF16>() : idesc_pair<32, BF16>()};
-      int s = 0, lt = 0, fc1_t = 0;
+      int s = 0, fc1_t = 0, uses0 = 0, uses1 = 0;
       uint32_t ph = 0;
       const bool ins = cp.instr != nullptr;
       unsigned long long w_full = 0, w_tempty = 0, w_ux = 0, wl_full[3] = {0, 0, 0}, wl_te[3] = {0, 0, 0};
       const long long t_begin = clock64();
-      for_tasks([&](int l, int j, int nb) {
+      for_tasks([&](int l, int j, int nb, int acc) {
         const uint32_t idesc = l < 3 ? id256 : id_tail[l - 3];
-        const int acc = lt & 1;
         const unsigned long long te0 = w_tempty, fu0 = w_full;
-        cwait(&tempty[acc], ((lt >> 1) & 1) ^ 1, w_tempty, ins);
+        cwait(&tempty[acc], (uint32_t)((acc ? uses1++ : uses0++) & 1) ^ 1, w_tempty, ins);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * C_BN;
+        const uint32_t bufc = tmem_base + acc * C_BN;
+        // TAIL in place: acc4 at column 128, acc5 at 64; their A (H3 / H4) from column 0 of the same buffer
+        const uint32_t d = (TAIL && l == 3) ? bufc + 128 : ((TAIL && l == 4) ? bufc + 64 : bufc);
         for (int kb = 0; kb < kbs[l]; kb++) {
           cwait(&full[s], ph, w_full, ins);
           tc_fence_after();
@@ -235,6 +256,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           const uint64_t bd = sdesc_sw128(smem_u32(sB + s * C_B_BYTES));
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; kk++) {
+            if (TAIL && l >= 3) {   // A = 16 K elements of H3 / H4 = 8 TMEM columns
+              umma_f16_pair_ts(d, bufc + (uint32_t)((kb * BK + kk * UMMA_K) / 2), bd + (uint64_t)(kk * 2), idesc,
+                               (kb | kk) != 0);
+              continue;
+            }
             const uint64_t a_kk = (l == 0 && cp.x_slab) ? sdesc_k16_plain(smem_u32(sA + s * C_A_BYTES) + kk * BM * 32)
                                                          : ad + (uint64_t)(kk * 2);
             umma_f16_pair(d, a_kk, bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
@@ -254,7 +280,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           fc1_t++;
         }
         umma_commit_pair(&tfull[acc]);
-        lt++;
         if (ins && l < 3) { wl_full[l] += w_full - fu0; wl_te[l] += w_tempty - te0; }
       });
       if (ins) {
@@ -271,11 +296,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     const bool elected = (q == 0) && (lane == 0);
     const bool ins = cp.instr != nullptr && lane == 0;
     unsigned long long w_tfull = 0;
-    int lt = 0, box_ctr = 0;
-    for_tasks([&](int l, int j, int nb) {
+    int box_ctr = 0, uses0 = 0, uses1 = 0;
+    for_tasks([&](int l, int j, int nb, int acc) {
       const int pm = pair + j * npairs;
-      const int acc = lt & 1;
-      cwait(&tfull[acc], (lt >> 1) & 1, w_tfull, ins);
+      cwait(&tfull[acc], (uint32_t)((acc ? uses1++ : uses0++) & 1), w_tfull, ins);
       tc_fence_after();
       const int trow0 = pm * 2 * BM + (int)rank * BM;   // this CTA's first row of the block
       const int row = trow0 + q * 32 + lane;
@@ -288,19 +312,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         }
       }
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * C_BN);
-      if (TAIL && l == 4) {
-        // FC5 + head: h == 0 warps own their quadrant's rows: ReLU(acc + b5) . head_w + head_b -> sigma
+      if (TAIL && l == 2) {
+        // FC3 -> H3 = ReLU(acc3 + b3), 16-bit, packed two per column into columns [64 h, 64 h + 64) of this
+        // buffer (FC4's A operand); the quadrant's other warp must have read its acc3 columns first
+        const float* b3 = sbias ? sBias + cp.n2 : cp.b3;
+        uint32_t pk[64];
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          uint32_t v[64];
+          TMEM_LD32(tbase + 128 * h + 64 * c, v);
+          TMEM_LD32(tbase + 128 * h + 64 * c + 32, (v + 32));
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 64; i += 4) {
+            const float4 b = *reinterpret_cast<const float4*>(b3 + 128 * h + 64 * c + i);
+            pk[32 * c + i / 2] = Pack<BF16>::two_relu(__uint_as_float(v[i]) + b.x, __uint_as_float(v[i + 1]) + b.y);
+            pk[32 * c + i / 2 + 1] = Pack<BF16>::two_relu(__uint_as_float(v[i + 2]) + b.z, __uint_as_float(v[i + 3]) + b.w);
+          }
+        }
+        named_bar_sync(3 + q, 64);
+        TMEM_ST32(tbase + 64 * h, pk);
+        TMEM_ST32(tbase + 64 * h + 32, (pk + 32));
+        tmem_wait_st();
+      } else if (TAIL && l == 3) {
+        // FC4 -> H4 = ReLU(acc4 + b4) into columns [32 h, 32 h + 32) (FC5's A operand; H3 is dead)
+        uint32_t v[64], pk[32];
+        TMEM_LD32(tbase + 128 + 64 * h, v);
+        TMEM_LD32(tbase + 128 + 64 * h + 32, (v + 32));
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 64; i += 4) {
+          const float4 b = __ldg(reinterpret_cast<const float4*>(cp.b4 + 64 * h + i));
+          pk[i / 2] = Pack<BF16>::two_relu(__uint_as_float(v[i]) + b.x, __uint_as_float(v[i + 1]) + b.y);
+          pk[i / 2 + 1] = Pack<BF16>::two_relu(__uint_as_float(v[i + 2]) + b.z, __uint_as_float(v[i + 3]) + b.w);
+        }
+        TMEM_ST32(tbase + 32 * h, pk);
+        tmem_wait_st();
+      } else if (TAIL && l == 4) {
+        // FC5 + head: h == 0 warps own their quadrant's rows: ReLU(acc5 + b5) . head_w + head_b -> sigma
         if (h == 0) {
           float z0 = 0.0f, z1 = 0.0f;
-          for (int c = 0; c < cp.n5; c += 32) {
+#pragma unroll
+          for (int c = 0; c < 64; c += 32) {
             uint32_t v[32];
-            TMEM_LD32(tbase + c, v);
+            TMEM_LD32(tbase + 64 + c, v);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; i++) {
               const float a = fmaxf(__uint_as_float(v[i]) + __ldg(cp.b5 + c + i), 0.0f);
               z0 = fmaf(__ldg(cp.head_w + c + i), a, z0);
-              if (cp.head_n == 2) z1 = fmaf(__ldg(cp.head_w + cp.n5 + c + i), a, z1);
+              if (cp.head_n == 2) z1 = fmaf(__ldg(cp.head_w + 64 + c + i), a, z1);
             }
           }
           if (row < M) {
@@ -309,25 +370,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           }
         }
       } else {
-        // H3 (no TAIL) leaves for the tail kernel: stream it past L2 (evict_first) so it does not push out
-        // live H1 / H2
         const int half = tn[l] / C_GROUPS;      // this group's columns of the tile
-        const float* bias = l == 1 ? cp.b2 : (l == 2 ? cp.b3 : (l == 3 ? cp.b4 : nullptr));
+        const float* bias = l == 1 ? cp.b2 : (l == 2 ? cp.b3 : nullptr);
         uint32_t bias_s = 0u;   // smem address of this tile's bias columns (added like a u1 row)
         if (sbias && (l == 1 || l == 2)) {
           bias_s = smem_u32(sBias) + (uint32_t)((l == 1 ? 0 : cp.n2) + nb * tn[l]) * 4u;
           bias = nullptr;
         }
-        const float* slope = l == 0 ? cp.s1 : (l == 1 ? cp.s2 : (l == 2 ? cp.s3 : nullptr));
+        const float* slope = l == 0 ? cp.s1 : (l == 1 ? cp.s2 : cp.s3);
         epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, bias_s, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
-                             nb * tn[l], trow0, q, h, lane, 0, cp.instr ? cp.instr + 16 + 8 * (l < 3 ? l : 0) : nullptr,
+                             nb * tn[l], trow0, q, h, lane, 0, cp.instr ? cp.instr + 16 + 8 * l : nullptr,
                              (FC1_DIRECT && l == 0) ? const_cast<void*>(cp.h1) : nullptr, cp.n1, M, 0ull, slope, C_OUT_BOXES == 2 * C_GROUPS ? sOut + (C_GROUPS + h) * EPI_GROUP_BOX : nullptr,
                              &box_ctr);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&tempty[acc], 0);
-      lt++;
       const bool last_of_layer = nb == ntile[l] - 1;
       if (FC1_DIRECT && l == 0) {
         // direct stores: this tile's H1 rows are written once every lane's stores are ordered before the
@@ -354,7 +412,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           named_bar_sync(1 + h, 128);
           if (lane == 0) mbar_arrive(&h1t[nb]);
         }
-      } else if ((l < 2 || (TAIL && l < 4)) && last_of_layer) {
+      } else if (l < 2 && last_of_layer) {
         // the block's rows of this layer are stored once this group's bulk stores completed
         if (elected) {
           bulk_wait_all();
@@ -363,11 +421,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         named_bar_sync(1 + h, 128);
         if (lane == 0) mbar_arrive(&hready[l]);
       }
-      if (l >= 1 && last_of_layer) {
-        // the input of this layer for the block (H1 for FC2, H2 for FC3, H3 / H4 for FC4 / FC5) has been
-        // consumed by the MMAs (tfull of the last tile): drop this CTA's rows from L2 without write-back
-        const void* in_buf[5] = {nullptr, cp.h1, cp.h2, cp.h3, cp.h4};
-        const int in_w[5] = {0, cp.n1, cp.n2, cp.n3, cp.n4};
+      if ((l == 1 || l == 2) && last_of_layer) {
+        // the input of this layer for the block (H1 for FC2, H2 for FC3) has been consumed by the MMAs
+        // (tfull of the last tile): drop this CTA's rows from L2 without write-back
+        const void* in_buf[3] = {nullptr, cp.h1, cp.h2};
+        const int in_w[3] = {0, cp.n1, cp.n2};
         const uint8_t* base = reinterpret_cast<const uint8_t*>(in_buf[l]);
         const int ld = in_w[l] * 2;                            // bytes per row
         const int lines = ld / 128;
@@ -390,10 +448,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
 bool chain_supported(int n1, int n2, int n3, int k1) {
   return n1 % C_BN == 0 && n2 % C_BN == 0 && n3 % C_BN == 0 && k1 % BK == 0 && n1 / BK >= 1;
 }
-// FC4 / FC5 as 256-row pair tiles: N in {128, 64} / {64, 32} (the paper: 128 -> 64 -> head)
-bool chain_tail_supported(int n4, int n5, int n3) {
-  return (n4 == 128 || n4 == 64) && (n5 == 64 || n5 == 32) && n3 % BK == 0 && n4 % BK == 0;
-}
+// FC4 / FC5 / head in TMEM (TAIL): the paper's 256 -> 128 -> 64 -> head, in place in one C_BN-column buffer
+bool chain_tail_supported(int n4, int n5, int n3) { return n3 == C_BN && n4 == 128 && n5 == 64; }
 
 cudaError_t launch_chain(const CUtensorMap* tm[12], int M, int bf16, const ChainParams& cp, int num_sms, bool pdl,
                          cudaStream_t s) {

@@ -145,39 +145,44 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
   __syncthreads();
   // u1[r][o] = b1[o] + sum_i W1u[o][i] x_u[i]   (W1u stored transposed: coalesced over o)
   // 64 outputs per pass, 4 threads per output: thread part q sums inputs [q*P, q*P + P) (up to 32 weight
-  // loads in flight, one L2 round trip instead of d_u / 16 dependent ones), then the four partial sums
-  // are added in part order through shared memory. The order is fixed, so u1 does not depend on the
+  // loads in flight, one L2 round trip instead of d_u / 16 dependent ones); after one barrier the four
+  // partial sums of each output are added in part order. The order is fixed, so u1 does not depend on the
   // slice count or on the other requests of the call.
-  float* part = stage;   // [4][64] partial sums (reuses the pooling stage)
+  float* part = xs + a.part_off;   // [4][H] partial sums
   const int q = threadIdx.x >> 6, ol = threadIdx.x & 63;
   const int P = (d_u + 3) / 4;
   const int i0 = min(q * P, d_u), i1 = min(i0 + P, d_u);
   const int npass = (a.H + 63) / 64;
-  for (int pass = blockIdx.y; pass < npass && !a.stats; pass += gridDim.y) {
-    const int o = pass * 64 + ol;
-    float acc = 0.0f;
-    if (!a.dense && o < a.H) {   // dense SE: W1's user columns run inside FC1 with the gated per-ad x (u1 = b1)
-      int i = i0;
-      for (; i + 32 <= i1; i += 32) {
-        float w[32];
+  if (!a.stats) {
+    for (int pass = blockIdx.y; pass < npass; pass += gridDim.y) {
+      const int o = pass * 64 + ol;
+      float acc = 0.0f;
+      if (!a.dense && o < a.H) {   // dense SE: W1's user columns run inside FC1 with the gated per-ad x (u1 = b1)
+        int i = i0;
+        for (; i + 32 <= i1; i += 32) {
+          float w[32];
 #pragma unroll
-        for (int j = 0; j < 32; j++) w[j] = __ldg(a.w1u_t + (int64_t)(i + j) * a.H + o);
+          for (int j = 0; j < 32; j++) w[j] = __ldg(a.w1u_t + (int64_t)(i + j) * a.H + o);
 #pragma unroll
-        for (int j = 0; j < 32; j++) acc = fmaf(w[j], xs[i + j], acc);
+          for (int j = 0; j < 32; j++) acc = fmaf(w[j], xs[i + j], acc);
+        }
+        for (; i + 8 <= i1; i += 8) {
+          float w[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) w[j] = __ldg(a.w1u_t + (int64_t)(i + j) * a.H + o);
+#pragma unroll
+          for (int j = 0; j < 8; j++) acc = fmaf(w[j], xs[i + j], acc);
+        }
+        for (; i < i1; i++) acc = fmaf(__ldg(a.w1u_t + (int64_t)i * a.H + o), xs[i], acc);
       }
-      for (; i + 8 <= i1; i += 8) {
-        float w[8];
-#pragma unroll
-        for (int j = 0; j < 8; j++) w[j] = __ldg(a.w1u_t + (int64_t)(i + j) * a.H + o);
-#pragma unroll
-        for (int j = 0; j < 8; j++) acc = fmaf(w[j], xs[i + j], acc);
-      }
-      for (; i < i1; i++) acc = fmaf(__ldg(a.w1u_t + (int64_t)i * a.H + o), xs[i], acc);
+      if (o < a.H) part[q * a.H + o] = acc;
     }
-    part[q * 64 + ol] = acc;
     __syncthreads();
-    if (q == 0 && o < a.H) {
-      acc = a.b1[o] + part[ol] + part[64 + ol] + part[128 + ol] + part[192 + ol];
+    for (int pass = blockIdx.y; pass < npass; pass += gridDim.y) {
+      if (q != 0) break;
+      const int o = pass * 64 + ol;
+      if (o >= a.H) continue;
+      const float acc = a.b1[o] + part[o] + part[a.H + o] + part[2 * a.H + o] + part[3 * a.H + o];
       a.u1[(int64_t)r * a.H + o] = acc;
       if (a.u1t) {   // u1 = term_0 + term_1 (+ term_2), each RNE in 16 bits: the FC1 tensor-core operand
         float u = acc;
@@ -196,7 +201,6 @@ __global__ void __launch_bounds__(256) user_kernel(UserArgs a) {
         }
       }
     }
-    __syncthreads();
   }
   if (main_cta) {   // bounds in registers: the stores may alias ad_offsets, which would reload it per step
     const int64_t e0 = a.ad_offsets[r], e1 = a.ad_offsets[r + 1];
@@ -681,23 +685,22 @@ __global__ void rows_kernel(RowsArgs a) {
 // ---------------------------------------------------------------------------------------------
 template <typename T>
 static void user_dispatch(const UserArgs& a, int R, cudaStream_t s) {
-  const size_t smem = ((size_t)a.n_user * a.k + 4) * sizeof(float) + (size_t)8 * 32 * a.k * sizeof(float);
-  // few requests (the latency path): split the u1 GEMV over up to 4 CTAs per request
+  UserArgs b = a;
+  b.part_off = (int)((((size_t)a.n_user * a.k + 3) & ~(size_t)3) + (size_t)8 * 32 * a.k);   // after x_u and the row stage
+  const size_t smem = ((size_t)b.part_off + (size_t)4 * a.H) * sizeof(float);
+  // few requests (the latency path): the u1 GEMV's 64-output passes over up to 16 CTAs per request
   const int slices = R >= 64 ? 1 : std::min(16, std::max(1, (a.H + 63) / 64));
   const dim3 grid((unsigned)R, (unsigned)slices);
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 256, smem, s>>>(b);
+  };
   switch (a.k) {
-    case 2: user_kernel<T, 2><<<grid, 256, smem, s>>>(a); break;
-    case 4: user_kernel<T, 4><<<grid, 256, smem, s>>>(a); break;
-    case 8: user_kernel<T, 8><<<grid, 256, smem, s>>>(a); break;
-    case 16: user_kernel<T, 16><<<grid, 256, smem, s>>>(a); break;
-    case 32: {
-      static DevOnce attr;
-      if (attr.first()) {   // 8 warps x 32 rows x 32 floats = 32 KB of staging + x_u
-        cudaFuncSetAttribute(user_kernel<T, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      }
-      user_kernel<T, 32><<<grid, 256, smem, s>>>(a);
-      break;
-    }
+    case 2: go(user_kernel<T, 2>); break;
+    case 4: go(user_kernel<T, 4>); break;
+    case 8: go(user_kernel<T, 8>); break;
+    case 16: go(user_kernel<T, 16>); break;
+    case 32: go(user_kernel<T, 32>); break;
   }
 }
 

@@ -39,6 +39,17 @@ __device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, u
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// A from TENSOR MEMORY (each CTA's own 128 rows: lane = row, 32-bit column c = K elements 2c | 2c+1 << 16;
+// tools/probes/umma_ts_pair_probe.cu), B from shared memory (each CTA half of the N rows)
+__device__ __forceinline__ void umma_f16_pair_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // arrive on the same barrier offset in both CTAs of the pair once all prior MMAs completed
 __device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
   asm volatile(
