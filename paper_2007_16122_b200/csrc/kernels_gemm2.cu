@@ -142,7 +142,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
-  pdl_wait();
+  // PDL: everything that reads what earlier kernels wrote (A, the u1 operand, req_of_ad, biases in the
+  // epilogue) waits for them; the producer first issues the weight loads, which do not depend on them
+  if (warp != 0) pdl_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -153,15 +155,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>
       uint32_t ph = 0;
       int lt = 0;
       constexpr int TERMS = BF16 ? 3 : 2;
-      // the pair tile's first request rounded down to 8 (16 B-aligned TMA box start), prefetched
       auto pm_of = [&](int it) { int pm, nb; tile_of(it, pm, nb); return pm; };
-      int r_next = (U1 && w_first < w_count) ? (ep.req_of_ad[ep.a0 + pm_of(w_first) * 2 * BM] & ~7) : 0;
       if (RES && w_count > 0) {   // this pair's weight half, once
         if (leader) mbar_expect_tx(bres, 2 * kb_count * Cfg::B_ATOM);
         for (int kb = 0; kb < kb_count; kb++)
           tma_load_2d_pair(sRes + kb * Cfg::B_ATOM, &tmB, bres, kb * BK, (pair % num_n) * BN + (int)rank * (BN / 2),
                            pol_b);
       }
+      // streamed weights: the first tile's first STAGES weight k-blocks before the dependency wait
+      int pre = 0;
+      if (!RES && w_first < w_count) {
+        int pm0, nb0;
+        tile_of(w_first, pm0, nb0);
+        pre = kb_count < Cfg::STAGES ? kb_count : Cfg::STAGES;
+        for (int kb = 0; kb < pre; kb++) {
+          if (leader) mbar_expect_tx(&full[kb], 2 * Cfg::STAGE_BYTES);
+          tma_load_2d_pair(sB + kb * Cfg::B_BYTES, &tmB, &full[kb], kb * BK, nb0 * BN + (int)rank * (BN / 2), pol_b);
+        }
+      }
+      pdl_wait();
+      // the pair tile's first request rounded down to 8 (16 B-aligned TMA box start), prefetched
+      int r_next = (U1 && w_first < w_count) ? (ep.req_of_ad[ep.a0 + pm_of(w_first) * 2 * BM] & ~7) : 0;
       for (int it = w_first; it < w_count; it += w_step, lt++) {
         int pm, nb;
         tile_of(it, pm, nb);
@@ -169,6 +183,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<BN, U1, RES>
         const int r_first = r_next;
         if (U1 && it + w_step < w_count) r_next = ep.req_of_ad[ep.a0 + pm_of(it + w_step) * 2 * BM] & ~7;
         for (int kb = 0; kb < kb_count; kb++) {
+          if (pre > 0) {   // weights already in flight (stage kb of the first tile): only A
+            tma_load_a_pair(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb, mrow, pol_a, ep.a_slab != 0);
+            pre--;
+            if (++s == Cfg::STAGES) { s = 0; ph ^= 1; }
+            continue;
+          }
           mbar_wait(&empty[s], ph ^ 1);
           if (leader) mbar_expect_tx(&full[s], 2 * Cfg::STAGE_BYTES);
           tma_load_a_pair(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb, mrow, pol_a, ep.a_slab != 0);

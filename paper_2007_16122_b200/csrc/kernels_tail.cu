@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
-  pdl_wait();
+  if (warp != 0) pdl_wait();   // PDL (the producer first issues the weight loads that do not depend on it)
 
   // the per-CTA op sequence (producer and MMA walk it identically):
   //   t = 0: FC3(0) FC4(0);  t >= 1: FC3(t) FC5(t-1) FC4(t);  end: FC5(T-1)
@@ -84,8 +84,21 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       int s = 0;
       uint32_t ph = 0;
       auto next = [&]() { if (++s == T_STAGES) { s = 0; ph ^= 1; } };
+      // the first tile's first T_STAGES W3 k-blocks before the dependency wait
+      int pre = (int)blockIdx.x < num_tiles ? (kb3 < T_STAGES ? kb3 : T_STAGES) : 0;
+      for (int kb = 0; kb < pre; kb++) {
+        mbar_expect_tx(&full[kb], T_STAGE_BYTES);
+        tma_load_2d(sStage + kb * T_STAGE_BYTES + T_A_BYTES, &tmB3, &full[kb], kb * BK, 0, pol_b);
+      }
+      pdl_wait();
       auto load_fc3 = [&](int mb) {
         for (int kb = 0; kb < kb3; kb++) {
+          if (pre > 0) {   // W3 already in flight for this stage
+            tma_load_2d(sStage + s * T_STAGE_BYTES, &tmA3, &full[s], kb * BK, mb * BM, pol_a);
+            pre--;
+            next();
+            continue;
+          }
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], T_STAGE_BYTES);
           tma_load_2d(sStage + s * T_STAGE_BYTES, &tmA3, &full[s], kb * BK, mb * BM, pol_a);
