@@ -202,6 +202,10 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
   const int r = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   asm volatile("griddepcontrol.wait;" ::: "memory");   // PDL: the scores of the previous kernel
+#ifdef COLD_TOPK_TIMING
+  long long tm0 = clock64(), tm1 = 0, tm2 = 0, tm3 = 0, tm4 = 0;
+  int nrounds = 0;
+#endif
   const int64_t base = a.ad_offsets[r];
   const int n = (int)(a.ad_offsets[r + 1] - base);
   const int K = a.K;
@@ -231,6 +235,10 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
   }
 
   // ---- radix select (4-bit digits, MSB first) ----
+#ifdef COLD_TOPK_TIMING
+  __syncthreads();
+  tm1 = clock64();
+#endif
   uint32_t P = 0, mask = 0, need = (uint32_t)K;
   int round = 0;
   for (int shift = 28; shift >= 0; shift -= 4, round++) {
@@ -286,6 +294,10 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
   }
 
   // ---- collect: keys above the prefix (any order), then the first `need` keys on it by position ----
+#ifdef COLD_TOPK_TIMING
+  tm2 = clock64();
+  nrounds = round;
+#endif
   const uint32_t n_gt = (uint32_t)K - need;
   uint32_t cnt = 0;   // packed (gt << 16) | eq for this thread
 #pragma unroll
@@ -332,6 +344,9 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
   __syncthreads();
 
   // ---- bitonic sort of the P2 = pow2 >= K composites, descending (threads >= P2 sort padding) ----
+#ifdef COLD_TOPK_TIMING
+  tm3 = clock64();
+#endif
   int P2 = 1;
   while (P2 < K) P2 <<= 1;
   unsigned long long x = t < K ? cand[t] : 0ull;
@@ -357,6 +372,13 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
     a.idx[(int64_t)r * K + t] = (int32_t)(0xffffffffu - (uint32_t)(x & 0xffffffffu));
     a.key[(int64_t)r * K + t] = from_orderable((uint32_t)(x >> 32));
   }
+#ifdef COLD_TOPK_TIMING
+  __syncthreads();
+  tm4 = clock64();
+  if (t == 0 && r == 0)
+    printf("topk_small timing: load %lld select %lld (%d rounds) collect %lld sort+store %lld cycles\n", tm1 - tm0,
+           tm2 - tm1, nrounds, tm3 - tm2, tm4 - tm3);
+#endif
 }
 
 void launch_topk(const TopkArgs& a0, cudaStream_t s) {
