@@ -2,13 +2,16 @@
 // persistent tcgen05 kernel (... x 256 x 128 x 64 x 2; L163 sigma):
 //
 //   H3 = ReLU(H2 W3^T + b3)   (K3 = 512, N3 = 256)   A = H2 tile from HBM/L2 (TMA), B = W3 (TMA)
-//   H4 = ReLU(H3 W4^T + b4)   (N4 = 128)             A = H3 in shared memory,   B = W4 (TMA)
-//   H5 = ReLU(H4 W5^T + b5)   (N5 = 64)              A = H4 in shared memory,   B = W5 (TMA)
+//   H4 = ReLU(H3 W4^T + b4)   (N4 = 128)             A = H3 in TMEM,            B = W4 (TMA)
+//   H5 = ReLU(H4 W5^T + b5)   (N5 = 64)              A = H4 in TMEM,            B = W5 (TMA)
 //   p  = sigma(z1 - z0), z = W6 H5 + b6              in the epilogue threads, fp32
 //
-// Per 128-row tile only the fp32 score leaves the SM: H3 / H4 are written by the epilogue warps
-// straight into shared memory in the 128 B-swizzled K-major layout the next tcgen05.mma reads.
-// Accumulators live in TMEM at columns [0,256) / [256,384) / [384,448). The single MMA thread
+// Per 128-row tile only the fp32 score leaves the SM. Accumulators live in TMEM at columns [0,256) /
+// [256,384) / [384,448); the epilogue writes H3 (16-bit, two per column) back over acc3's columns
+// [0,128) and H4 over acc4's [256,320) once both warps of a lane quadrant have read them, and FC4 / FC5
+// take their A operand from there (tcgen05.mma with A in tensor memory: tools/probes/umma_ts_probe.cu).
+// Shared memory then holds only the stage ring (4 stages of 48 KB instead of 2 beside 96 KB of H3 / H4
+// tiles). The single MMA thread
 // interleaves two tiles so the tensor pipe works on FC3(t+1) while the epilogue drains FC4(t):
 //   FC3(0) | FC4(0) FC3(1) | FC5(0) FC4(1) FC3(2) | FC5(1) ...
 // (each FC4 / FC5 waits for the epilogue to have written its A operand; the producer fills the
@@ -22,14 +25,11 @@ namespace cold {
 constexpr int T_EPI_WARPS = 8;
 constexpr int T_THREADS = 64 + 32 * T_EPI_WARPS;
 constexpr int T_N3 = 256, T_N4 = 128, T_N5 = 64;
-constexpr int T_STAGES = 2;
+constexpr int T_STAGES = 4;
 constexpr int T_A_BYTES = BM * BK * 2;                  // 16 KB
 constexpr int T_B_BYTES = T_N3 * BK * 2;                // 32 KB (largest B k-block)
 constexpr int T_STAGE_BYTES = T_A_BYTES + T_B_BYTES;    // 48 KB
-constexpr int T_H3_BYTES = BM * T_N3 * 2;               // 64 KB  (4 SW128 atoms)
-constexpr int T_H4_BYTES = BM * T_N4 * 2;               // 32 KB  (2 SW128 atoms)
-constexpr int T_SMEM = T_STAGES * T_STAGE_BYTES + T_H3_BYTES + T_H4_BYTES + 1024 + 256;
-constexpr int T_ATOM = BM * 128;                        // one [128 rows][64 cols] swizzled atom
+constexpr int T_SMEM = T_STAGES * T_STAGE_BYTES + 1024 + 256;
 
 template <bool BF16>
 __global__ void __launch_bounds__(T_THREADS, 1)
@@ -39,13 +39,11 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sStage = smem;
-  uint8_t* sH3 = smem + T_STAGES * T_STAGE_BYTES;
-  uint8_t* sH4 = sH3 + T_H3_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sH4 + T_H4_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + T_STAGES * T_STAGE_BYTES);
   uint64_t* full = bars;                 // [T_STAGES]
   uint64_t* empty = bars + T_STAGES;     // [T_STAGES]
   uint64_t* tfull = bars + 2 * T_STAGES; // [3]: FC3, FC4, FC5 accumulators ready
-  uint64_t* hready = tfull + 3;          // [2]: H3, H4 written (and acc3 / acc4 drained)
+  uint64_t* hready = tfull + 3;          // [2]: H3, H4 written into TMEM (and acc3 / acc4 drained)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hready + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -146,15 +144,16 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         }
         umma_commit(&tfull[0]);
       };
-      auto mma_from_smem = [&](const uint8_t* sAct, int kbs, uint32_t acc, uint32_t idesc, uint64_t* done) {
+      // A (H3 / H4) from TMEM column tA: 16 K elements = 8 columns per MMA
+      auto mma_from_tmem = [&](uint32_t tA, int kbs, uint32_t acc, uint32_t idesc, uint64_t* done) {
         for (int kb = 0; kb < kbs; kb++) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
-          const uint64_t ad = sdesc_sw128(smem_u32(sAct + kb * T_ATOM));
           const uint64_t bd = sdesc_sw128(smem_u32(sStage + s * T_STAGE_BYTES + T_A_BYTES));
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; kk++)
-            umma_f16(acc, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
+            umma_f16_ts(acc, tA + (uint32_t)((kb * BK + kk * UMMA_K) / 2), bd + (uint64_t)(kk * 2), idesc,
+                        (kb | kk) != 0);
           umma_commit(&empty[s]);
           next();
         }
@@ -162,20 +161,24 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       };
       int lt = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, lt++) {
-        mma_fc3();                                           // acc3 free: epi3(lt-1) preceded hready[0](lt-1)
+        // acc3 free: epi3(lt-1) preceded hready[0](lt-1); and FC4(lt-1), which reads H3(lt-1) from acc3's
+        // columns, has completed (no MMA overwrites a TMEM operand of an MMA still in flight)
+        if (lt > 0) mbar_wait(&tfull[1], (lt - 1) & 1);
+        mma_fc3();
         if (lt > 0) {
           mbar_wait(&hready[1], (lt - 1) & 1);               // H4(lt-1) written, acc4 drained
           tc_fence_after();
-          mma_from_smem(sH4, T_N4 / BK, acc5, id5, &tfull[2]);
+          mma_from_tmem(acc4, T_N4 / BK, acc5, id5, &tfull[2]);
+          mbar_wait(&tfull[2], (lt - 1) & 1);                // FC5(lt-1) read H4 from acc4's columns
         }
         mbar_wait(&hready[0], lt & 1);                       // H3(lt) written, acc3 drained
         tc_fence_after();
-        mma_from_smem(sH3, T_N3 / BK, acc4, id4, &tfull[1]);
+        mma_from_tmem(acc3, T_N3 / BK, acc4, id4, &tfull[1]);
       }
       if (lt > 0) {
         mbar_wait(&hready[1], (lt - 1) & 1);
         tc_fence_after();
-        mma_from_smem(sH4, T_N4 / BK, acc5, id5, &tfull[2]);
+        mma_from_tmem(acc4, T_N4 / BK, acc5, id5, &tfull[2]);
       }
     }
   } else {
@@ -185,48 +188,35 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     const int h = ew >> 2;
     const int r = q * 32 + lane;                 // row inside the tile
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
-    // bias + ReLU + RNE cast of 32 accumulator columns into a swizzled activation tile in smem
-    // bias + ReLU + RNE cast of 32 accumulator columns (already loaded in v) into smem
-    auto drain_regs = [&](const uint32_t* v, const float* bias, int c0, uint8_t* sAct) {
-      float f[32];
+    // acc columns [c0, c0 + 128 or 64) of this warp -> bias + ReLU + RNE cast, packed two per 32-bit column, then
+    // written back over the first half of the same accumulator (the next layer's A operand) once the
+    // quadrant's other warp has read its columns too
+    auto drain_pack = [&](uint32_t acc, int ncol, const float* bias, int bar) {
+      uint32_t pk[64];
+      const int c0 = h * ncol;
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
-        f[i] = fmaxf(__uint_as_float(v[i]) + b.x, 0.0f);
-        f[i + 1] = fmaxf(__uint_as_float(v[i + 1]) + b.y, 0.0f);
-        f[i + 2] = fmaxf(__uint_as_float(v[i + 2]) + b.z, 0.0f);
-        f[i + 3] = fmaxf(__uint_as_float(v[i + 3]) + b.w, 0.0f);
-      }
-      uint8_t* atom = sAct + (c0 / 64) * T_ATOM;
-      const int j0 = (c0 % 64) / 8;
-#pragma unroll
-      for (int j = 0; j < 4; j++) {
-        uint4 w;
-        w.x = Pack<BF16>::two(f[8 * j + 0], f[8 * j + 1]);
-        w.y = Pack<BF16>::two(f[8 * j + 2], f[8 * j + 3]);
-        w.z = Pack<BF16>::two(f[8 * j + 4], f[8 * j + 5]);
-        w.w = Pack<BF16>::two(f[8 * j + 6], f[8 * j + 7]);
-        sts128(smem_u32(atom) + sw128_offset(r, j0 + j), w);
-      }
-    };
-    // columns [c_lo, c_hi) of the accumulator at TMEM column tbase -> activation tile sAct
-    auto drain_range = [&](uint32_t tbase, int c_lo, int c_hi, const float* bias, uint8_t* sAct) {
-      uint32_t v[32];
-      TMEM_LD32(lane_base + tbase + c_lo, v);
-      for (int c = c_lo; c < c_hi; c += 32) {
+      for (int c = 0; c < 2; c++) {
+        if (c * 64 >= ncol) break;
+        uint32_t v[64];
+        TMEM_LD32(lane_base + acc + c0 + 64 * c, v);
+        TMEM_LD32(lane_base + acc + c0 + 64 * c + 32, (v + 32));
         tmem_wait_ld();
-        uint32_t w[32];
 #pragma unroll
-        for (int i = 0; i < 32; i++) w[i] = v[i];
-        if (c + 32 < c_hi) TMEM_LD32(lane_base + tbase + c + 32, v);
-        drain_regs(w, bias, c, sAct);
+        for (int i = 0; i < 64; i += 4) {
+          const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c0 + 64 * c + i));
+          pk[32 * c + i / 2] = Pack<BF16>::two_relu(__uint_as_float(v[i]) + b.x, __uint_as_float(v[i + 1]) + b.y);
+          pk[32 * c + i / 2 + 1] = Pack<BF16>::two_relu(__uint_as_float(v[i + 2]) + b.z, __uint_as_float(v[i + 3]) + b.w);
+        }
       }
+      asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+      TMEM_ST32(lane_base + acc + c0 / 2, pk);
+      if (ncol > 64) TMEM_ST32(lane_base + acc + c0 / 2 + 32, (pk + 32));
+      tmem_wait_st();
     };
     auto epi3 = [&](int lt) {
       mbar_wait(&tfull[0], lt & 1);
       tc_fence_after();
-      drain_range(0, h * (T_N3 / 2), (h + 1) * (T_N3 / 2), tp.b3, sH3);
-      fence_async_smem();      // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      drain_pack(0, T_N3 / 2, tp.b3, 1 + q);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&hready[0]);
@@ -234,8 +224,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     auto epi4 = [&](int lt) {
       mbar_wait(&tfull[1], lt & 1);
       tc_fence_after();
-      drain_range(T_N3, h * (T_N4 / 2), (h + 1) * (T_N4 / 2), tp.b4, sH4);
-      fence_async_smem();
+      drain_pack(T_N3, T_N4 / 2, tp.b4, 1 + q);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&hready[1]);

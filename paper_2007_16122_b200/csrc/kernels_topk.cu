@@ -8,6 +8,9 @@
 // extra sort key. The K winners are then bitonic-sorted in shared memory on the 64-bit
 // composite (key << 32 | ~position), descending.
 #include "internal.h"
+#ifdef COLD_TOPK_TIMING
+#include <cstdio>
+#endif
 
 namespace cold {
 
@@ -177,12 +180,14 @@ __global__ void __launch_bounds__(TOPK_THREADS) topk_kernel(TopkArgs a) {
 // 4,000-ad request). The radix kernel above is issue-bound on its single SM there (~20 us: one CTA,
 // 1024 threads; ncu r03d). Same result, bit for bit, in a fifth of the instructions:
 //   * 512 threads; thread t owns positions t*KPT .. t*KPT+KPT-1 (blocked: thread order = position order);
-//   * radix select with 4-bit digits and no atomics: each thread counts its keys per digit in 4-bit
+//   * the nibbles all keys share are skipped (block AND / OR); then a radix select with 4-bit digits and
+//     no atomics: each thread counts its keys per digit in 4-bit
 //     fields of a 64-bit word (one shift-add per key, <= 8 keys per word), widens them to 16-bit
 //     fields, a warp sums them with __reduce_add_sync, lane 0 publishes 8 words; after a barrier warp 0
 //     sums the 16 warps' counts per bin (lane = bin), finds the digit with a 16-lane scan + ballot and
-//     publishes it (second barrier; the per-round buffers alternate); stops as soon as every key that
-//     matches the prefix is needed;
+//     publishes it (second barrier; the per-round buffers alternate); stops as soon as the keys above the
+//     prefix and all keys on it fit the sort (<= 512), which the sort then orders (3 rounds instead of 6
+//     for a 4000-ad request's sigmoid keys);
 //   * launched as a programmatic dependent of the scoring kernels (PDL): its launch overlaps their tail;
 //   * collect: keys above the prefix in any order, keys equal to it by ascending position (one
 //     block-wide exclusive scan of the packed (gt, eq) counts);
@@ -198,6 +203,7 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
   __shared__ __align__(16) uint32_t wcnt[2][NW][8];   // per-warp digit counts (bin b: word b/2, half b%2)
   __shared__ uint32_t wtot[NW];                       // per-warp packed (gt << 16 | eq) totals
   __shared__ uint4 sres[2];                           // per round: digit, its count, count above it
+  __shared__ uint2 spre[NW];                          // per-warp AND / OR of the keys (common prefix)
   __shared__ unsigned long long sbuf[2][TOPK_SMALL_THREADS];
   const int r = blockIdx.x;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -239,9 +245,24 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
   __syncthreads();
   tm1 = clock64();
 #endif
-  uint32_t P = 0, mask = 0, need = (uint32_t)K;
+  // the nibbles every valid key shares (sigmoid keys share their top bits) are resolved up front
+  uint32_t kand = 0xffffffffu, kor = 0u;
+#pragma unroll
+  for (int j = 0; j < KPT; j++)
+    if ((valid >> j) & 1u) { kand &= u[j]; kor |= u[j]; }
+  kand = __reduce_and_sync(FULL, kand);
+  kor = __reduce_or_sync(FULL, kor);
+  if (lane == 0) spre[warp] = make_uint2(kand, kor);
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < NW; w++) { const uint2 v = spre[w]; kand &= v.x; kor |= v.y; }
+  const uint32_t diff = kand ^ kor;
+  const int shift0 = diff ? ((31 - __clz(diff)) & ~3) : -4;   // the highest nibble in which keys differ
+  uint32_t mask = shift0 >= 28 ? 0u : (0xffffffffu << (shift0 + 4));
+  uint32_t P = kand & mask, need = (uint32_t)K;
+  uint32_t csel = (uint32_t)n;   // keys on the prefix (all of them until a digit is chosen)
   int round = 0;
-  for (int shift = 28; shift >= 0; shift -= 4, round++) {
+  for (int shift = shift0; shift >= 0; shift -= 4, round++) {
     unsigned long long nib[NC];
 #pragma unroll
     for (int c = 0; c < NC; c++) nib[c] = 0ull;
@@ -286,12 +307,15 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
     }
     __syncthreads();
     const uint4 res = sres[round & 1];
-    const uint32_t csel = res.y;
+    csel = res.y;
     need -= res.z;
     P |= res.x << shift;
     mask |= 15u << shift;
-    if (csel == need) break;   // every key matching the prefix is a winner: no need to resolve further
+    // the keys above the prefix and ALL keys on it fit the sort: stop resolving (the sort orders them)
+    if ((uint32_t)K - need + csel <= (uint32_t)TOPK_SMALL_THREADS) break;
   }
+  // take every key on the prefix (sorted below) when they fit, else the first `need` of them by position
+  const bool take_all = (uint32_t)K - need + csel <= (uint32_t)TOPK_SMALL_THREADS;
 
   // ---- collect: keys above the prefix (any order), then the first `need` keys on it by position ----
 #ifdef COLD_TOPK_TIMING
@@ -336,7 +360,7 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
       const unsigned long long comp = ((unsigned long long)u[j] << 32) | (0xffffffffu - (uint32_t)(t * KPT + j));
       if (m > P) cand[gslot++] = comp;
       else if (m == P) {
-        if (erank < need) cand[n_gt + erank] = comp;
+        if (take_all || erank < need) cand[n_gt + erank] = comp;
         erank++;
       }
     }
@@ -347,9 +371,10 @@ __global__ void __launch_bounds__(TOPK_SMALL_THREADS) topk_small_kernel(TopkArgs
 #ifdef COLD_TOPK_TIMING
   tm3 = clock64();
 #endif
+  const int S = take_all ? (int)(n_gt + csel) : K;   // candidates to sort (the first K are the result)
   int P2 = 1;
-  while (P2 < K) P2 <<= 1;
-  unsigned long long x = t < K ? cand[t] : 0ull;
+  while (P2 < S) P2 <<= 1;
+  unsigned long long x = t < S ? cand[t] : 0ull;
   int cur = 1;   // sbuf[0] holds the candidates; the first exchange writes sbuf[1]
   for (int size = 2; size <= P2; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {

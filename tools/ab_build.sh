@@ -2,6 +2,7 @@
 # Build an A/B variant of libcold.so with extra nvcc defines into paper_2007_16122_b200/_ab/<name>.so
 # usage: bash tools/ab_build.sh <name> -DFOO ...   then: COLD_LIB_AB=$PWD/paper_2007_16122_b200/_ab/<name>.so python bench.py ...
 set -e
+set -o pipefail
 NAME=$1; shift
 OUT=paper_2007_16122_b200/_ab/$NAME
 mkdir -p $OUT
