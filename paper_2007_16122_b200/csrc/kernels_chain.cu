@@ -207,8 +207,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           if (TAIL && l >= 3) {   // FC4 / FC5: A is in TMEM, only the weight half streams
             if (leader) mbar_expect_tx(&full[s], 2 * (bhalf * BK * 2));
           } else {
-            if (leader) mbar_expect_tx(&full[s], 2 * (C_A_BYTES + bhalf * BK * 2));
-            tma_load_a_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb, mrow, l == 0 ? pol_x : pol_a, l == 0 && cp.x_slab);
+#ifdef COLD_CHAIN_NO_A   // timing experiment (results wrong): layer COLD_CHAIN_NO_A's A operand is not loaded
+            if (l == COLD_CHAIN_NO_A) {
+              if (leader) mbar_expect_tx(&full[s], 2 * (bhalf * BK * 2));
+            } else
+#endif
+            {
+              if (leader) mbar_expect_tx(&full[s], 2 * (C_A_BYTES + bhalf * BK * 2));
+              tma_load_a_pair(sA + s * C_A_BYTES, tA[l], &full[s], kb, mrow, l == 0 ? pol_x : pol_a, l == 0 && cp.x_slab);
+            }
           }
           tma_load_2d_pair(sB + s * C_B_BYTES, tB[l], &full[s], kb * BK, nb * tn[l] + (int)rank * bhalf, pol_b);
           if (++s == C_STAGES) { s = 0; ph ^= 1; }
@@ -378,8 +385,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           bias = nullptr;
         }
         const float* slope = l == 0 ? cp.s1 : (l == 1 ? cp.s2 : cp.s3);
+#ifdef COLD_CHAIN_EPI_DBG   // timing experiment (results wrong): epi.cuh debug mode for one layer's epilogue
+        const int edbg = l == COLD_CHAIN_EPI_DBG_L ? COLD_CHAIN_EPI_DBG : 0;
+#else
+        constexpr int edbg = 0;
+#endif
         epi_store_wide<BF16>(tbase, h * half, (h + 1) * half, bias, bias_s, u1row, 1, sOut + h * EPI_GROUP_BOX, tC[l],
-                             nb * tn[l], trow0, q, h, lane, 0, cp.instr ? cp.instr + 16 + 8 * l : nullptr,
+                             nb * tn[l], trow0, q, h, lane, edbg, cp.instr ? cp.instr + 16 + 8 * l : nullptr,
                              (FC1_DIRECT && l == 0) ? const_cast<void*>(cp.h1) : nullptr, cp.n1, M, 0ull, slope, C_OUT_BOXES == 2 * C_GROUPS ? sOut + (C_GROUPS + h) * EPI_GROUP_BOX : nullptr,
                              &box_ctr);
       }
