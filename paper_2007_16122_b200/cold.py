@@ -36,7 +36,7 @@ PROF_CHAIN, PROF_TAIL, PROF_MLP_F32 = 20, 21, 22
 # cold_config.kernel_flags (include/cold.h COLD_K_*)
 K_LAYERWISE, K_NO_U1_MMA, K_SINGLE_CTA, K_PAIR_STREAM, K_STREAM_B = 1, 2, 4, 8, 16
 K_TAIL_NONE, K_TAIL3, K_CHAIN_TAIL, K_SERIAL_USER, K_NO_PDL, K_X_ROWS = 32, 64, 128, 256, 512, 1024
-K_LAT_TAIL45, K_LAT_FC2_256, K_LAT_CHAIN = 2048, 4096, 8192
+K_LAT_TAIL45, K_LAT_FC2_256 = 2048, 4096
 
 
 class ColdError(RuntimeError):

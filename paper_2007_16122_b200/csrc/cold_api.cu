@@ -118,8 +118,6 @@ struct cold_ctx {
   // small calls also run FC2 as 128-wide pair tiles (twice the CTA pairs of the 256-wide tiles)
   bool lat_fc2_128 = false;
   CUtensorMap tmW2q;                 // W2 with 64-row boxes (half of a 128-wide pair tile)
-  // small calls: the whole FC stack in one launch of 8-CTA clusters (kernels_latchain.cu)
-  bool latchain = false;
   std::vector<CUtensorMap> tmOH;     // per chunk slot of the span
   int gspan = 1;                     // chunks per column-wise gather pass (X_ac holds gspan * chunk rows)
   int gather_ring = 0;               // > 0: cross-bag columns through a cp.async ring of this depth
@@ -585,12 +583,6 @@ extern "C" cold_status cold_create(const cold_config* cfg, cold_ctx** out) {
     c->lat_tail3 = !c->chain_tail && !c->prelu && !(c->kflags & COLD_K_LAT_TAIL45) &&
                    tail_supported(c->widths[2], c->widths[3], c->widths[4], c->widths[1]);
     c->lat_fc2_128 = c->lat_tail3 && c->widths[1] % 128 == 0 && !(c->kflags & COLD_K_LAT_FC2_256);
-    // (COLD_K_LAT_CHAIN: measured slower, 81 vs 61 us p50 per 4000-ad request: at most 15 clusters of 8
-    // CTAs are co-resident, so the 16th 256-row block runs as a second wave, and one block's FC1 -> FC2 ->
-    // FC3-FC5 path through four pairs takes ~27 us, longer than the three layer launches together)
-    c->latchain = c->lat_fc2_128 && !c->dense_se && (c->kflags & COLD_K_LAT_CHAIN) &&
-                  latchain_supported(c->widths[0], c->widths[1], c->widths[2], c->widths[3], c->widths[4], c->d_ac_pad) &&
-                  c->widths[5] <= 2;
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess ||
       [&] {   // the user kernel is on the latency path's critical chain: highest stream priority
@@ -869,7 +861,7 @@ extern "C" cold_status cold_load_params(cold_ctx* c, const cold_params* p, uint6
         s = make_tmap(&c->tmW2q, c->d_w[l], c->precision, Kp, out, 64);
         if (s) return s;
       }
-      if ((c->chain_tail || c->latchain) && (l == 3 || l == 4)) {   // half-N boxes for the chains' pair tiles
+      if (c->chain_tail && (l == 3 || l == 4)) {   // half-N boxes for the chain's pair tiles
         s = make_tmap(l == 3 ? &c->tmW4h : &c->tmW5h, c->d_w[l], c->precision, Kp, out, out / 2);
         if (s) return s;
       }
@@ -1240,35 +1232,6 @@ static void run_network(cold_ctx* c, int64_t a0, int64_t n, int xslot, float* sc
 #endif
   // small calls: FC1, FC2 as pair GEMMs, then FC3 -> FC4 -> FC5 -> head in the one-CTA tail kernel
   const bool lat3 = c->lat_tail3 && n_gemm == c->L - 1 - c->n_tail && n < c->chain_min;
-  if (lat3 && c->latchain) {   // ... or all of it in one launch of 8-CTA clusters
-    ChainParams cp;
-    memset(&cp, 0, sizeof(cp));
-    cp.b2 = c->d_b[1];
-    cp.b3 = c->d_b[2];
-    cp.x_slab = c->x_slab ? 1 : 0;
-    cp.u1 = c->d_u1;
-    cp.ld_u1 = c->widths[0];
-    cp.req_of_ad = c->d_req;
-    cp.a0 = a0;
-    cp.n1 = c->widths[0];
-    cp.n2 = c->widths[1];
-    cp.n3 = c->widths[2];
-    cp.k1 = c->d_ac_pad;
-    cp.n4 = c->widths[3];
-    cp.n5 = c->widths[4];
-    cp.b4 = c->d_b[3];
-    cp.b5 = c->d_b[4];
-    cp.head_w = c->d_head_w;
-    cp.head_b = c->d_head_b;
-    cp.head_n = c->widths[5];
-    cp.scores = scores_out;
-    const CUtensorMap* tm[12] = {&c->tmAX[xslot], &c->tmB[0], &c->tmW2q, &c->tmB[2], &c->tmW4h, &c->tmW5h,
-                                 &c->tmA[1], &c->tmA[2], &c->tmC[0], &c->tmC[1], &c->tmOH[xslot], &c->tmU1T};
-    c->mark_begin(st);
-    launch_latchain(tm, (int)n, c->precision == COLD_BF16 ? 1 : 0, cp, c->pdl && !c->prof, st);
-    c->mark_end(COLD_PROF_CHAIN, st, c->layer_flop(0, c->L, n));
-    return;
-  }
   if (lat3) n_gemm = c->L - 4;
   for (int l = 0; l < n_gemm; l++) {
     EpiParams ep;

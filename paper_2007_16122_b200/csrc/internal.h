@@ -213,12 +213,6 @@ struct ChainParams {
                                          // hready, [2] MMA full, [3] MMA tempty, [4] MMA uxfull, [5] epi tfull
 };
 bool chain_supported(int n1, int n2, int n3, int k1);
-// small calls: the whole FC stack in one launch of 8-CTA clusters (kernels_latchain.cu)
-bool latchain_supported(int n1, int n2, int n3, int n4, int n5, int k1);
-// tm: X (slot), W1, W2 (64-row boxes), W3, W4 half-box, W5 half-box, H1 / H2 (load maps), H1 / H2 (store
-// maps), one-hot (slot), u1 terms
-cudaError_t launch_latchain(const CUtensorMap* tm[12], int M, int bf16, const ChainParams& cp, bool pdl,
-                            cudaStream_t s);
 bool chain_tail_supported(int n4, int n5, int n3);
 // tm: X (slot), W1, W2, W3, H1, H2, H3, one-hot (slot), u1 terms, W4 half-box, W5 half-box, H4
 cudaError_t launch_chain(const CUtensorMap* tm[12], int M, int bf16, const ChainParams& cp, int num_sms, bool pdl,

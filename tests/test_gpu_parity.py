@@ -127,8 +127,7 @@ _KV = {"tail45": {}, "tail3": {"kernel_flags": 64}, "no_tail": {"kernel_flags": 
        "chain_tail": {"kernel_flags": 128, "chain_min_ads": 1}, "layerwise_pair_stream": {"kernel_flags": 1 | 8},
        "layerwise_no_u1mma": {"kernel_flags": 1 | 2}, "serial_user_no_pdl": {"kernel_flags": 256 | 512},
        "x_rows": {"kernel_flags": 1024}, "x_rows_layerwise": {"kernel_flags": 1024 | 1},
-       "lat_tail45": {"kernel_flags": 2048}, "lat_fc2_256": {"kernel_flags": 4096},
-       "lat_chain": {"kernel_flags": 8192}}
+       "lat_tail45": {"kernel_flags": 2048}, "lat_fc2_256": {"kernel_flags": 4096}}
 
 
 @pytest.mark.parametrize("variant", sorted(_KV))
