@@ -54,8 +54,18 @@ constexpr int C_OUT_BYTES = C_OUT_BOXES * EPI_GROUP_BOX;
 constexpr int C_UXA = BM * 32, C_UXB = (C_BN / 2) * 16 * 4, C_UX_BUF = C_UXA + C_UXB, C_NUX = 2;
 constexpr int C_BIASF = 1024;                          // FC2 + FC3 biases staged in smem (n2 + n3 <= 1024)
 constexpr int C_BIAS_BYTES = C_BIASF * 4;
-constexpr int C_STAGES = (232448 - C_OUT_BYTES - C_NUX * C_UX_BUF - 1024 - 512 - C_BIAS_BYTES) / C_STAGE_BYTES;
-constexpr int C_SMEM = C_STAGES * C_STAGE_BYTES + C_OUT_BYTES + C_NUX * C_UX_BUF + 1024 + 512 + C_BIAS_BYTES;
+// FC1's first XRES_KB k-blocks of the block's X rows stay resident for its n-tiles (loaded once per block
+// instead of once per n-tile: 10 instead of 16 X k-block loads per block); the ring gives up the stage this
+// takes (4 stages measured as fast as 5). Chain 277.2 vs 278.3 us per chunk, whole step +1%
+// (profiles/r03/ab_xr_*.jsonl). -DCOLD_CHAIN_XRES_KB=0 restores the re-load per n-tile.
+#ifdef COLD_CHAIN_XRES_KB
+constexpr int XRES_KB = COLD_CHAIN_XRES_KB;
+#else
+constexpr int XRES_KB = 2;
+#endif
+constexpr int C_X_BYTES = XRES_KB * C_A_BYTES;
+constexpr int C_STAGES = (232448 - C_OUT_BYTES - C_NUX * C_UX_BUF - 1024 - 512 - C_BIAS_BYTES - C_X_BYTES) / C_STAGE_BYTES;
+constexpr int C_SMEM = C_STAGES * C_STAGE_BYTES + C_OUT_BYTES + C_NUX * C_UX_BUF + 1024 + 512 + C_BIAS_BYTES + C_X_BYTES;
 static_assert(C_STAGES >= 4, "chain kernel pipeline depth");
 
 // debug: cycles a role spent blocked in a barrier wait (cp.instr != null)
@@ -85,7 +95,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   uint8_t* sB = sA + C_STAGES * C_A_BYTES;
   uint8_t* sOut = smem + C_STAGES * C_STAGE_BYTES;
   uint8_t* sUX = sOut + C_OUT_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sUX + C_NUX * C_UX_BUF);
+  uint8_t* sX = sUX + C_NUX * C_UX_BUF;           // XRES_KB resident X k-blocks of the block (FC1)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + C_X_BYTES);
   uint64_t* full = bars;                          // leader: A+B bytes of both CTAs
   uint64_t* empty = full + C_STAGES;              // both: released by the leader's pair commit
   uint64_t* tfull = empty + C_STAGES;             // both: accumulator ready [2]
@@ -94,7 +105,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
   uint64_t* uxempty = uxfull + C_NUX;             // both: u1 MMA of the buffer's last FC1 tile done [C_NUX]
   uint64_t* hready = uxempty + C_NUX;             // local: [l] block of layer l's output stored (H1..H4)
   uint64_t* h1t = hready + 4;                     // local: [nb] FC1 n-tile nb of the block stored (H1_TILES)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(h1t + 4);
+  uint64_t* xfull = h1t + 4;                      // leader: both CTAs' resident X k-blocks landed
+  uint64_t* xempty = xfull + 1;                   // both: the block's last FC1 MMAs done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xempty + 1);
   // FC2 / FC3 biases in shared memory: the epilogue reads them with LDS instead of a global load that
   // stalled it (ncu r01h: 9% of the chain's stall samples on the bias add)
   float* sBias = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 512);
@@ -157,6 +170,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
     for (int s = 0; s < C_NUX; s++) { mbar_init(&uxfull[s], 1); mbar_init(&uxempty[s], 1); }
     for (int i = 0; i < 4; i++) mbar_init(&hready[i], C_EPI_WARPS);
     for (int i = 0; i < 4; i++) mbar_init(&h1t[i], C_EPI_WARPS);
+    mbar_init(xfull, 1);
+    mbar_init(xempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const CUtensorMap* maps[12] = {&tmX, &tmW1, &tmW2, &tmW3, &tmH1, &tmH2, &tmH3, &tmOH, &tmU1T, &tmW4, &tmW5, &tmH4};
     for (int i = 0; i < (TAIL ? 12 : 9); i++) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)maps[i]) : "memory");
@@ -187,7 +202,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       const uint64_t pol_x = policy_evict_first();  // X: read once
       const uint64_t pol_a = policy_evict_last();   // H1 / H2: read while hot, then discarded
       const uint64_t pol_b = policy_evict_last();   // weights: re-read by every block
-      int s = 0, fc1_t = 0;
+      int s = 0, fc1_t = 0, x_t = 0;
       uint32_t ph = 0;
       const bool ins = cp.instr != nullptr;
       unsigned long long w_empty = 0, w_hready = 0;
@@ -198,13 +213,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           if (nb == 0) cwait(&hready[l - 1], (uint32_t)(j & 1), w_hready, ins);   // own rows of the input
         }
         const int bhalf = tn[l] / 2;                  // weight rows this CTA stages (half the tile N)
+        const int xres = l == 0 ? min(XRES_KB, kbs[0]) : 0;
+        if (xres > 0 && nb == 0) {   // the block's resident X k-blocks, once for its FC1 n-tiles
+          cwait(xempty, (uint32_t)(x_t & 1) ^ 1, w_empty, ins);
+          if (leader) mbar_expect_tx(xfull, 2 * xres * C_A_BYTES);
+          for (int kb = 0; kb < xres; kb++)
+            tma_load_a_pair(sX + kb * C_A_BYTES, tA[0], xfull, kb, mrow, pol_x, cp.x_slab);
+          x_t++;
+        }
         for (int kb = 0; kb < kbs[l]; kb++) {
           // FC2 reads H1 one FC1 n-tile (C_BN columns) at a time: wait for that tile's stores only, so FC2(j)
           // starts on the first tiles of H1(j) while the last FC1 tile is still draining
           if (H1_TILES && l == 1 && (kb * BK) % C_BN == 0)
             cwait(&h1t[(kb * BK) / C_BN], (uint32_t)(j & 1), w_hready, ins);
           cwait(&empty[s], ph ^ 1, w_empty, ins);
-          if (TAIL && l >= 3) {   // FC4 / FC5: A is in TMEM, only the weight half streams
+          if ((TAIL && l >= 3) || kb < xres) {   // FC4 / FC5: A in TMEM; FC1: A resident: only the weights
             if (leader) mbar_expect_tx(&full[s], 2 * (bhalf * BK * 2));
           } else {
 #ifdef COLD_CHAIN_NO_A   // timing experiment (results wrong): layer COLD_CHAIN_NO_A's A operand is not loaded
@@ -243,7 +266,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
       constexpr uint32_t id256 = idesc_pair<C_BN, BF16>();
       const uint32_t id_tail[2] = {cp.n4 == 128 ? idesc_pair<128, BF16>() : idesc_pair<64, BF16>(),
                                    cp.n5 == 64 ? idesc_pair<64, BF16>() : idesc_pair<32, BF16>()};
-      int s = 0, fc1_t = 0, uses0 = 0, uses1 = 0;
+      int s = 0, fc1_t = 0, uses0 = 0, uses1 = 0, x_t = 0;
       uint32_t ph = 0;
       const bool ins = cp.instr != nullptr;
       unsigned long long w_full = 0, w_tempty = 0, w_ux = 0, wl_full[3] = {0, 0, 0}, wl_te[3] = {0, 0, 0};
@@ -256,10 +279,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
         const uint32_t bufc = tmem_base + acc * C_BN;
         // TAIL in place: acc4 at column 128, acc5 at 64; their A (H3 / H4) from column 0 of the same buffer
         const uint32_t d = (TAIL && l == 3) ? bufc + 128 : ((TAIL && l == 4) ? bufc + 64 : bufc);
+        const int xres = l == 0 ? min(XRES_KB, kbs[0]) : 0;
+        if (xres > 0 && nb == 0) {
+          cwait(xfull, (uint32_t)(x_t & 1), w_full, ins);
+          tc_fence_after();
+        }
         for (int kb = 0; kb < kbs[l]; kb++) {
           cwait(&full[s], ph, w_full, ins);
           tc_fence_after();
-          const uint64_t ad = sdesc_sw128(smem_u32(sA + s * C_A_BYTES));
+          uint8_t* a_tile = kb < xres ? sX + kb * C_A_BYTES : sA + s * C_A_BYTES;
+          const uint64_t ad = sdesc_sw128(smem_u32(a_tile));
           const uint64_t bd = sdesc_sw128(smem_u32(sB + s * C_B_BYTES));
 #pragma unroll
           for (int kk = 0; kk < BK / UMMA_K; kk++) {
@@ -268,7 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
                                (kb | kk) != 0);
               continue;
             }
-            const uint64_t a_kk = (l == 0 && cp.x_slab) ? sdesc_k16_plain(smem_u32(sA + s * C_A_BYTES) + kk * BM * 32)
+            const uint64_t a_kk = (l == 0 && cp.x_slab) ? sdesc_k16_plain(smem_u32(a_tile) + kk * BM * 32)
                                                          : ad + (uint64_t)(kk * 2);
             umma_f16_pair(d, a_kk, bd + (uint64_t)(kk * 2), idesc, (kb | kk) != 0);
           }
@@ -285,6 +314,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C_THREADS, 1)
           if (BF16) umma_f16_pair(d, adx, sdesc_k16_plain(ux + C_UXA + 2 * (C_BN / 2) * 16), id256, 1u);
           umma_commit_pair(&uxempty[b]);
           fc1_t++;
+          if (XRES_KB > 0 && nb == ntile[0] - 1) {   // the block's FC1 MMAs are issued: X buffer free once done
+            umma_commit_pair(xempty);
+            x_t++;
+          }
         }
         umma_commit_pair(&tfull[acc]);
         if (ins && l < 3) { wl_full[l] += w_full - fu0; wl_te[l] += w_tempty - te0; }
