@@ -142,6 +142,25 @@ def test_kernel_variants_match_oracle(variant):
 
 
 @pytest.mark.parametrize("prec", ["f16", "bf16"])
+@pytest.mark.parametrize("flags", [0, 2048, 4096, 128])
+def test_latency_path_single_request(prec, flags):
+    """One configs[1]-shaped request (1 user x 4000 ads, below chain_min_ads: the latency path, user kernel
+    forked beside the gather) + top-500: FC1 / FC2 pair GEMMs (FC2 128-wide) and the FC3-FC5 tail kernel with
+    H3 / H4 as TMEM operands (flags 0), FC3 pair GEMM + tail45 (2048), FC2 256-wide (4096), the chain-tail
+    build, which also routes small calls to FC3 pair GEMM + tail45 (128) -- scores vs the oracle, top-K vs
+    the oracle's order of the same keys (AMB-13)."""
+    sch, params, batch = small_case("paper", R=1, n_ads=(4000,), precision=prec, cap=50000, seed=91)
+    ctx = make_ctx(sch, params, max_requests=4, kernel_flags=flags)
+    p, z = _oracle_scores(sch, params, batch)
+    got = gpu_scores(ctx, batch)
+    _check_scores(got, p, z, prec, f"latency path {prec} flags {flags}")
+    idx, key = gpu_topk(ctx, got, batch.ad_offsets, 500)
+    oidx, _ = oracle.topk_batch(got.astype(np.float64), batch.ad_offsets, 500)
+    np.testing.assert_array_equal(idx, oidx)
+    ctx.close()
+
+
+@pytest.mark.parametrize("prec", ["f16", "bf16"])
 def test_chain_kernel_many_blocks(prec):
     """The FC1->FC3 chain kernel (forced for every chunk size) over several chunks of 1280 ads with many
     256-row blocks per CTA pair, requests crossing block boundaries, a ragged last block."""
